@@ -1,0 +1,35 @@
+"""CPU fp64 oracle for the hot path of arXiv 2306.13618 — TEST INFRASTRUCTURE ONLY.
+
+This package is the plain, slow, obviously-correct reference that the CUDA path is
+checked against.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import it.  The product package
+(``paper_2306_13618_b200``) never imports, links or executes anything in here, and
+this package never imports the product: the two share no code.
+
+What is computed, and where it comes from (``P:n`` = line n of the paper text
+``PAPER.md``; ``S:n`` = line n of ``SPEC.md``):
+
+* ``kernels``     — radial kernels K^Gauss, K^IMQ of Eq. (4.2) in the
+                    config form exp(-r^2/eps) and (r^2+c^2)^(-1/2).
+* ``direct``      — the kernel sum (4.3) by its plain definition, an
+                    O(n m) double loop vectorised over blocks of targets.
+* ``sinkhorn``    — Algorithm 1 step by step: updates (3.3)/(3.4)
+                    with dense direct sums, the plan recovery of P:488, the dual
+                    (3.1) and the discrete primal.
+* ``mmd``         — the discrete MMD^2 of Eq. (3.5), V-statistic form.
+
+Every function is pinned by ``tests/test_oracle_pins.py`` against closed forms,
+brute force and invariants that do not reuse the oracle's own formulas (see
+DESIGN.md "Oracle pins").  No function here is "parity unpinned".
+"""
+
+from .kernels import gauss, imq, kernel_fn  # noqa: F401
+from .direct import kernel_sum_direct  # noqa: F401
+from .sinkhorn import (  # noqa: F401
+    uot_sinkhorn_direct,
+    dual_objective,
+    primal_objective_dense,
+    primal_objective_marginals,
+    SinkhornResult,
+)
+from .mmd import mmd2_direct, mmd2_combined  # noqa: F401

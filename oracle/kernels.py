@@ -1,0 +1,30 @@
+"""Radial kernels of the paper, fp64 (TEST INFRASTRUCTURE ONLY — see oracle/__init__.py).
+
+Paper Eq. (4.2):  K^Gauss(y) = exp(-||y||^2 / l^2),  K^IMQ(y) = 1/sqrt(||y||^2 + c^2).
+Table 1 uses the same forms.  The configs (BASELINE.json) write the
+Gaussian as exp(-||x-y||^2 / eps), i.e. ``param = eps = l^2``; the IMQ ``param`` is c.
+"""
+
+import numpy as np
+
+GAUSS = 0
+IMQ = 1
+
+
+def gauss(r2, eps):
+    """exp(-r^2/eps) from the squared distance r2 (Eq. 4.2, with l^2 = eps)."""
+    return np.exp(-np.asarray(r2, dtype=np.float64) / eps)
+
+
+def imq(r2, c):
+    """(r^2 + c^2)^(-1/2) from the squared distance r2 (Eq. 4.2)."""
+    return 1.0 / np.sqrt(np.asarray(r2, dtype=np.float64) + c * c)
+
+
+def kernel_fn(kind, param):
+    """Return K as a function of the squared distance."""
+    if kind == GAUSS:
+        return lambda r2: gauss(r2, param)
+    if kind == IMQ:
+        return lambda r2: imq(r2, param)
+    raise ValueError(f"unknown kernel kind {kind!r}")
