@@ -1,0 +1,191 @@
+/*
+ * uotk.h — C ABI of the B200 fast radial-kernel library for arXiv 2306.13618
+ * ("Unbalanced Optimal Transport and Maximum Mean Discrepancies: Interconnections
+ * and Rapid Evaluation", Lakshmanan & Pichler).
+ *
+ * Citations: "P:n" = line n of the paper text, with its section /
+ * equation / algorithm; "S:n" = line n of SPEC.md (interfaces only, not binding).
+ *
+ * The library evaluates the radial-kernel product K v, K_ij = k(||x_i - y_j||),
+ * by NFFT-based fast summation (Sec. 4; factorisation (4.5)-(4.6),
+ * P:590-592) or by a direct O(n m) sum (Eq. 4.3), and uses it inside the
+ * entropic unbalanced-OT Sinkhorn iteration (Algorithm 2) and the
+ * MMD^2 sums (Eq. 3.5).  Every step runs in hand-written sm_100a kernels;
+ * cuFFT provides the equispaced FFT of (4.6).
+ *
+ * Conventions shared by all entry points
+ * --------------------------------------
+ *  - Points are row-major n x d arrays of double (x in R^{n x d}, Alg. 2 input,
+ *    P:616), d in {1, 2, 3} (the paper restricts to d <= 3).
+ *  - Every array argument may be DEVICE memory (cudaMalloc / torch cuda tensor)
+ *    or HOST memory (pinned or pageable); the library detects which with
+ *    cudaPointerGetAttributes.  Host inputs are copied to device workspaces and
+ *    host outputs copied back, all on `cuda_stream`.  All arrays are caller-owned;
+ *    the library never retains a pointer after the call returns.
+ *  - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *    enqueued on it.  Calls that return host scalars (uot result, mmd2) or write
+ *    host outputs synchronise the stream before returning; a call with only
+ *    device outputs returns without synchronising.
+ *  - Outputs are in the CALLER's point order (the library sorts internally).
+ *  - `opts` may be NULL (defaults, see uotk_opts_init).
+ *  - `comm` is a uotk_comm created by uotk_comm_create, or NULL for one GPU.
+ *    With a communicator every rank passes its LOCAL shard of the points; the
+ *    oversampled Fourier coefficients of each kernel sum are summed over ranks
+ *    (NCCL all-reduce) so each rank obtains the sums at its own targets from
+ *    all ranks' sources.  Scalar results (uot result, mmd2) are global and
+ *    identical on all ranks.
+ *  - Return value: UOTK_OK (0) or a negative status; uotk_last_error() returns a
+ *    thread-local description of the last failure.  No C++ exception crosses
+ *    the ABI.  Not re-entrant on one device from several host threads.
+ */
+#ifndef UOTK_H
+#define UOTK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UOTK_ABI_VERSION 1
+
+/* Status codes (mirroring SPEC's split of input vs numeric errors). */
+enum {
+    UOTK_OK = 0,
+    UOTK_EINVAL = -1,       /* null pointer, d not in {1,2,3}, negative size, eps/lam/param <= 0, bad opts */
+    UOTK_EDOMAIN = -2,      /* non-finite coordinate, or (UOT) a mass <= 0 or non-finite (KL needs mu_i > 0) */
+    UOTK_EOVERFLOW = -3,    /* non-finite or non-positive intermediate t, u, v in Sinkhorn */
+    UOTK_ENOMEM = -4,       /* device allocation failed */
+    UOTK_ECUDA = -5,        /* CUDA runtime / kernel error */
+    UOTK_ECUFFT = -6,       /* cuFFT error */
+    UOTK_ENCCL = -7,        /* NCCL error or NCCL library not loadable */
+    UOTK_EUNSUPPORTED = -8  /* parameter combination the library does not support (e.g. grid too large) */
+};
+
+/* Radial kernels of Eq. (4.2), P:560 (Table 1), as functions of r = ||x - y||:
+ *   UOTK_GAUSS: k(r) = exp(-r^2 / param)          (param = l^2 = eps in the configs' form)
+ *   UOTK_IMQ:   k(r) = 1 / sqrt(r^2 + param^2)    (param = c)                            */
+typedef enum { UOTK_GAUSS = 0, UOTK_IMQ = 1 } uotk_kernel_kind;
+
+/* Evaluation method.  AUTO picks DIRECT when n_src * n_tgt is below a measured
+ * crossover and NFFT otherwise. */
+typedef enum { UOTK_AUTO = 0, UOTK_NFFT = 1, UOTK_DIRECT = 2 } uotk_method;
+
+/* Fast-summation parameters (Rem. 4.4 P:612 and footnote P:653 leave them to the
+ * implementation; defaults and auto rules are in DESIGN.md "Parameters").
+ * A zero field means "automatic / default". */
+typedef struct {
+    int32_t method;   /* uotk_method                                                     */
+    int32_t N;        /* bandwidth per axis of I_N (Eq. 4.4), even; 0 = auto       */
+    double sigma;     /* oversampling: grid n_g = sigma * N per axis (even); 0 = 2.0      */
+    int32_t m;        /* window half-width; 2m taps per axis (footnote P:653); 0 = 8      */
+    int32_t p;        /* IMQ boundary polynomial order (K_B); 0 = 12          */
+    double eps_B;     /* IMQ boundary band width in torus units; 0 = auto                 */
+    double h;         /* torus scaling h (Eq. 4.7, Rem. 4.3 P:610); 0 = auto        */
+    double tol;       /* target truncation tolerance of the auto rules; 0 = 1e-16        */
+    int32_t flags;    /* reserved, must be 0                                             */
+    int32_t reserved; /* must be 0                                                       */
+} uotk_opts;
+
+/* What a call actually used (any pointer to it may be NULL). */
+typedef struct {
+    int32_t method_used; /* UOTK_NFFT or UOTK_DIRECT */
+    int32_t N;           /* bandwidth (0 for DIRECT) */
+    int32_t n_grid;      /* oversampled grid points per axis (0 for DIRECT) */
+    int32_t m;           /* window half-width (0 for DIRECT) */
+    double h;            /* torus scaling (0 for DIRECT) */
+} uotk_info;
+
+/* Result of uotk_uot_sinkhorn, all global over ranks.
+ * Objective values of the plan pi = e^{lam beta} k e^{lam gamma} (.) (mu x nu) recovered
+ * from the final potentials, lam = 1/eps:
+ *   primal     discrete primal of (2.9), via the plan's marginals
+ *   dual       dual function (3.1) of Theorem 3.1
+ *   plan_mass  pi(X x X) = sum_i p_i
+ *   mass_a     mu(X);  mass_b  nu(X)
+ *   max_dbeta, max_dgamma   sup-norm change of beta / gamma in the last iteration */
+typedef struct {
+    double primal;
+    double dual;
+    double plan_mass;
+    double mass_a;
+    double mass_b;
+    double max_dbeta;
+    double max_dgamma;
+    int32_t iters;
+    int32_t reserved;
+    uotk_info info;
+} uotk_uot_result;
+
+/* Fill *opts with the defaults (all automatic). */
+void uotk_opts_init(uotk_opts* opts);
+
+/*
+ * Kernel sum, Eq. (4.3):
+ *     out_i = sum_j k(||tgt_i - src_j||) alpha_j ,   i < n_tgt.
+ * src: n_src x d, alpha: n_src (any sign), tgt: n_tgt x d, out: n_tgt.
+ * n_src = 0 gives out = 0; n_tgt = 0 is a no-op.
+ * NFFT path: adjoint NFFT of alpha at src (window spreading), FFT, multiplication
+ * by the regularised kernel's Fourier coefficients b_k (Eq. 4.4-4.6), inverse FFT,
+ * interpolation at tgt.  With `comm`, src/alpha/tgt/out are local shards.
+ */
+int uotk_kernel_sum(int d, int64_t n_src, const double* src, const double* alpha,
+                    int64_t n_tgt, const double* tgt, int kind, double param,
+                    double* out, const uotk_opts* opts, uotk_info* info,
+                    void* comm, void* cuda_stream);
+
+/*
+ * Entropic unbalanced OT by Sinkhorn iterations, Algorithm 2 / Algorithm 1
+ * with the Gibbs kernel k_ij = exp(-||x_i - y_j||^2 / eps) (r = 2).
+ *   x: n x d, a: n masses (mu_i > 0);  y: m x d, b: m masses (nu_j > 0)
+ *   eps   entropic regularisation = 1/lambda of the paper (Def. 2.7)
+ *   lam1, lam2   marginal KL penalties eta_1, eta_2 (configs use lam1 = lam2)
+ *   iters        number of iterations; one iteration = the beta-step (3.3) followed by
+ *                the gamma-step (3.4), i.e. two kernel sums; iters >= 0
+ *   gamma_init   starting gamma^0 (m values) or NULL for gamma^0 = 0
+ *   beta, gamma  outputs: final dual potentials (n and m values)
+ *   res          output: objective values (see uotk_uot_result); may be NULL
+ * With iters = 0 the outputs are beta = 0, gamma = gamma^0.
+ */
+int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a,
+                      int64_t m, const double* y, const double* b,
+                      double eps, double lam1, double lam2, int iters,
+                      const double* gamma_init, double* beta, double* gamma,
+                      uotk_uot_result* res, const uotk_opts* opts,
+                      void* comm, void* cuda_stream);
+
+/*
+ * MMD^2 of Eq. (3.5), V-statistic (diagonal terms included):
+ *   sum_ij a_i a_j k(x_i,x_j) - 2 sum_ij a_i b_j k(x_i,y_j) + sum_ij b_i b_j k(y_i,y_j)
+ * evaluated as one quadratic form over z = x u y with weights w = (a, -b).
+ * x: n x d, a: n;  y: m x d, b: m (any sign);  *mmd2: host double (output).
+ */
+int uotk_mmd2(int d, int64_t n, const double* x, const double* a,
+              int64_t m, const double* y, const double* b, int kind, double param,
+              double* mmd2, const uotk_opts* opts, uotk_info* info,
+              void* comm, void* cuda_stream);
+
+/* Multi-GPU communicator (one process per GPU).  uotk_comm_unique_id fills 128
+ * bytes on one rank; broadcast them (e.g. with torch.distributed) and call
+ * uotk_comm_create on every rank with the current CUDA device set.  NCCL is
+ * loaded at run time (libnccl.so.2); UOTK_ENCCL if it cannot be. */
+int uotk_comm_unique_id(void* id128);
+int uotk_comm_create(const void* id128, int nranks, int rank, void** comm_out);
+int uotk_comm_destroy(void* comm);
+
+/* Thread-local description of the last error (never NULL). */
+const char* uotk_last_error(void);
+
+/* Returns UOTK_ABI_VERSION. */
+int uotk_abi_version(void);
+
+/* Number of this library's kernels launched by the calling thread since the last
+ * reset (bench.py's "gpu_launches"); uotk_launch_counter_reset sets it to 0. */
+int64_t uotk_launch_counter(void);
+void uotk_launch_counter_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UOTK_H */

@@ -1,0 +1,247 @@
+"""B200-native fast radial-kernel sums for unbalanced OT and MMD (arXiv 2306.13618).
+
+Python surface of the C ABI in ``include/uotk.h``: three operations with the same
+names as the C entry points, marshalling arguments only.
+
+* :func:`kernel_sum`   — s_i = sum_j k(||tgt_i - src_j||) alpha_j       (Eq. 4.3)
+* :func:`uot_sinkhorn` — entropic UOT by Sinkhorn, Algorithm 2
+* :func:`mmd2`         — MMD^2 of Eq. (3.5)
+
+Arrays may be torch tensors (CUDA or CPU) or numpy arrays, float64 and contiguous;
+points are row-major (n, d).  Outputs are allocated like the inputs (CUDA tensors for
+CUDA inputs, host arrays otherwise — the library then stages the copies itself).
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._native import UotkError, UotkOpts, UotkInfo, UotkUotResult  # noqa: F401
+
+GAUSS = 0
+IMQ = 1
+AUTO, NFFT, DIRECT = 0, 1, 2
+_KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, GAUSS: GAUSS, IMQ: IMQ}
+_METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
+
+__all__ = ["kernel_sum", "uot_sinkhorn", "mmd2", "Comm", "UOTResult", "GAUSS", "IMQ", "UotkError",
+           "launch_counter", "reset_launch_counter", "library_path"]
+
+
+def library_path():
+    return _native.LIB_PATH
+
+
+def _torch():
+    try:
+        import torch
+        return torch
+    except ImportError:  # pragma: no cover
+        return None
+
+
+class _Arr:
+    """Pointer view of a caller array (torch tensor or numpy array), float64, contiguous."""
+
+    def __init__(self, a, name, ncols=None):
+        self.obj = a
+        torch = _torch()
+        if torch is not None and isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64:
+                raise TypeError(f"{name}: expected float64, got {a.dtype}")
+            if not a.is_contiguous():
+                raise ValueError(f"{name}: tensor must be contiguous")
+            self.is_torch = True
+            self.is_cuda = a.is_cuda
+            self.ptr = a.data_ptr() if a.numel() else None
+            self.shape = tuple(a.shape)
+        else:
+            a = np.asarray(a)
+            if a.dtype != np.float64:
+                raise TypeError(f"{name}: expected float64, got {a.dtype}")
+            if not a.flags.c_contiguous:
+                raise ValueError(f"{name}: array must be C-contiguous")
+            self.obj = a
+            self.is_torch = False
+            self.is_cuda = False
+            self.ptr = a.ctypes.data if a.size else None
+            self.shape = a.shape
+        if ncols is not None:
+            if len(self.shape) == 1 and ncols == 1:
+                self.shape = (self.shape[0], 1)
+            if len(self.shape) != 2 or self.shape[1] != ncols:
+                raise ValueError(f"{name}: expected shape (n, {ncols}), got {self.shape}")
+
+    @property
+    def n(self):
+        return self.shape[0]
+
+
+def _dim(points, name):
+    shp = points.shape if hasattr(points, "shape") else np.asarray(points).shape
+    if len(shp) == 1:
+        return 1
+    if len(shp) != 2:
+        raise ValueError(f"{name}: expected an (n, d) array")
+    return shp[1]
+
+
+def _like(ref, n):
+    """Allocate an output of n doubles like `ref` (CUDA tensor, CPU tensor or numpy)."""
+    torch = _torch()
+    if ref.is_torch:
+        return torch.empty(n, dtype=torch.float64, device=ref.obj.device)
+    return np.empty(n, dtype=np.float64)
+
+
+def _stream(stream, arrays):
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    torch = _torch()
+    if torch is not None and any(a.is_cuda for a in arrays):
+        return torch.cuda.current_stream().cuda_stream
+    return 0
+
+
+def _opts(opts):
+    o = UotkOpts()
+    _native.load().uotk_opts_init(ctypes.byref(o))
+    if opts:
+        for k, v in opts.items():
+            if k == "method":
+                v = _METHOD[v]
+            setattr(o, k, v)
+    return o
+
+
+def _comm_ptr(comm):
+    return None if comm is None else comm.handle
+
+
+def _info_dict(info):
+    return {"method": {1: "nfft", 2: "direct"}.get(info.method_used, "?"), "N": info.N,
+            "n_grid": info.n_grid, "m": info.m, "h": info.h}
+
+
+def kernel_sum(src, alpha, tgt, kind="gauss", param=None, opts=None, comm=None, stream=None, out=None,
+               return_info=False):
+    """s_i = sum_j k(||tgt_i - src_j||) alpha_j  (Eq. 4.3).  kind 'gauss': exp(-r^2/param);
+    'imq': (r^2 + param^2)^(-1/2).  opts: dict of uotk_opts fields (method='auto'|'nfft'|'direct')."""
+    lib = _native.load()
+    d = _dim(src, "src")
+    S, A, T = _Arr(src, "src", d), _Arr(alpha, "alpha"), _Arr(tgt, "tgt", d)
+    if A.shape != (S.n,):
+        raise ValueError("alpha must have shape (n_src,)")
+    if out is None:
+        out = _like(T, T.n)
+    O = _Arr(out, "out")
+    info = UotkInfo()
+    o = _opts(opts)
+    code = lib.uotk_kernel_sum(d, S.n, S.ptr, A.ptr, T.n, T.ptr, _KIND[kind], float(param), O.ptr,
+                               ctypes.byref(o), ctypes.byref(info), _comm_ptr(comm),
+                               _stream(stream, [S, A, T, O]))
+    _native.check(code)
+    return (O.obj, _info_dict(info)) if return_info else O.obj
+
+
+@dataclass
+class UOTResult:
+    primal: float
+    dual: float
+    plan_mass: float
+    mass_a: float
+    mass_b: float
+    max_dbeta: float
+    max_dgamma: float
+    iters: int
+    info: dict
+
+    @property
+    def uot_cost(self):
+        """UOT_{2;eta;lambda} value: the primal (2.9) at the final iterate (reading R3)."""
+        return self.primal
+
+
+def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, opts=None, comm=None, stream=None):
+    """Entropic UOT (Def. 2.7) by Algorithm 2: Gaussian Gibbs kernel exp(-|x-y|^2/eps),
+    eps = 1/lambda_paper, marginal penalties lam (= eta_1) and lam2 (= eta_2, default lam).
+    Returns (beta, gamma, UOTResult)."""
+    lib = _native.load()
+    d = _dim(x, "x")
+    X, A, Y, B = _Arr(x, "x", d), _Arr(a, "a"), _Arr(y, "y", d), _Arr(b, "b")
+    if A.shape != (X.n,) or B.shape != (Y.n,):
+        raise ValueError("masses must match the point counts")
+    G0 = _Arr(gamma_init, "gamma_init") if gamma_init is not None else None
+    beta = _like(X, X.n)
+    gamma = _like(Y, Y.n)
+    BO, GO = _Arr(beta, "beta"), _Arr(gamma, "gamma")
+    res = UotkUotResult()
+    o = _opts(opts)
+    lam2 = lam if lam2 is None else lam2
+    code = lib.uotk_uot_sinkhorn(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam), float(lam2),
+                                 int(iters), G0.ptr if G0 else None, BO.ptr, GO.ptr, ctypes.byref(res),
+                                 ctypes.byref(o), _comm_ptr(comm), _stream(stream, [X, A, Y, B, BO, GO]))
+    _native.check(code)
+    r = UOTResult(res.primal, res.dual, res.plan_mass, res.mass_a, res.mass_b, res.max_dbeta, res.max_dgamma,
+                  res.iters, _info_dict(res.info))
+    return BO.obj, GO.obj, r
+
+
+def mmd2(x, a, y, b, kind="gauss", param=None, opts=None, comm=None, stream=None, return_info=False):
+    """MMD^2 of Eq. (3.5) (V-statistic) between sum_i a_i delta_{x_i} and sum_j b_j delta_{y_j}."""
+    lib = _native.load()
+    d = _dim(x, "x")
+    X, A, Y, B = _Arr(x, "x", d), _Arr(a, "a"), _Arr(y, "y", d), _Arr(b, "b")
+    if A.shape != (X.n,) or B.shape != (Y.n,):
+        raise ValueError("weights must match the point counts")
+    val = ctypes.c_double(0.0)
+    info = UotkInfo()
+    o = _opts(opts)
+    code = lib.uotk_mmd2(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, _KIND[kind], float(param), ctypes.byref(val),
+                         ctypes.byref(o), ctypes.byref(info), _comm_ptr(comm), _stream(stream, [X, A, Y, B]))
+    _native.check(code)
+    return (val.value, _info_dict(info)) if return_info else val.value
+
+
+class Comm:
+    """Multi-GPU communicator (NCCL inside libuotk.so).  Create collectively on all ranks:
+    ``Comm.from_torch_distributed()`` broadcasts the NCCL unique id over the default
+    torch.distributed process group."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        lib = _native.load()
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        h = ctypes.c_void_p()
+        _native.check(lib.uotk_comm_create(buf, nranks, rank, ctypes.byref(h)))
+        self.handle = h.value
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _native.check(_native.load().uotk_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(obj[0], world, rank)
+
+    def close(self):
+        if self.handle:
+            _native.check(_native.load().uotk_comm_destroy(self.handle))
+            self.handle = None
+
+
+def launch_counter():
+    """Kernels this library launched on the calling thread since the last reset."""
+    return _native.load().uotk_launch_counter()
+
+
+def reset_launch_counter():
+    _native.load().uotk_launch_counter_reset()

@@ -1,0 +1,456 @@
+// The C ABI (include/uotk.h): validation, host/device staging, and the drivers of the
+// three operations — kernel sum (4.3), UOT Sinkhorn (Algorithm 2 / Algorithm 1) and
+// MMD^2 (3.5) — over the NFFT passes (nfft.cu, fused3d.cu) or the direct kernel (direct.cu).
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "reduce.cuh"
+
+namespace uotk {
+
+extern thread_local std::string g_last_error;
+extern thread_local int64_t g_launches;
+void comm_unique_id(void* id128);
+void* comm_create(const void* id128, int nranks, int rank);
+void comm_destroy(void* comm);
+void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);
+int comm_nranks(void* comm);
+void ensure_pool();
+
+// Optimised NFFT half-step for d = 3 (fused3d.cu); returns false if not applicable.
+bool fused3d_available(const FastParams& fp);
+void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
+                           const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s);
+
+namespace {
+
+// AUTO: below this many source-target pairs the direct kernel wins (measured).
+constexpr double kDirectCrossoverPairs = 4.0e7;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return UOTK_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("internal error: ") + e.what();
+        return UOTK_ECUDA;
+    } catch (...) {
+        g_last_error = "internal error";
+        return UOTK_ECUDA;
+    }
+}
+
+uotk_opts resolve(const uotk_opts* o) {
+    uotk_opts r;
+    memset(&r, 0, sizeof r);
+    if (o) r = *o;
+    if (r.flags != 0 || r.reserved != 0) fail(UOTK_EINVAL, "opts.flags / opts.reserved must be 0");
+    if (r.method < 0 || r.method > 2) fail(UOTK_EINVAL, "opts.method must be AUTO, NFFT or DIRECT");
+    if (r.N < 0 || r.m < 0 || r.p < 0 || r.sigma < 0 || r.eps_B < 0 || r.h < 0 || r.tol < 0 || r.tol >= 1)
+        fail(UOTK_EINVAL, "negative option value");
+    return r;
+}
+
+void need(bool ok, const char* msg) {
+    if (!ok) fail(UOTK_EINVAL, msg);
+}
+
+void check_points_arg(int d, int64_t n, const void* p, const char* what) {
+    if (n < 0) fail(UOTK_EINVAL, std::string(what) + ": negative size");
+    if (n > 0 && !p) fail(UOTK_EINVAL, std::string(what) + ": null pointer");
+    (void)d;
+}
+
+int pick_method(const uotk_opts& o, double pairs, void* comm) {
+    if (o.method == UOTK_DIRECT) {
+        if (comm && comm_nranks(comm) > 1) fail(UOTK_EUNSUPPORTED, "DIRECT method with a multi-rank communicator");
+        return UOTK_DIRECT;
+    }
+    if (o.method == UOTK_NFFT) return UOTK_NFFT;
+    if (comm && comm_nranks(comm) > 1) return UOTK_NFFT;
+    return pairs <= kDirectCrossoverPairs ? UOTK_DIRECT : UOTK_NFFT;
+}
+
+void fill_info(uotk_info* info, int method, const FastParams* fp) {
+    if (!info) return;
+    memset(info, 0, sizeof *info);
+    info->method_used = method;
+    if (fp) {
+        info->N = fp->N;
+        info->n_grid = fp->ng;
+        info->m = fp->m;
+        info->h = fp->h;
+    }
+}
+
+struct NfftSetup {
+    FastParams fp;
+    SpectralPlan sp;
+};
+
+void setup_nfft(NfftSetup& ns, int d, int kind, double param, const double* p1, int64_t n1, const double* p2,
+                int64_t n2, const uotk_opts& o, void* comm, cudaStream_t s) {
+    Geometry g = compute_geometry(d, p1, n1, p2, n2, s, comm);
+    ns.fp = choose_params(d, kind, param, g, o);
+    ns.sp.fp = ns.fp;
+    build_spectral_plan(ns.sp, s);
+}
+
+size_t grid_elems(const FastParams& fp) {
+    size_t g = 1;
+    for (int t = 0; t < fp.d; ++t) g *= fp.ng;
+    return g;
+}
+
+int read_flag(const DevBuf<int>& flag, cudaStream_t s) {
+    int h = 0;
+    UOTK_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UOTK_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+}  // namespace
+
+template struct DevBuf<int>;
+
+// ============================================================== kernel sum
+static void kernel_sum_impl(int d, int64_t n_src, const double* src, const double* alpha, int64_t n_tgt,
+                            const double* tgt, int kind, double param, double* out, const uotk_opts* opts_in,
+                            uotk_info* info, void* comm, cudaStream_t s) {
+    need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
+    need(kind == UOTK_GAUSS || kind == UOTK_IMQ, "unknown kernel kind");
+    need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");
+    check_points_arg(d, n_src, src, "src");
+    check_points_arg(d, n_src, alpha, "alpha");
+    check_points_arg(d, n_tgt, tgt, "tgt");
+    check_points_arg(d, n_tgt, out, "out");
+    const uotk_opts o = resolve(opts_in);
+    ensure_pool();
+    InArr S, A, T;
+    S.bind(src, (size_t)n_src * d, s);
+    A.bind(alpha, (size_t)n_src, s);
+    T.bind(tgt, (size_t)n_tgt * d, s);
+    OutArr O;
+    O.bind(out, (size_t)n_tgt, s);
+    const int method = pick_method(o, (double)n_src * (double)n_tgt, comm);
+    if (method == UOTK_DIRECT) {
+        fill_info(info, method, nullptr);
+        if (n_tgt > 0) {
+            if (n_src == 0) UOTK_CUDA(cudaMemsetAsync(O.d, 0, n_tgt * sizeof(double), s));
+            else direct_sum_epi(d, n_src, S.d, A.d, n_tgt, T.d, kind, param, EpiStore{O.d, nullptr}, nullptr, s);
+        }
+    } else {
+        NfftSetup ns;
+        setup_nfft(ns, d, kind, param, S.d, n_src, T.d, n_tgt, o, comm, s);
+        fill_info(info, method, &ns.fp);
+        PointSet PS, PT;
+        make_pointset(PS, S.d, n_src, ns.fp, s);
+        make_pointset(PT, T.d, n_tgt, ns.fp, s);
+        DevBuf<double> w(n_src, s), grid(grid_elems(ns.fp), s);
+        DevBuf<double2> spec(ns.sp.spec_elems, s);
+        permute_values(w.p, A.d, PS.perm.p, n_src, s);
+        grid.zero();
+        spread(PS, w.p, grid.p, ns.fp, s);
+        fft_chain(ns.sp, grid.p, spec.p, s, comm);
+        gather_epi(PT, grid.p, ns.fp, EpiStore{O.d, PT.perm.p}, nullptr, s);
+    }
+    O.flush();
+    if (O.host) UOTK_CUDA(cudaStreamSynchronize(s));
+}
+
+// ============================================================== UOT Sinkhorn
+static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
+                     double eps, double lam1, double lam2, int iters, const double* gamma_init, double* beta_out,
+                     double* gamma_out, uotk_uot_result* res, const uotk_opts* opts_in, void* comm, cudaStream_t s) {
+    need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
+    need(n >= 1 && m >= 1, "n and m must be >= 1");
+    need(x && a && y && b && beta_out && gamma_out, "null pointer argument");
+    need(eps > 0 && std::isfinite(eps), "eps must be positive and finite");
+    need(lam1 > 0 && lam2 > 0 && std::isfinite(lam1) && std::isfinite(lam2), "lam1, lam2 must be positive");
+    need(iters >= 0, "iters must be >= 0");
+    const uotk_opts o = resolve(opts_in);
+    ensure_pool();
+    InArr X, A, Y, B, G0;
+    X.bind(x, (size_t)n * d, s);
+    A.bind(a, (size_t)n, s);
+    Y.bind(y, (size_t)m * d, s);
+    B.bind(b, (size_t)m, s);
+    if (gamma_init) G0.bind(gamma_init, (size_t)m, s);
+    OutArr BO, GO;
+    BO.bind(beta_out, (size_t)n, s);
+    GO.bind(gamma_out, (size_t)m, s);
+
+    const double lam = 1.0 / eps;                 // paper lambda (Def. 2.7)
+    const double c1 = lam1 / (1.0 + lam1 * lam);  // (3.3): beta = -c1 log t
+    const double c2 = lam2 / (1.0 + lam2 * lam);  // (3.4): gamma = -c2 log t~
+
+    DevBuf<int> flag(1, s);
+    flag.zero();
+    check_mass(A.d, n, flag.p, s);
+    check_mass(B.d, m, flag.p, s);
+    DevBuf<unsigned long long> dmax(2, s);
+    dmax.zero();
+
+    const int method = pick_method(o, (double)n * (double)m, comm);
+    // per-point state: potentials, masses, next weights, t at x (final) and t~ at y (last)
+    DevBuf<double> pot_x(n, s), pot_y(m, s), mass_x(n, s), mass_y(m, s), wx(n, s), wy(m, s), tx(n, s), ty(m, s);
+    pot_x.zero();
+    const int32_t* perm_x = nullptr;
+    const int32_t* perm_y = nullptr;
+    FastParams fpv;
+    const FastParams* fpp = nullptr;
+    NfftSetup ns;
+    PointSet PX, PY;
+    if (method == UOTK_DIRECT) {
+        UOTK_CUDA(cudaMemcpyAsync(mass_x.p, A.d, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        UOTK_CUDA(cudaMemcpyAsync(mass_y.p, B.d, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (gamma_init) UOTK_CUDA(cudaMemcpyAsync(pot_y.p, G0.d, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        else pot_y.zero();
+    } else {
+        setup_nfft(ns, d, UOTK_GAUSS, eps, X.d, n, Y.d, m, o, comm, s);
+        fpv = ns.fp;
+        fpp = &fpv;
+        make_pointset(PX, X.d, n, ns.fp, s);
+        make_pointset(PY, Y.d, m, ns.fp, s);
+        perm_x = PX.perm.p;
+        perm_y = PY.perm.p;
+        permute_values(mass_x.p, A.d, perm_x, n, s);
+        permute_values(mass_y.p, B.d, perm_y, m, s);
+        if (gamma_init) permute_values(pot_y.p, G0.d, perm_y, m, s);
+        else pot_y.zero();
+    }
+    if (read_flag(flag, s) & 4) fail(UOTK_EDOMAIN, "masses must be positive and finite (KL needs mu_i > 0)");
+
+    // v = e^{lam gamma^0}: weights of the first beta-step
+    scaled_mass(mass_y.p, pot_y.p, m, lam, wy.p, s);
+    EpiSinkhorn ex{pot_x.p, mass_x.p, wx.p, nullptr, c1, lam, flag.p};
+    EpiSinkhorn ey{pot_y.p, mass_y.p, wy.p, nullptr, c2, lam, flag.p};
+
+    if (method == UOTK_DIRECT) {
+        for (int it = 0; it < iters; ++it) {
+            const bool last = it == iters - 1;
+            direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, ex, last ? dmax.p : nullptr, s);  // (3.3)
+            EpiSinkhorn e2 = ey;
+            if (last) e2.t_store = ty.p;
+            direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
+        }
+        // marginals of the recovered plan: t at x from the final gamma
+        direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, EpiStore{tx.p, nullptr}, nullptr, s);
+        if (iters == 0) {
+            scaled_mass(mass_x.p, pot_x.p, n, lam, wx.p, s);
+            direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, EpiStore{ty.p, nullptr}, nullptr, s);
+        }
+    } else {
+        const FastParams& fp = ns.fp;
+        const size_t ge = grid_elems(fp);
+        DevBuf<double> grid(ge, s), grid2;
+        DevBuf<double2> spec(ns.sp.spec_elems, s);
+        const bool fused = fused3d_available(fp);
+        if (fused) grid2.alloc(ge, s);
+        grid.zero();
+        spread(PY, wy.p, grid.p, fp, s);  // adjoint NFFT of nu (.) v at y
+        for (int it = 0; it < iters; ++it) {
+            const bool last = it == iters - 1;
+            EpiSinkhorn e2 = ey;
+            if (last) e2.t_store = ty.p;
+            if (fused) {
+                // beta-step at x: gather t from g', update, spread mu (.) u into the other grid
+                fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                grid2.zero();
+                fused3d_gather_spread(PX, grid.p, grid2.p, fp, ex, last ? dmax.p : nullptr, s);
+                fft_chain(ns.sp, grid2.p, spec.p, s, comm);
+                grid.zero();
+                fused3d_gather_spread(PY, grid2.p, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
+            } else {
+                fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                gather_epi(PX, grid.p, fp, ex, last ? dmax.p : nullptr, s);  // (3.3)
+                grid.zero();
+                spread(PX, wx.p, grid.p, fp, s);
+                fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                gather_epi(PY, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
+                grid.zero();
+                spread(PY, wy.p, grid.p, fp, s);
+            }
+        }
+        // grid holds the spread of nu (.) v with the final v: t at x for the marginals
+        fft_chain(ns.sp, grid.p, spec.p, s, comm);
+        gather_epi(PX, grid.p, fp, EpiStore{tx.p, nullptr}, nullptr, s);
+        if (iters == 0) {
+            scaled_mass(mass_x.p, pot_x.p, n, lam, wx.p, s);
+            grid.zero();
+            spread(PX, wx.p, grid.p, fp, s);
+            fft_chain(ns.sp, grid.p, spec.p, s, comm);
+            gather_epi(PY, grid.p, fp, EpiStore{ty.p, nullptr}, nullptr, s);
+        }
+    }
+
+    // objective terms and their global sums
+    DevBuf<double> cols(5 * (size_t)std::max(n, m), s), sums(12, s);
+    uot_terms(pot_x.p, mass_x.p, tx.p, n, lam, lam1, cols.p, s);
+    sum_columns(cols.p, n, 5, sums.p, s);
+    uot_terms(pot_y.p, mass_y.p, ty.p, m, lam, lam2, cols.p, s);
+    sum_columns(cols.p, m, 5, sums.p + 5, s);
+    // dmax as doubles (non-negative: the bit patterns order like the values)
+    UOTK_CUDA(cudaMemcpyAsync(sums.p + 10, dmax.p, 2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (comm) {
+        comm_allreduce(sums.p, 10, 0, comm, s);
+        comm_allreduce(sums.p + 10, 2, 1, comm, s);
+    }
+    double hs[12];
+    UOTK_CUDA(cudaMemcpyAsync(hs, sums.p, sizeof hs, cudaMemcpyDeviceToHost, s));
+    // potentials back to caller order
+    if (method == UOTK_DIRECT) {
+        UOTK_CUDA(cudaMemcpyAsync(BO.d, pot_x.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        UOTK_CUDA(cudaMemcpyAsync(GO.d, pot_y.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else {
+        unpermute_values(BO.d, pot_x.p, perm_x, n, s);
+        unpermute_values(GO.d, pot_y.p, perm_y, m, s);
+    }
+    BO.flush();
+    GO.flush();
+    const int fl = read_flag(flag, s);  // synchronises the stream
+    if (fl & 3) fail(UOTK_EOVERFLOW, "non-positive or non-finite kernel sum / scaling in the Sinkhorn loop");
+
+    if (res) {
+        const double P = hs[0], bp = hs[1], plogp = hs[2], emb = hs[3], mx = hs[4];
+        const double Q = hs[5], gq = hs[6], qlogq = hs[7], emg = hs[8], my = hs[9];
+        const double tot = P;
+        memset(res, 0, sizeof *res);
+        // primal (2.9) / P:462 through the marginals: the <pi, d^2> terms cancel against the entropy
+        res->primal = bp + gq + eps * (mx * my - tot) + lam1 * (plogp + mx - tot) + lam2 * (qlogq + my - Q);
+        // dual (3.1)
+        res->dual = -lam1 * emb - lam2 * emg + lam1 * mx + lam2 * my - eps * (tot - mx * my);
+        res->plan_mass = tot;
+        res->mass_a = mx;
+        res->mass_b = my;
+        res->max_dbeta = hs[10];
+        res->max_dgamma = hs[11];
+        res->iters = iters;
+        fill_info(&res->info, method, fpp);
+    }
+}
+
+// ============================================================== MMD^2
+static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
+                      const double* b, int kind, double param, double* mmd2, const uotk_opts* opts_in, uotk_info* info,
+                      void* comm, cudaStream_t s) {
+    need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
+    need(kind == UOTK_GAUSS || kind == UOTK_IMQ, "unknown kernel kind");
+    need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");
+    need(mmd2 != nullptr, "mmd2 output pointer is null");
+    check_points_arg(d, n, x, "x");
+    check_points_arg(d, n, a, "a");
+    check_points_arg(d, m, y, "y");
+    check_points_arg(d, m, b, "b");
+    const uotk_opts o = resolve(opts_in);
+    ensure_pool();
+    InArr X, A, Y, B;
+    X.bind(x, (size_t)n * d, s);
+    A.bind(a, (size_t)n, s);
+    Y.bind(y, (size_t)m * d, s);
+    B.bind(b, (size_t)m, s);
+    const int64_t nz = n + m;
+    // z = x u y (row-major), w = (a, -b): MMD^2 = sum_i w_i (K w)_i  (3.5)
+    DevBuf<double> z((size_t)nz * d, s), w(nz, s), prod(nz, s), sum(1, s);
+    if (n) UOTK_CUDA(cudaMemcpyAsync(z.p, X.d, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (m) UOTK_CUDA(cudaMemcpyAsync(z.p + (size_t)n * d, Y.d, (size_t)m * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    signed_concat(A.d, n, B.d, m, w.p, s);
+    const int method = pick_method(o, (double)nz * (double)nz, comm);
+    if (nz == 0) {
+        fill_info(info, method, nullptr);
+        *mmd2 = 0.0;
+        return;
+    }
+    if (method == UOTK_DIRECT) {
+        fill_info(info, method, nullptr);
+        direct_sum_epi(d, nz, z.p, w.p, nz, z.p, kind, param, EpiDot{w.p, prod.p}, nullptr, s);
+    } else {
+        NfftSetup ns;
+        setup_nfft(ns, d, kind, param, z.p, nz, nullptr, 0, o, comm, s);
+        fill_info(info, method, &ns.fp);
+        PointSet PZ;
+        make_pointset(PZ, z.p, nz, ns.fp, s);
+        DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s);
+        DevBuf<double2> spec(ns.sp.spec_elems, s);
+        permute_values(ws.p, w.p, PZ.perm.p, nz, s);
+        grid.zero();
+        spread(PZ, ws.p, grid.p, ns.fp, s);
+        fft_chain(ns.sp, grid.p, spec.p, s, comm);
+        gather_epi(PZ, grid.p, ns.fp, EpiDot{ws.p, prod.p}, nullptr, s);
+    }
+    sum_columns(prod.p, nz, 1, sum.p, s);
+    if (comm) comm_allreduce(sum.p, 1, 0, comm, s);
+    UOTK_CUDA(cudaMemcpyAsync(mmd2, sum.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    UOTK_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace uotk
+
+// ============================================================== extern "C"
+using namespace uotk;
+
+extern "C" {
+
+void uotk_opts_init(uotk_opts* opts) {
+    if (opts) memset(opts, 0, sizeof *opts);
+}
+
+int uotk_kernel_sum(int d, int64_t n_src, const double* src, const double* alpha, int64_t n_tgt, const double* tgt,
+                    int kind, double param, double* out, const uotk_opts* opts, uotk_info* info, void* comm,
+                    void* cuda_stream) {
+    return guarded([&] {
+        kernel_sum_impl(d, n_src, src, alpha, n_tgt, tgt, kind, param, out, opts, info, comm,
+                        (cudaStream_t)cuda_stream);
+    });
+}
+
+int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
+                      double eps, double lam1, double lam2, int iters, const double* gamma_init, double* beta,
+                      double* gamma, uotk_uot_result* res, const uotk_opts* opts, void* comm, void* cuda_stream) {
+    return guarded([&] {
+        uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm,
+                 (cudaStream_t)cuda_stream);
+    });
+}
+
+int uotk_mmd2(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
+              int kind, double param, double* mmd2, const uotk_opts* opts, uotk_info* info, void* comm,
+              void* cuda_stream) {
+    return guarded([&] {
+        mmd2_impl(d, n, x, a, m, y, b, kind, param, mmd2, opts, info, comm, (cudaStream_t)cuda_stream);
+    });
+}
+
+int uotk_comm_unique_id(void* id128) {
+    return guarded([&] {
+        if (!id128) fail(UOTK_EINVAL, "null id buffer");
+        comm_unique_id(id128);
+    });
+}
+
+int uotk_comm_create(const void* id128, int nranks, int rank, void** comm_out) {
+    return guarded([&] {
+        if (!id128 || !comm_out) fail(UOTK_EINVAL, "null argument");
+        *comm_out = comm_create(id128, nranks, rank);
+    });
+}
+
+int uotk_comm_destroy(void* comm) {
+    return guarded([&] { comm_destroy(comm); });
+}
+
+const char* uotk_last_error(void) { return g_last_error.c_str(); }
+
+int uotk_abi_version(void) { return UOTK_ABI_VERSION; }
+
+int64_t uotk_launch_counter(void) { return g_launches; }
+
+void uotk_launch_counter_reset(void) { g_launches = 0; }
+
+}  // extern "C"

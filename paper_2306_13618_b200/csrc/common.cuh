@@ -1,0 +1,151 @@
+// Internal definitions shared by the uotk CUDA sources (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/uotk.h"
+
+namespace uotk {
+
+// ------------------------------------------------------------------ errors
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what, const char* file, int line);
+void check_cufft(cufftResult r, const char* what, const char* file, int line);
+
+#define UOTK_CUDA(call) ::uotk::check_cuda((call), #call, __FILE__, __LINE__)
+#define UOTK_CUFFT(call) ::uotk::check_cufft((call), #call, __FILE__, __LINE__)
+#define UOTK_LAUNCHED() ::uotk::note_launch(__FILE__, __LINE__)
+
+void note_launch(const char* file, int line);  // counts launches + checks launch errors
+void add_launches(int k);                      // launches made by library code we call (CUB)
+
+// ------------------------------------------------------------------ device buffers
+// Stream-ordered device allocation (cudaMallocAsync on the call's stream; the
+// device's default pool keeps memory cached between calls).
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+    void alloc(size_t count, cudaStream_t stream);
+    void zero() { if (n) UOTK_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    ~DevBuf();
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept;
+};
+
+bool is_device_pointer(const void* ptr);
+
+// A caller array that may live on the host or the device: `d` is always a device
+// pointer valid for the duration of the call.
+struct InArr {
+    const double* d = nullptr;
+    DevBuf<double> staged;
+    void bind(const double* user, size_t count, cudaStream_t s);
+};
+struct OutArr {
+    double* d = nullptr;
+    double* user = nullptr;
+    size_t count = 0;
+    bool host = false;
+    DevBuf<double> staged;
+    cudaStream_t s = nullptr;
+    void bind(double* user_ptr, size_t cnt, cudaStream_t stream);
+    void flush();  // device -> host copy if needed (async)
+};
+
+// ------------------------------------------------------------------ geometry / plan
+constexpr int kMaxD = 3;
+
+struct Geometry {
+    int d = 0;
+    double center[kMaxD] = {0, 0, 0};
+    double rmax = 0;
+};
+
+// Parameters of one fast summation.
+struct FastParams {
+    int d = 0;
+    int kind = 0;
+    double param = 0;      // kernel parameter in original units
+    int N = 0;             // bandwidth
+    int ng = 0;            // oversampled grid size per axis
+    int m = 8;             // window half width (taps = 2m)
+    double b = 0;          // Kaiser-Bessel shape, pi (2 - 1/sigma)
+    double h = 1;          // torus scaling
+    double center[kMaxD] = {0, 0, 0};
+    double eps_B = 0;      // IMQ boundary band
+    int p = 0;             // IMQ boundary order
+    std::vector<double> poly;  // IMQ boundary polynomial in t = (r - r0)/eps_B (torus units), ascending
+};
+
+// Sorted, scaled point set on device.
+struct PointSet {
+    int d = 0;
+    int64_t n = 0;
+    DevBuf<double> u;        // d * n, SoA, grid units: u_t = (x_t - c_t)/h * ng
+    DevBuf<int32_t> key;     // n, linear cell key (sorted ascending)
+    DevBuf<int32_t> perm;    // n, sorted position -> caller index
+};
+
+// Fourier-side plan: the D_k table and the cuFFT handles.
+struct SpectralPlan {
+    FastParams fp;
+    DevBuf<double> Dk;       // (N+1)^(d-1) * (N/2+1)
+    cufftHandle r2c = 0, c2r = 0;  // owned by the context cache
+    size_t grid_elems = 0;   // ng^d
+    size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
+};
+
+// ------------------------------------------------------------------ library context
+struct Context;
+Context& ctx();
+void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r);
+
+// ------------------------------------------------------------------ host plan (nfft_plan.cu)
+FastParams choose_params(int d, int kind, double param, const Geometry& g, const uotk_opts& o);
+void build_spectral_plan(SpectralPlan& sp, cudaStream_t s);
+
+// ------------------------------------------------------------------ kernels (launchers)
+// geometry: bbox + max radius over up to two point sets (row-major n x d)
+struct GeomScratch;
+Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2, int64_t n2,
+                          cudaStream_t s, void* comm);
+// scale, key and sort one point set; weights are permuted separately by permute_values
+void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s);
+void permute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
+void unpermute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
+
+// NFFT passes
+void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s);
+void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
+void gather(const PointSet& ps, const double* grid, double* out_sorted, const FastParams& fp, cudaStream_t s);
+template <class Epi>
+void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,
+                unsigned long long* dmax, cudaStream_t s);
+
+// direct sums t_i = sum_j k(|tgt_i - src_j|) w_j (row-major points) followed by an epilogue
+template <class Epi>
+void direct_sum_epi(int d, int64_t n_src, const double* src, const double* w, int64_t n_tgt,
+                    const double* tgt, int kind, double param, const Epi& epi,
+                    unsigned long long* dmax, cudaStream_t s);
+
+// small reductions: sums[k] = sum_i terms_k(i), deterministic order; see reduce.cu
+void sum_columns(const double* vals, int64_t n, int ncols, double* out_dev, cudaStream_t s);
+
+}  // namespace uotk

@@ -1,0 +1,128 @@
+// K6: direct tiled kernel sum, Eq. (4.3) / the dense mat-vecs of Algorithm 1
+// (P:506):  t_i = sum_j k(||tgt_i - src_j||) w_j  in fp64, no approximation.
+// Targets live in registers, source tiles are staged in shared memory; the source
+// range is split over blockIdx.y when there are too few targets to fill the GPU,
+// with partial sums combined in a fixed order (deterministic) before the epilogue.
+#include "common.cuh"
+#include "epilogue.cuh"
+
+namespace uotk {
+
+namespace {
+
+constexpr int kDT = 128;   // threads per block = targets per block
+constexpr int kTile = 128; // sources per shared-memory tile
+
+template <int D>
+__device__ __forceinline__ double pair_sum_tile(const double (*sp)[kTile], const double* sw, int cnt,
+                                                const double* xi, int kind, double inv_or_c2) {
+    double acc = 0.0;
+    if (kind == UOTK_GAUSS) {
+#pragma unroll 4
+        for (int j = 0; j < cnt; ++j) {
+            double r2 = 0.0;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const double v = xi[t] - sp[t][j];
+                r2 = fma(v, v, r2);
+            }
+            acc = fma(exp(-r2 * inv_or_c2), sw[j], acc);
+        }
+    } else {
+#pragma unroll 4
+        for (int j = 0; j < cnt; ++j) {
+            double r2 = inv_or_c2;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const double v = xi[t] - sp[t][j];
+                r2 = fma(v, v, r2);
+            }
+            acc = fma(1.0 / sqrt(r2), sw[j], acc);
+        }
+    }
+    return acc;
+}
+
+// partial[y][i] = sum over this block's source slice; if nsplit == 1 the epilogue runs here
+template <int D, class Epi>
+__global__ void __launch_bounds__(kDT) direct_k(int64_t n_src, const double* __restrict__ src,
+                                                const double* __restrict__ w, int64_t n_tgt,
+                                                const double* __restrict__ tgt, int kind, double inv_or_c2,
+                                                int64_t slice, double* __restrict__ partial, Epi epi,
+                                                unsigned long long* dmax) {
+    __shared__ double sp[D][kTile];
+    __shared__ double sw[kTile];
+    const int64_t i = blockIdx.x * (int64_t)kDT + threadIdx.x;
+    double xi[D];
+    for (int t = 0; t < D; ++t) xi[t] = i < n_tgt ? tgt[i * D + t] : 0.0;
+    const int64_t j0 = blockIdx.y * slice;
+    const int64_t j1 = min(n_src, j0 + slice);
+    double acc = 0.0;
+    for (int64_t jt = j0; jt < j1; jt += kTile) {
+        const int cnt = (int)((j1 - jt) < kTile ? (j1 - jt) : kTile);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cnt; k += kDT) {
+            for (int t = 0; t < D; ++t) sp[t][k] = src[(jt + k) * D + t];
+            sw[k] = w[jt + k];
+        }
+        __syncthreads();
+        acc += pair_sum_tile<D>(sp, sw, cnt, xi, kind, inv_or_c2);  // two-level summation
+    }
+    double dd = 0.0;
+    if (i < n_tgt) {
+        if (partial) partial[blockIdx.y * n_tgt + i] = acc;
+        else dd = epi(i, acc);
+    }
+    if (!partial) warp_max_atomic(dmax, dd);
+}
+
+template <class Epi>
+__global__ void combine_k(const double* __restrict__ partial, int nsplit, int64_t n, Epi epi,
+                          unsigned long long* dmax) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double dd = 0.0;
+    if (i < n) {
+        double acc = 0.0;
+        for (int y = 0; y < nsplit; ++y) acc += partial[y * n + i];
+        dd = epi(i, acc);
+    }
+    warp_max_atomic(dmax, dd);
+}
+
+}  // namespace
+
+template <class Epi>
+void direct_sum_epi(int d, int64_t n_src, const double* src, const double* w, int64_t n_tgt, const double* tgt,
+                    int kind, double param, const Epi& epi, unsigned long long* dmax, cudaStream_t s) {
+    if (n_tgt == 0) return;
+    const int64_t tb = (n_tgt + kDT - 1) / kDT;
+    // split the sources so that the grid has >= ~4 blocks per SM, slices >= 4 tiles
+    int64_t nsplit = 1;
+    while (tb * nsplit < 592 && n_src / (nsplit * 2) >= 4 * kTile) nsplit *= 2;
+    if (nsplit > 65535) nsplit = 65535;
+    const int64_t slice = n_src == 0 ? 1 : (n_src + nsplit - 1) / nsplit;
+    const double arg = kind == UOTK_GAUSS ? 1.0 / param : param * param;
+    DevBuf<double> partial;
+    if (nsplit > 1) partial.alloc((size_t)nsplit * n_tgt, s);
+    dim3 grid((unsigned)tb, (unsigned)nsplit);
+#define UOTK_DIRECT_LAUNCH(DD)                                                                           \
+    direct_k<DD, Epi><<<grid, kDT, 0, s>>>(n_src, src, w, n_tgt, tgt, kind, arg, slice, partial.p, epi, dmax)
+    if (d == 1) UOTK_DIRECT_LAUNCH(1);
+    else if (d == 2) UOTK_DIRECT_LAUNCH(2);
+    else UOTK_DIRECT_LAUNCH(3);
+#undef UOTK_DIRECT_LAUNCH
+    UOTK_LAUNCHED();
+    if (nsplit > 1) {
+        combine_k<Epi><<<(unsigned)((n_tgt + 255) / 256), 256, 0, s>>>(partial.p, (int)nsplit, n_tgt, epi, dmax);
+        UOTK_LAUNCHED();
+    }
+}
+
+template void direct_sum_epi<EpiStore>(int, int64_t, const double*, const double*, int64_t, const double*, int,
+                                       double, const EpiStore&, unsigned long long*, cudaStream_t);
+template void direct_sum_epi<EpiSinkhorn>(int, int64_t, const double*, const double*, int64_t, const double*, int,
+                                          double, const EpiSinkhorn&, unsigned long long*, cudaStream_t);
+template void direct_sum_epi<EpiDot>(int, int64_t, const double*, const double*, int64_t, const double*, int,
+                                     double, const EpiDot&, unsigned long long*, cudaStream_t);
+
+}  // namespace uotk

@@ -1,0 +1,62 @@
+// Per-point epilogues applied to a freshly computed kernel sum t_i (K5 in DESIGN.md).
+#pragma once
+#include <cstdint>
+
+namespace uotk {
+
+// out[perm[i]] = t  (perm == nullptr -> out[i] = t): the plain kernel sum (4.3).
+struct EpiStore {
+    double* out;
+    const int32_t* perm;
+    __device__ __forceinline__ double operator()(int64_t i, double t) const {
+        out[perm ? perm[i] : i] = t;
+        return 0.0;
+    }
+};
+
+// One Sinkhorn half-step, (3.3) / (3.4) in scaling form:
+//   pot_i   <- -c log t_i            (c = eta/(1 + eta*lambda))
+//   w_next  <- mass_i * exp(lambda * pot_i)   (= mass_i * t_i^(-eta*lambda/(1+eta*lambda)))
+// Returns |pot_new - pot_old| for the sup-norm change; flags t <= 0 or non-finite.
+struct EpiSinkhorn {
+    double* pot;
+    const double* mass;
+    double* w_next;
+    double* t_store;  // optional copy of t (for the plan marginals)
+    double c;
+    double lam;
+    int* flag;
+    __device__ __forceinline__ double operator()(int64_t i, double t) const {
+        if (!(t > 0.0) || !isfinite(t)) {
+            atomicOr(flag, 1);
+            t = 1.0;
+        }
+        const double pnew = -c * log(t);
+        const double dd = fabs(pnew - pot[i]);
+        pot[i] = pnew;
+        const double w = mass[i] * exp(lam * pnew);
+        if (!isfinite(w)) atomicOr(flag, 2);
+        w_next[i] = w;
+        if (t_store) t_store[i] = t;
+        return dd;
+    }
+};
+
+// prod[i] = w[i] * t (MMD^2 quadratic form sum_i w_i (K w)_i, reduced afterwards).
+struct EpiDot {
+    const double* w;
+    double* prod;
+    __device__ __forceinline__ double operator()(int64_t i, double t) const {
+        prod[i] = w[i] * t;
+        return 0.0;
+    }
+};
+
+// warp max of non-negative doubles, one atomicMax per warp on the uint64 bit pattern
+__device__ __forceinline__ void warp_max_atomic(unsigned long long* dst, double v) {
+    if (!dst) return;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(dst, (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace uotk

@@ -1,0 +1,220 @@
+// Generic NFFT passes (any d, any m): window spreading (adjoint NFFT, inner sum of
+// (4.6)), the FFT chain with the fused D_k multiplication, and interpolation
+// (forward NFFT, outer sum of (4.6)) — P:590-592.  These are the simple
+// thread-per-point kernels; the tuned d = 3 fused kernels live in fused3d.cu.
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "window.cuh"
+
+namespace uotk {
+
+void comm_allreduce_spectrum(double2* buf, size_t count, void* comm, cudaStream_t s);  // comm.cu
+
+namespace {
+
+inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
+
+// g[l] += w_j prod_t phi(u_jt - l_t): one thread per point, global fp64 RED per tap.
+template <int D, int M>
+__global__ void spread_simple_k(const double* __restrict__ u, const double* __restrict__ w, int64_t n, int ng,
+                                KBWindow win, double* __restrict__ grid) {
+    constexpr int T = 2 * M;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double W[D][T];
+    int base[D];
+    for (int t = 0; t < D; ++t) {
+        const double ut = u[t * n + i];
+        const double fl = floor(ut);
+        const double f = ut - fl;
+        base[t] = (int)fl - M + 1 + ng / 2;
+#pragma unroll
+        for (int a = 0; a < T; ++a) W[t][a] = kb_phi(f + (M - 1 - a), win);
+    }
+    const double wi = w[i];
+    if (D == 1) {
+#pragma unroll
+        for (int a = 0; a < T; ++a) atomicAdd(grid + base[0] + a, wi * W[0][a]);
+    } else if (D == 2) {
+        for (int a = 0; a < T; ++a) {
+            const double wa = wi * W[0][a];
+            double* row = grid + (int64_t)(base[0] + a) * ng + base[1];
+#pragma unroll
+            for (int b = 0; b < T; ++b) atomicAdd(row + b, wa * W[D - 1][b]);
+        }
+    } else {
+        for (int a = 0; a < T; ++a) {
+            for (int b = 0; b < T; ++b) {
+                const double wab = wi * W[0][a] * W[1][b];
+                double* row = grid + ((int64_t)(base[0] + a) * ng + (base[1] + b)) * ng + base[D - 1];
+#pragma unroll
+                for (int c = 0; c < T; ++c) atomicAdd(row + c, wab * W[D - 1][c]);
+            }
+        }
+    }
+}
+
+// t_i = sum_l g[l] prod_t phi(u_it - l_t), then the epilogue.
+template <int D, int M, class Epi>
+__global__ void gather_simple_k(const double* __restrict__ u, int64_t n, int ng, KBWindow win,
+                                const double* __restrict__ grid, Epi epi, unsigned long long* dmax) {
+    constexpr int T = 2 * M;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double dd = 0.0;
+    if (i < n) {
+        double W[D][T];
+        int base[D];
+        for (int t = 0; t < D; ++t) {
+            const double ut = u[t * n + i];
+            const double fl = floor(ut);
+            const double f = ut - fl;
+            base[t] = (int)fl - M + 1 + ng / 2;
+#pragma unroll
+            for (int a = 0; a < T; ++a) W[t][a] = kb_phi(f + (M - 1 - a), win);
+        }
+        double acc = 0.0;
+        if (D == 1) {
+#pragma unroll
+            for (int a = 0; a < T; ++a) acc += grid[base[0] + a] * W[0][a];
+        } else if (D == 2) {
+            for (int a = 0; a < T; ++a) {
+                const double* row = grid + (int64_t)(base[0] + a) * ng + base[1];
+                double r = 0.0;
+#pragma unroll
+                for (int b = 0; b < T; ++b) r += row[b] * W[D - 1][b];
+                acc += r * W[0][a];
+            }
+        } else {
+            for (int a = 0; a < T; ++a) {
+                double ra = 0.0;
+                for (int b = 0; b < T; ++b) {
+                    const double* row = grid + ((int64_t)(base[0] + a) * ng + (base[1] + b)) * ng + base[D - 1];
+                    double r = 0.0;
+#pragma unroll
+                    for (int c = 0; c < T; ++c) r += row[c] * W[D - 1][c];
+                    ra += r * W[1][b];
+                }
+                acc += ra * W[0][a];
+            }
+        }
+        dd = epi(i, acc);
+    }
+    warp_max_atomic(dmax, dd);
+}
+
+// H_k = G_k * D_k for |k_t| <= N/2 (k in I_N with the Nyquist split), 0 elsewhere.
+// D_k layout: ((k_0 + N/2) (N+1) + (k_1 + N/2)) (N/2+1) + k_last  (last axis halved).
+template <int D>
+__global__ void scale_spectrum_k(double2* __restrict__ spec, const double* __restrict__ Dk, int ng, int N,
+                                 int64_t total) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int nh = ng / 2 + 1;
+    int64_t rem = i / nh;
+    const int kl = (int)(i % nh);
+    bool inside = kl <= N / 2;
+    int64_t didx = kl;
+    int64_t dstride = N / 2 + 1;
+#pragma unroll
+    for (int t = D - 2; t >= 0; --t) {
+        const int q = (int)(rem % ng);
+        rem /= ng;
+        const int k = q < ng / 2 ? q : q - ng;
+        inside = inside && (k >= -N / 2) && (k <= N / 2);
+        didx += (int64_t)(k + N / 2) * dstride;
+        dstride *= (N + 1);
+    }
+    if (!inside) {
+        spec[i] = make_double2(0.0, 0.0);
+        return;
+    }
+    const double f = Dk[didx];
+    double2 v = spec[i];
+    v.x *= f;
+    v.y *= f;
+    spec[i] = v;
+}
+
+template <int D, int M>
+void spread_dm(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
+    KBWindow win = make_window(fp.b, M);
+    spread_simple_k<D, M><<<blocks_for(ps.n, 128), 128, 0, s>>>(ps.u.p, w, ps.n, fp.ng, win, grid);
+    UOTK_LAUNCHED();
+}
+
+template <int D, int M, class Epi>
+void gather_dm(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,
+               unsigned long long* dmax, cudaStream_t s) {
+    KBWindow win = make_window(fp.b, M);
+    gather_simple_k<D, M, Epi><<<blocks_for(ps.n, 128), 128, 0, s>>>(ps.u.p, ps.n, fp.ng, win, grid, epi, dmax);
+    UOTK_LAUNCHED();
+}
+
+}  // namespace
+
+#define UOTK_DISPATCH_DM(d, m, CALL)                                              \
+    do {                                                                          \
+        switch ((d) * 16 + (m)) {                                                 \
+            case 16 + 2: { constexpr int DD = 1, MM = 2; CALL; } break;            \
+            case 16 + 3: { constexpr int DD = 1, MM = 3; CALL; } break;            \
+            case 16 + 4: { constexpr int DD = 1, MM = 4; CALL; } break;            \
+            case 16 + 5: { constexpr int DD = 1, MM = 5; CALL; } break;            \
+            case 16 + 6: { constexpr int DD = 1, MM = 6; CALL; } break;            \
+            case 16 + 7: { constexpr int DD = 1, MM = 7; CALL; } break;            \
+            case 16 + 8: { constexpr int DD = 1, MM = 8; CALL; } break;            \
+            case 32 + 2: { constexpr int DD = 2, MM = 2; CALL; } break;            \
+            case 32 + 3: { constexpr int DD = 2, MM = 3; CALL; } break;            \
+            case 32 + 4: { constexpr int DD = 2, MM = 4; CALL; } break;            \
+            case 32 + 5: { constexpr int DD = 2, MM = 5; CALL; } break;            \
+            case 32 + 6: { constexpr int DD = 2, MM = 6; CALL; } break;            \
+            case 32 + 7: { constexpr int DD = 2, MM = 7; CALL; } break;            \
+            case 32 + 8: { constexpr int DD = 2, MM = 8; CALL; } break;            \
+            case 48 + 2: { constexpr int DD = 3, MM = 2; CALL; } break;            \
+            case 48 + 3: { constexpr int DD = 3, MM = 3; CALL; } break;            \
+            case 48 + 4: { constexpr int DD = 3, MM = 4; CALL; } break;            \
+            case 48 + 5: { constexpr int DD = 3, MM = 5; CALL; } break;            \
+            case 48 + 6: { constexpr int DD = 3, MM = 6; CALL; } break;            \
+            case 48 + 7: { constexpr int DD = 3, MM = 7; CALL; } break;            \
+            case 48 + 8: { constexpr int DD = 3, MM = 8; CALL; } break;            \
+            default: fail(UOTK_EINVAL, "unsupported (d, m)");                     \
+        }                                                                         \
+    } while (0)
+
+void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s) {
+    if (ps.n == 0) return;
+    UOTK_DISPATCH_DM(fp.d, fp.m, (spread_dm<DD, MM>(ps, w_sorted, grid, fp, s)));
+}
+
+template <class Epi>
+void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,
+                unsigned long long* dmax, cudaStream_t s) {
+    if (ps.n == 0) return;
+    UOTK_DISPATCH_DM(fp.d, fp.m, (gather_dm<DD, MM, Epi>(ps, grid, fp, epi, dmax, s)));
+}
+
+template void gather_epi<EpiStore>(const PointSet&, const double*, const FastParams&, const EpiStore&,
+                                   unsigned long long*, cudaStream_t);
+template void gather_epi<EpiSinkhorn>(const PointSet&, const double*, const FastParams&, const EpiSinkhorn&,
+                                      unsigned long long*, cudaStream_t);
+template void gather_epi<EpiDot>(const PointSet&, const double*, const FastParams&, const EpiDot&,
+                                 unsigned long long*, cudaStream_t);
+
+void gather(const PointSet& ps, const double* grid, double* out_sorted, const FastParams& fp, cudaStream_t s) {
+    gather_epi(ps, grid, fp, EpiStore{out_sorted, nullptr}, nullptr, s);
+}
+
+void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
+    const FastParams& fp = sp.fp;
+    UOTK_CUFFT(cufftSetStream(sp.r2c, s));
+    UOTK_CUFFT(cufftSetStream(sp.c2r, s));
+    UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
+    const int64_t total = (int64_t)sp.spec_elems;
+    if (fp.d == 1) scale_spectrum_k<1><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total);
+    else if (fp.d == 2) scale_spectrum_k<2><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total);
+    else scale_spectrum_k<3><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total);
+    UOTK_LAUNCHED();
+    if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
+    UOTK_CUFFT(cufftExecZ2D(sp.c2r, (cufftDoubleComplex*)spec, grid));
+}
+
+}  // namespace uotk

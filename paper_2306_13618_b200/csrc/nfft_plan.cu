@@ -1,0 +1,305 @@
+// Host planning of the fast summation (Sec. 4) and the kernel-coefficient
+// setup on the device:  torus scaling h (Eq. 4.7; Rem. 4.3), bandwidth N
+// (Eq. 4.4; Rem. 4.4), regularised kernel K_R, its Fourier
+// coefficients b_k, and the deconvolved multiplier
+//     D_k = w_k b_k / (n_g^{2d} prod_t phihat(k_t)^2),   k in I_N,
+// which turns "spread -> FFT -> *D_k -> inverse FFT -> interpolate" into the
+// factorisation (4.5)-(4.6).  See DESIGN.md "Fast summation".
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace uotk {
+
+namespace {
+
+// next integer >= v whose prime factors are all in {2,3,5,7}, and even
+int nice_even(int v) {
+    if (v < 2) v = 2;
+    for (int x = v + (v & 1);; x += 2) {
+        int y = x;
+        for (int p : {2, 3, 5, 7})
+            while (y % p == 0) y /= p;
+        if (y == 1) return x;
+    }
+}
+
+// Modified Bessel I_0 by its power series (all terms positive), long double.
+long double bessel_i0(long double z) {
+    long double q = z * z / 4.0L, term = 1.0L, sum = 1.0L;
+    for (int k = 1; k < 400; ++k) {
+        term *= q / ((long double)k * (long double)k);
+        sum += term;
+        if (term < sum * 1e-21L) break;
+    }
+    return sum;
+}
+
+// Taylor coefficients y_k = K^(k)(r0)/k! of K(r) = (h^2 r^2 + c^2)^(-1/2) at r0
+// (power-series recurrence for g^alpha with g(s) = A + B s + C s^2).
+std::vector<long double> imq_taylor(long double h, long double c, long double r0, int n) {
+    long double g[3] = {h * h * r0 * r0 + c * c, 2 * h * h * r0, h * h};
+    const long double alpha = -0.5L;
+    std::vector<long double> y(n, 0.0L);
+    y[0] = powl(g[0], alpha);
+    for (int k = 1; k < n; ++k) {
+        long double acc = 0;
+        for (int i = 1; i <= 2 && i <= k; ++i) acc += ((alpha + 1) * i - k) * g[i] * y[k - i];
+        y[k] = acc / (k * g[0]);
+    }
+    return y;
+}
+
+// Boundary polynomial K_B on t = (r - r0)/eps_B in [0, 1], r0 = 1/2 - eps_B:
+// P^(j)(0) = eps_B^j K^(j)(r0) for j < p (C^{p-1} match with K) and P^(j)(1) = 0 for
+// 1 <= j < p (flat at the torus boundary r = 1/2, so the radial extension by the
+// constant P(1) is smooth across the sphere ||y|| = 1/2 in every dimension; reading R10).
+std::vector<double> imq_boundary_poly(double h, double c, double eps_B, int p) {
+    const long double r0 = 0.5L - eps_B;
+    std::vector<long double> y = imq_taylor(h, c, r0, p);
+    std::vector<long double> a(p);
+    long double e = 1;
+    for (int j = 0; j < p; ++j) { a[j] = y[j] * e; e *= eps_B; }
+    const int q = p - 1;  // unknown c_i, i = 0..p-2, for t^{p+i}
+    std::vector<long double> M(q * q), rhs(q);
+    auto ff = [](int n, int k) -> long double {  // n!/(n-k)!
+        if (k > n) return 0;
+        long double r = 1;
+        for (int i = 0; i < k; ++i) r *= (n - i);
+        return r;
+    };
+    for (int k = 1; k <= q; ++k) {
+        long double s = 0;
+        for (int j = k; j < p; ++j) s += a[j] * ff(j, k);
+        rhs[k - 1] = -s;
+        for (int i = 0; i < q; ++i) M[(k - 1) * q + i] = ff(p + i, k);
+    }
+    // Gaussian elimination with partial pivoting
+    for (int col = 0; col < q; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < q; ++r)
+            if (fabsl(M[r * q + col]) > fabsl(M[piv * q + col])) piv = r;
+        if (piv != col) {
+            for (int k = 0; k < q; ++k) std::swap(M[col * q + k], M[piv * q + k]);
+            std::swap(rhs[col], rhs[piv]);
+        }
+        for (int r = col + 1; r < q; ++r) {
+            long double f = M[r * q + col] / M[col * q + col];
+            for (int k = col; k < q; ++k) M[r * q + k] -= f * M[col * q + k];
+            rhs[r] -= f * rhs[col];
+        }
+    }
+    std::vector<long double> cc(q);
+    for (int r = q - 1; r >= 0; --r) {
+        long double s = rhs[r];
+        for (int k = r + 1; k < q; ++k) s -= M[r * q + k] * cc[k];
+        cc[r] = s / M[r * q + r];
+    }
+    std::vector<double> poly(2 * p - 1);
+    for (int j = 0; j < p; ++j) poly[j] = (double)a[j];
+    for (int i = 0; i < q; ++i) poly[p + i] = (double)cc[i];
+    return poly;
+}
+
+}  // namespace
+
+FastParams choose_params(int d, int kind, double param, const Geometry& g, const uotk_opts& o) {
+    FastParams fp;
+    fp.d = d;
+    fp.kind = kind;
+    fp.param = param;
+    for (int t = 0; t < d; ++t) fp.center[t] = g.center[t];
+    fp.m = o.m > 0 ? o.m : 8;
+    if (fp.m < 2 || fp.m > 8) fail(UOTK_EINVAL, "opts.m must be in [2, 8]");
+    const double sigma = o.sigma > 0 ? o.sigma : 2.0;
+    if (sigma < 1.25) fail(UOTK_EINVAL, "opts.sigma must be >= 1.25");
+    const double tol = o.tol > 0 ? o.tol : 1e-16;
+    const double L = std::log(1.0 / tol);
+    const double rmax = g.rmax;
+
+    double Rbar_max;  // largest torus radius the points may occupy
+    double h_min;
+    if (kind == UOTK_GAUSS) {
+        // pure periodisation: pair differences must stay inside the cell (|diff_t| < 1/2)
+        Rbar_max = 0.24;
+        const double h_decay = 2.0 * std::sqrt(param * L);  // K(h/2) <= tol K(0)
+        h_min = h_decay;
+        fp.eps_B = 0;
+        fp.p = 0;
+    } else {
+        fp.p = o.p > 0 ? o.p : 12;
+        if (fp.p < 2 || fp.p > 16) fail(UOTK_EINVAL, "opts.p must be in [2, 16]");
+        fp.eps_B = o.eps_B > 0 ? o.eps_B : 0.1;
+        if (fp.eps_B >= 0.25) fail(UOTK_EINVAL, "opts.eps_B must be < 0.25");
+        Rbar_max = 0.25 - fp.eps_B / 2;  // pair distances <= 1/2 - eps_B (reading R11)
+        h_min = 0;
+    }
+    double h = std::max(rmax / Rbar_max, h_min);
+    if (o.h > 0) {
+        if (o.h < rmax / Rbar_max * (1 - 1e-12)) fail(UOTK_EINVAL, "opts.h too small for the point cloud");
+        h = o.h;
+    }
+    if (!(h > 0)) h = (kind == UOTK_IMQ) ? std::max(param, 1e-3) : 1.0;
+    fp.h = h;
+
+    int N = o.N;
+    if (N <= 0) {
+        if (kind == UOTK_GAUSS) {
+            const double eb = param / (h * h);  // kernel exp(-|y|^2/eb) in torus units
+            N = (int)std::ceil(2.0 * std::sqrt(L / (M_PI * M_PI * eb)));
+            N = nice_even(std::max(N, 8));
+        } else {
+            N = (d == 3) ? 192 : 256;
+        }
+    }
+    if (N % 2) fail(UOTK_EINVAL, "opts.N must be even");
+    fp.N = N;
+    int ng = nice_even((int)std::ceil(sigma * N - 1e-9));
+    // the window footprint of every point must stay inside the grid without wrap
+    const double Rbar = rmax / h;
+    const int ng_min = (int)std::ceil((fp.m + 2) / (0.5 - Rbar));
+    if (ng < ng_min) ng = nice_even(ng_min);
+    if (ng < 2 * N) ng = nice_even(2 * N);  // keeps k = +-N/2 distinct on the grid
+    double grid = std::pow((double)ng, d);
+    if (grid > 2.0e9) fail(UOTK_EUNSUPPORTED, "oversampled grid too large");
+    fp.ng = ng;
+    fp.b = M_PI * (2.0 - (double)N / ng);  // b = pi (2 - 1/sigma_eff)
+    if (kind == UOTK_IMQ) fp.poly = imq_boundary_poly(h, param, fp.eps_B, fp.p);
+    return fp;
+}
+
+// ---------------------------------------------------------------------------- kernels
+struct KernelCoef {
+    int kind;
+    double h2;      // h^2
+    double param;
+    double r0, eps_B;
+    int npoly;
+    double poly[32];
+};
+
+// Samples of the regularised kernel K_R on the N^d grid j/N, j in I_N (stored at j mod N).
+template <int D>
+__global__ void sample_kernel_k(double* out, int N, KernelCoef kc) {
+    int64_t total = 1;
+    for (int t = 0; t < D; ++t) total *= N;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t rem = i;
+    double r2 = 0;
+    for (int t = D - 1; t >= 0; --t) {
+        int q = (int)(rem % N);
+        rem /= N;
+        int j = q < N / 2 ? q : q - N;
+        double y = (double)j / N;
+        r2 += y * y;
+    }
+    double v;
+    if (kc.kind == UOTK_GAUSS) {
+        v = exp(-kc.h2 * r2 / kc.param);
+    } else {
+        double r = sqrt(r2);
+        if (r <= kc.r0) {
+            v = 1.0 / sqrt(kc.h2 * r2 + kc.param * kc.param);
+        } else {
+            double tt = r >= 0.5 ? 1.0 : (r - kc.r0) / kc.eps_B;
+            double acc = 0;
+            for (int k = kc.npoly - 1; k >= 0; --k) acc = acc * tt + kc.poly[k];
+            v = acc;
+        }
+    }
+    out[i] = v;
+}
+
+// D_k on k in [-N/2, N/2]^(d-1) x [0, N/2]; b_k read from the N-point half spectrum.
+template <int D>
+__global__ void dk_kernel(double* Dk, const double2* bspec, const double* psi, int N) {
+    const int nh = N / 2 + 1;     // last axis
+    const int nf = N + 1;         // other axes
+    int64_t total = nh;
+    for (int t = 0; t < D - 1; ++t) total *= nf;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t rem = i;
+    int kl = (int)(rem % nh);
+    rem /= nh;
+    double fac = psi[kl] * ((kl == N / 2) ? 0.5 : 1.0);
+    int64_t bidx = kl;
+    int64_t bstride = nh;
+    for (int t = D - 2; t >= 0; --t) {
+        int k = (int)(rem % nf) - N / 2;
+        rem /= nf;
+        int ak = k < 0 ? -k : k;
+        fac *= psi[ak] * ((ak == N / 2) ? 0.5 : 1.0);
+        int q = k < 0 ? k + N : k;   // N-periodic index (k = +-N/2 -> N/2)
+        bidx += (int64_t)q * bstride;
+        bstride *= N;
+    }
+    double invN = 1.0;
+    for (int t = 0; t < D; ++t) invN /= N;
+    Dk[i] = fac * bspec[bidx].x * invN;
+}
+
+void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
+    const FastParams& fp = sp.fp;
+    const int d = fp.d, N = fp.N, ng = fp.ng;
+    // 1) samples of K_R and their DFT -> b_k (real: K_R is real and even)
+    size_t nsamp = 1;
+    for (int t = 0; t < d; ++t) nsamp *= N;
+    size_t nspec = nsamp / N * (N / 2 + 1);
+    DevBuf<double> samp(nsamp, s);
+    DevBuf<double2> bspec(nspec, s);
+    KernelCoef kc{};
+    kc.kind = fp.kind;
+    kc.h2 = fp.h * fp.h;
+    kc.param = fp.param;
+    kc.eps_B = fp.eps_B;
+    kc.r0 = 0.5 - fp.eps_B;
+    kc.npoly = (int)fp.poly.size();
+    if (kc.npoly > 32) fail(UOTK_EINVAL, "boundary polynomial too long");
+    for (int k = 0; k < kc.npoly; ++k) kc.poly[k] = fp.poly[k];
+    const int tb = 256;
+    int gb = (int)((nsamp + tb - 1) / tb);
+    if (d == 1) sample_kernel_k<1><<<gb, tb, 0, s>>>(samp.p, N, kc);
+    else if (d == 2) sample_kernel_k<2><<<gb, tb, 0, s>>>(samp.p, N, kc);
+    else sample_kernel_k<3><<<gb, tb, 0, s>>>(samp.p, N, kc);
+    UOTK_LAUNCHED();
+    cufftHandle r2c, c2r;
+    get_fft_plans(d, N, &r2c, &c2r);
+    UOTK_CUFFT(cufftSetStream(r2c, s));
+    UOTK_CUFFT(cufftExecD2Z(r2c, samp.p, (cufftDoubleComplex*)bspec.p));
+
+    // 2) per-axis deconvolution psi(k) = 1/(n_g^2 phihat(k)^2), k = 0..N/2, with the
+    //    Kaiser-Bessel pair  phi(v) = sinh(b sqrt(m^2 - v^2))/sqrt(m^2 - v^2) * m/sinh(b m)
+    //    (v in grid units) and phihat(k) = (pi m / n_g) I0(m sqrt(b^2 - (2 pi k/n_g)^2)) / sinh(b m).
+    std::vector<double> psi(N / 2 + 1);
+    const long double m = fp.m, b = fp.b;
+    const long double sinh_bm = sinhl(b * m);
+    for (int k = 0; k <= N / 2; ++k) {
+        long double w = 2.0L * M_PI * k / ng;
+        long double z = m * sqrtl(b * b - w * w);
+        long double ph = (long double)M_PI * m / ng * bessel_i0(z) / sinh_bm;
+        psi[k] = (double)(1.0L / ((long double)ng * ng * ph * ph));
+    }
+    DevBuf<double> psi_d(psi.size(), s);
+    UOTK_CUDA(cudaMemcpyAsync(psi_d.p, psi.data(), psi.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+
+    // 3) D_k table
+    size_t ndk = (size_t)(N / 2 + 1);
+    for (int t = 0; t < d - 1; ++t) ndk *= (N + 1);
+    sp.Dk.alloc(ndk, s);
+    gb = (int)((ndk + tb - 1) / tb);
+    if (d == 1) dk_kernel<1><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
+    else if (d == 2) dk_kernel<2><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
+    else dk_kernel<3><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
+    UOTK_LAUNCHED();
+    // psi_d / samp / bspec are freed stream-ordered after the kernels that use them
+
+    get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
+    sp.grid_elems = 1;
+    for (int t = 0; t < d; ++t) sp.grid_elems *= ng;
+    sp.spec_elems = sp.grid_elems / ng * (ng / 2 + 1);
+}
+
+}  // namespace uotk

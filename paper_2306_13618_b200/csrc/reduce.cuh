@@ -1,0 +1,15 @@
+// Launchers of reduce.cu.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace uotk {
+
+void uot_terms(const double* pot, const double* mass, const double* t, int64_t n, double lam, double eta,
+               double* cols, cudaStream_t s);
+void check_mass(const double* a, int64_t n, int* flag, cudaStream_t s);
+void scaled_mass(const double* mass, const double* pot, int64_t n, double lam, double* w, cudaStream_t s);
+void signed_concat(const double* a, int64_t n, const double* b, int64_t m, double* w, cudaStream_t s);
+
+}  // namespace uotk

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (north star):
+  * kernel sums: max relative error 1e-9 — per entry for positive weights, and
+    max_i |ds_i| / max_i |s_i| for signed weights (reading R14);
+  * UOT cost (primal), dual, plan mass: 1e-8 relative; potentials: the paper's residual
+    ||dbeta||/||beta|| + ||dgamma||/||gamma|| <= 1e-8;
+  * MMD^2: |d| / max(|MMD^2|, 1e-3 * sum|terms|) <= 1e-8 (reading R13).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def uk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2306_13618_b200 as uk
+    return uk
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def rel_err(got, ref, signed):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    if signed:
+        return float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+    return float(np.max(np.abs(got - ref) / np.abs(ref)))
+
+
+# ------------------------------------------------------------------ kernel sums
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("signed", [False, True])
+def test_kernel_sum_parity(uk, method, kind, d, signed):
+    pr = W.random_sum(d, 3001, 1999, kind=kind, param=(0.0025 if kind == W.GAUSS else 0.05), seed=d, signed=signed)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    got, info = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), kind, pr.param,
+                              opts={"method": method}, return_info=True)
+    assert info["method"] == method
+    err = rel_err(got.cpu().numpy(), ref, signed)
+    assert err <= 1e-9, (err, info)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_kernel_sum_host_arrays_and_wide_gaussian(uk, d):
+    """Host (numpy) inputs are staged by the library; a wide Gaussian (C1's eps=0.05)
+    exercises the torus scaling h > 1 (Rem. 4.3)."""
+    pr = W.random_sum(d, 2500, 1500, kind=W.GAUSS, param=0.05, seed=11)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    got, info = uk.kernel_sum(pr.src, pr.alpha, pr.tgt, "gauss", 0.05, opts={"method": "nfft"}, return_info=True)
+    assert isinstance(got, np.ndarray)
+    assert info["h"] > 1.0
+    assert rel_err(got, ref, False) <= 1e-9
+
+
+def test_kernel_sum_edge_cases(uk):
+    rng = np.random.default_rng(0)
+    tgt = W.uniform_ball(rng, 7, 3, 0.2)
+    for method in ("direct", "nfft"):
+        out = uk.kernel_sum(cuda(np.zeros((0, 3))), cuda(np.zeros(0)), cuda(tgt), "gauss", 0.01,
+                            opts={"method": method})
+        assert torch.all(out == 0)
+        out = uk.kernel_sum(cuda(tgt), cuda(np.ones(7)), cuda(np.zeros((0, 3))), "gauss", 0.01,
+                            opts={"method": method})
+        assert out.numel() == 0
+        # single source exactly at the single target: K(0) alpha
+        p = np.array([[0.01, -0.02, 0.03]])
+        out = uk.kernel_sum(cuda(p), cuda(np.array([2.0])), cuda(p), "imq", 0.05, opts={"method": method})
+        assert abs(out.item() - 2.0 / 0.05) <= 1e-9 * 40
+        # all points coincident (zero radius cloud)
+        q = np.repeat(p, 5, 0)
+        out = uk.kernel_sum(cuda(q), cuda(np.ones(5)), cuda(q), "gauss", 0.01, opts={"method": method})
+        assert torch.allclose(out, torch.full_like(out, 5.0), rtol=1e-9, atol=0)
+    with pytest.raises(uk.UotkError) as e:
+        bad = tgt.copy()
+        bad[3, 1] = np.nan
+        uk.kernel_sum(cuda(bad), cuda(np.ones(7)), cuda(tgt), "gauss", 0.01, opts={"method": "nfft"})
+    assert e.value.code == -2
+
+
+def test_kernel_sum_c5_full_size_sampled(uk):
+    """C5 d=3 at n = m = 1e6 (NFFT), checked on 64 sampled targets by the oracle."""
+    pr = W.c5_sum(3, 1_000_000, kind=W.GAUSS)
+    got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"})
+    idx = np.random.default_rng(1).choice(len(pr.tgt), 64, replace=False)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt[idx], pr.kind, pr.param)
+    g = got.cpu().numpy()[idx]
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(g - ref)) / scale <= 1e-9
+
+
+# ------------------------------------------------------------------ UOT Sinkhorn
+def _uot_check(res, beta, gamma, ref, tol=1e-8):
+    resid = (np.linalg.norm(beta - ref.beta) / np.linalg.norm(ref.beta)
+             + np.linalg.norm(gamma - ref.gamma) / np.linalg.norm(ref.gamma))
+    assert resid <= tol, resid
+    assert abs(res.primal - ref.primal) <= tol * abs(ref.primal), (res.primal, ref.primal)
+    assert abs(res.dual - ref.dual) <= tol * abs(ref.dual), (res.dual, ref.dual)
+    assert abs(res.plan_mass - ref.plan_mass) <= tol * ref.plan_mass
+    assert abs(res.mass_a - ref.mass_a) <= 1e-13 * ref.mass_a
+    assert abs(res.mass_b - ref.mass_b) <= 1e-13 * ref.mass_b
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_c1_full(uk, method):
+    """C1 exactly (configs[0]): d=2, n=m=1000, eps=0.05, lam=1, 100 iterations."""
+    pr = W.c1_uot()
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": method})
+    assert res.info["method"] == method
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    assert abs(res.max_dbeta - ref.max_dbeta) <= 1e-6 * max(ref.max_dbeta, 1e-12) + 1e-14
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_c3_like_reduced(uk, method):
+    """C3 distributions and parameters (eps=0.02, lam=0.5, d=3) at reduced n, ragged sizes."""
+    pr = W.c3_uot(n=1537, m=1201, iters=25)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": method})
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+def test_uot_unequal_penalties_gamma_init_and_zero_iters(uk):
+    pr = W.c1_uot(n=300, m=250)
+    g0 = np.random.default_rng(3).uniform(-0.05, 0.05, 250)
+    for method in ("direct", "nfft"):
+        ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, 0.7, 2.5, 12, gamma0=g0)
+        beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, 0.7, lam2=2.5,
+                                           iters=12, gamma_init=cuda(g0), opts={"method": method})
+        _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+        ref0 = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, 1.0, 1.0, 0)
+        beta, gamma, res = uk.uot_sinkhorn(pr.x, pr.a, pr.y, pr.b, pr.eps, 1.0, iters=0, opts={"method": method})
+        assert np.all(gamma == 0) and np.all(beta == 0)
+        assert abs(res.dual - ref0.dual) <= 1e-9 * abs(ref0.dual)
+        assert abs(res.primal - ref0.primal) <= 1e-9 * abs(ref0.primal)
+
+
+def test_uot_bad_masses(uk):
+    pr = W.c1_uot(n=50, m=40)
+    a = pr.a.copy()
+    a[7] = 0.0
+    with pytest.raises(uk.UotkError) as e:
+        uk.uot_sinkhorn(cuda(pr.x), cuda(a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=3)
+    assert e.value.code == -2
+
+
+def test_uot_c3_full_size_sampled(uk):
+    """C3 at full size (n = m = 1e6, NFFT, as bench.py runs it) for a few iterations: the
+    last gamma-step identity gamma_j = -c2 log sum_i k_ij mu_i e^{lam beta_i} (3.4) checked
+    by the oracle at 48 sampled j, with the returned beta."""
+    pr = W.c3_uot(iters=3)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": "nfft"})
+    b = beta.cpu().numpy()
+    g = gamma.cpu().numpy()
+    lam = 1.0 / pr.eps
+    c2 = pr.lam / (1.0 + pr.lam * lam)
+    idx = np.random.default_rng(2).choice(len(pr.y), 48, replace=False)
+    tt = oracle.kernel_sum_direct(pr.x, pr.a * np.exp(lam * b), pr.y[idx], W.GAUSS, pr.eps)
+    ref = -c2 * np.log(tt)
+    assert np.max(np.abs(g[idx] - ref)) <= 1e-9 * np.max(np.abs(ref))
+    assert abs(res.mass_a - pr.a.sum()) <= 1e-12 * pr.a.sum()
+
+
+# ------------------------------------------------------------------ MMD^2
+def _mmd_tol(x, a, y, b, kind, param):
+    xx = abs(float(a @ oracle.kernel_sum_direct(x, a, x, kind, param)))
+    yy = abs(float(b @ oracle.kernel_sum_direct(y, b, y, kind, param)))
+    return xx + yy
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+def test_mmd2_c2_reduced(uk, method, kind):
+    pr = W.c2_mmd(n=2500, m=2100)
+    param = dict(pr.kernels)[kind]
+    ref = oracle.mmd2_direct(pr.x, pr.a, pr.y, pr.b, kind, param)
+    got, info = uk.mmd2(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), kind, param, opts={"method": method},
+                        return_info=True)
+    denom = max(abs(ref), 1e-3 * _mmd_tol(pr.x, pr.a, pr.y, pr.b, kind, param))
+    assert abs(got - ref) / denom <= 1e-8, (got, ref, info)
+
+
+def test_mmd2_identities(uk):
+    rng = np.random.default_rng(5)
+    x = W.uniform_ball(rng, 400, 3, 0.2)
+    a = rng.uniform(0.5, 1.5, 400)
+    for method in ("direct", "nfft"):
+        v = uk.mmd2(cuda(x), cuda(a), cuda(x), cuda(a), "gauss", 0.0025, opts={"method": method})
+        assert abs(v) <= 1e-10 * a.sum() ** 2
+        v = uk.mmd2(cuda(x[:1]), cuda(np.ones(1)), cuda(x[1:2]), cuda(np.ones(1)), "gauss", 0.0025,
+                    opts={"method": method})
+        r2 = float(np.sum((x[0] - x[1]) ** 2))
+        assert abs(v - (2 - 2 * np.exp(-r2 / 0.0025))) <= 1e-9
