@@ -1,0 +1,379 @@
+"""Benchmark of the hot path: UOT Sinkhorn iterations/s (and MMD^2 evals/s) at n=m=1M, d=3, fp64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C3|C1]
+
+A "step" is one full uot_sinkhorn call on the C3 workload (BASELINE.json configs[2]:
+d=3, n=m=1M, 8-component Gaussian mixtures clipped to radius 0.2, masses U(0.1,1),
+eps=0.02, lam=0.5, 200 iterations): point scaling, sorting, kernel coefficients and
+200 x (two NFFT kernel sums + Sinkhorn updates), then the objective values — every
+row of SURVEY.md §8(a).  value = iterations/s of the whole job (all ranks), inputs
+resident in HBM.  e2e = the same metric through the C ABI with pinned HOST buffers
+(H2D of the inputs and D2H of beta, gamma and the objectives inside the timed region).
+
+Multi-GPU (torchrun, one rank per GPU): the points are sharded over ranks (contiguous
+blocks), every rank spreads its shard and the oversampled Fourier coefficients are
+summed with NCCL inside libuotk.so (one all-reduce per kernel sum) — strong scaling.
+
+--impl reference times the CPU fp64 oracle (oracle/, Algorithm 1 with direct sums) on a
+bounded sample of the same workload on the host cores and extrapolates to its
+iterations/s (the paper's code is not available).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+# FP64 FMA pipe: 148 SMs x 64 DFMA/clk/SM x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS_NOMINAL = 148 * 64 * 2 * 1.965e9 / 1e12
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="C3", choices=["C3", "C1"])
+    p.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-mmd", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ncu", action="store_true", help="short run for ncu launch lists (no side legs)")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_problem(name, iters):
+    if name == "C3":
+        pr = W.c3_uot()
+    else:
+        pr = W.c1_uot()
+    if iters is not None:
+        pr.iters = iters
+    return pr
+
+
+def shard(arr, world, rank):
+    n = len(arr)
+    lo = n * rank // world
+    hi = n * (rank + 1) // world
+    return np.ascontiguousarray(arr[lo:hi])
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [v for v in sm if v > 300] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- reference arm / cpu baseline
+def oracle_sample(pr, n_targets, seed=0):
+    """Time the oracle's direct kernel sum (Algorithm 1's mat-vec, Eq. 3.3) for a
+    sample of targets against ALL sources; extrapolate to one Sinkhorn iteration
+    (two kernel sums over n + m targets — direct cost is linear in the targets)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(len(pr.x), n_targets, replace=False)
+    w = pr.b * np.ones(len(pr.b))
+    t0 = time.perf_counter()
+    oracle.kernel_sum_direct(pr.y, w, pr.x[idx], W.GAUSS, pr.eps)
+    dt = time.perf_counter() - t0
+    per_iter = dt * (len(pr.x) + len(pr.y)) / n_targets
+    return dt, per_iter
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    pr = make_problem(args.workload, args.iters)
+    n_t = 200 if args.workload == "C3" else 1000
+    times = []
+    for _ in range(args.warmup):
+        oracle_sample(pr, min(n_t, 50))
+    for _ in range(args.steps):
+        dt, per_iter = oracle_sample(pr, n_t)
+        times.append(per_iter)
+    per_iter = statistics.median(times)
+    value = 1.0 / per_iter
+    sample = (f"oracle direct kernel sum (numpy fp64) of {n_t} sampled targets x {len(pr.y)} sources per step, "
+              f"extrapolated x{(len(pr.x) + len(pr.y)) / n_t:.0f} to one iteration (2 kernel sums)")
+    line = {
+        "impl": "reference", "metric": "UOT Sinkhorn iterations/s", "value": value, "unit": "iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_iter * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(pr),
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(pr, extra=None):
+    cfg = {"workload": f"{pr.name}: UOT Sinkhorn d={pr.d} n={len(pr.x)} m={len(pr.y)} eps={pr.eps} "
+                       f"lam={pr.lam} iters={pr.iters}", "n": len(pr.x), "m": len(pr.y), "d": pr.d,
+           "eps": pr.eps, "lam": pr.lam, "iters": pr.iters}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ---------------------------------------------------------------------- our arm
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_13618_b200 as uk
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = uk.Comm.from_torch_distributed()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    pr = make_problem(args.workload, args.iters)
+    x, a, y, b = (shard(v, world, rank) for v in (pr.x, pr.a, pr.y, pr.b))
+    xd, ad, yd, bd = (torch.from_numpy(v).to(dev) for v in (x, a, y, b))
+    opts = {"method": "nfft"}
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def step():
+        return uk.uot_sinkhorn(xd, ad, yd, bd, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm)
+
+    for _ in range(args.warmup):
+        beta, gamma, res = step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    uk.reset_launch_counter()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ev[k][0].record(stream)
+            beta, gamma, res = step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = uk.launch_counter()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = t.item()
+    ms_per_step = total_ms / args.steps
+    value = pr.iters * args.steps / (total_ms / 1e3)
+
+    out = {}
+    if not args.ncu:
+        out["roofline"] = roofline_leg(uk, step, pr, res, world)
+        if not args.no_e2e:
+            out["e2e"] = e2e_leg(uk, pr, x, a, y, b, comm, barrier, world, dev)
+        if not args.no_mmd:
+            out["mmd2"] = mmd_leg(uk, world, rank, comm, dev, barrier)
+    if rank == 0:
+        line = {
+            "metric": "UOT Sinkhorn iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Gaussian mixtures, BASELINE.json configs[2])",
+            "config": workload_config(pr, {"method": res.info["method"], "N": res.info["N"],
+                                           "n_grid": res.info["n_grid"], "window_m": res.info["m"],
+                                           "h": res.info["h"], "parallelism": f"points sharded x{world}",
+                                           "l2": "flushed between steps (256 MB write outside the events)"}),
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "result": {"primal": res.primal, "dual": res.dual, "plan_mass": res.plan_mass,
+                       "max_dbeta": res.max_dbeta, "max_dgamma": res.max_dgamma},
+        }
+        line.update({k: v for k, v in out.items() if v is not None})
+        if not args.ncu and not args.no_cpu_baseline and world == 1:
+            dt, per_iter = oracle_sample(pr, 200 if args.workload == "C3" else 1000)
+            line["cpu_baseline"] = {
+                "value": 1.0 / per_iter, "unit": "iterations/s", "cores": 1, "kind": "oracle",
+                "sample": f"oracle direct kernel sum of 200 sampled targets x {len(pr.y)} sources "
+                          f"({dt:.1f} s), extrapolated linearly to one iteration (2 sums over n+m targets)"}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def fp64_peak():
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            j = json.load(f)
+        return float(j["tflops"]), f"measured DFMA microbenchmark ({j.get('when', '?')})"
+    except (OSError, ValueError, KeyError):
+        return FP64_PEAK_TFLOPS_NOMINAL, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
+def roofline_leg(uk, step, pr, res, world):
+    """Average duration of the dominant kernel measured live with CUDA events on its
+    stream over one profiled step; algorithmic FLOPs per launch = points x (2m)^d x 2
+    (one FMA per window tap) per spread or gather pass."""
+    import torch
+    uk.profile_reset()
+    uk.profile_enable(True)
+    step()
+    torch.cuda.synchronize()
+    prof = uk.profile_read()
+    uk.profile_enable(False)
+    uk.profile_reset()
+    taps = (2 * res.info["m"]) ** pr.d
+    n_local = len(pr.x) // world
+    kern = max(("fused", "spread", "gather"), key=lambda k: prof[k][0])
+    ms, cnt = prof[kern]
+    passes = 2 if kern == "fused" else 1
+    flops = n_local * taps * 2 * passes
+    avg_ms = ms / max(cnt, 1)
+    achieved = flops / (avg_ms / 1e3) / 1e12
+    peak, peak_src = fp64_peak()
+    total = sum(v[0] for v in prof.values())
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            traffic = json.load(f).get(kern)
+    except (OSError, ValueError):
+        pass
+    return {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src + " (FP64 FMA pipe)",
+            "avg_launch_ms": avg_ms, "launches_per_step": cnt, "share_of_step": ms / total if total else None,
+            "per_tag_ms": {k: round(v[0], 3) for k, v in prof.items()}}
+
+
+def e2e_leg(uk, pr, x, a, y, b, comm, barrier, world, dev):
+    import torch
+    hx, ha, hy, hb = (torch.from_numpy(v).pin_memory() for v in (x, a, y, b))
+    opts = {"method": "nfft"}
+    stream = torch.cuda.current_stream()
+    uk.uot_sinkhorn(hx, ha, hy, hb, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm, stream=stream)
+    steps = 2
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        beta, gamma, res = uk.uot_sinkhorn(hx, ha, hy, hb, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm,
+                                           stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    h2d = sum(v.numel() * 8 for v in (hx, ha, hy, hb))
+    d2h = (len(a) + len(b)) * 8 + 8 * 7
+    return {"value": pr.iters * steps / (ms / 1e3), "unit": "iterations/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "path": "uotk_uot_sinkhorn with pinned host buffers (library stages copies)"}
+
+
+def mmd_leg(uk, world, rank, comm, dev, barrier):
+    """MMD^2 evals/s at n=m=1M, d=3 (C2 distributions at the metric's size, Gaussian l=0.05)."""
+    import torch
+    pr = W.c2_mmd(n=1_000_000)
+    x, a, y, b = (torch.from_numpy(shard(v, world, rank)).to(dev) for v in (pr.x, pr.a, pr.y, pr.b))
+    kind, param = pr.kernels[0]
+    opts = {"method": "nfft"}
+    v = uk.mmd2(x, a, y, b, kind, param, opts=opts, comm=comm)
+    steps = 3
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        v = uk.mmd2(x, a, y, b, kind, param, opts=opts, comm=comm)  # returns a host scalar (synchronises)
+    dt = time.perf_counter() - t0
+    return {"metric": "MMD^2 evals/s", "value": steps / dt, "unit": "evals/s", "mmd2": v,
+            "config": "C2 distributions at n=m=1M, d=3, Gaussian exp(-r^2/0.0025), full call incl. setup"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

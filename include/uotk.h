@@ -184,6 +184,15 @@ int uotk_abi_version(void);
 int64_t uotk_launch_counter(void);
 void uotk_launch_counter_reset(void);
 
+/* Live kernel timing for benchmarks.  When enabled, each launch of an instrumented
+ * pass is bracketed by CUDA events recorded on its stream.  Tags: "spread", "gather",
+ * "fused" (d=3 gather-update-spread), "fft" (D2Z + D_k scale + Z2D), "direct",
+ * "setup".  uotk_profile_read synchronises on the recorded events and returns the
+ * summed milliseconds and the number of bracketed launches of one tag. */
+void uotk_profile_enable(int on);
+void uotk_profile_reset(void);
+int uotk_profile_read(const char* tag, double* ms, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

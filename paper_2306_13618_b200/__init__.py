@@ -245,3 +245,26 @@ def launch_counter():
 
 def reset_launch_counter():
     _native.load().uotk_launch_counter_reset()
+
+
+PROFILE_TAGS = ("spread", "gather", "fused", "fft", "direct", "setup")
+
+
+def profile_enable(on=True):
+    """Bracket every instrumented launch with CUDA events on its stream (see uotk.h)."""
+    _native.load().uotk_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    _native.load().uotk_profile_reset()
+
+
+def profile_read():
+    """{tag: (total_ms, launches)} of the bracketed launches since the last reset."""
+    lib = _native.load()
+    out = {}
+    for tag in PROFILE_TAGS:
+        ms, cnt = ctypes.c_double(), ctypes.c_int64()
+        _native.check(lib.uotk_profile_read(tag.encode(), ctypes.byref(ms), ctypes.byref(cnt)))
+        out[tag] = (ms.value, cnt.value)
+    return out

@@ -22,6 +22,7 @@ EXPORTED = (
     "uotk_opts_init", "uotk_kernel_sum", "uotk_uot_sinkhorn", "uotk_mmd2",
     "uotk_comm_unique_id", "uotk_comm_create", "uotk_comm_destroy",
     "uotk_last_error", "uotk_abi_version", "uotk_launch_counter", "uotk_launch_counter_reset",
+    "uotk_profile_enable", "uotk_profile_reset", "uotk_profile_read",
 )
 
 
@@ -99,6 +100,12 @@ def load():
     lib.uotk_launch_counter.restype = I64
     lib.uotk_launch_counter_reset.argtypes = []
     lib.uotk_launch_counter_reset.restype = None
+    lib.uotk_profile_enable.argtypes = [INT]
+    lib.uotk_profile_enable.restype = None
+    lib.uotk_profile_reset.argtypes = []
+    lib.uotk_profile_reset.restype = None
+    lib.uotk_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), ctypes.POINTER(I64)]
+    lib.uotk_profile_read.restype = INT
     _lib = lib
     return lib
 

@@ -5,6 +5,7 @@
 // with partial sums combined in a fixed order (deterministic) before the epilogue.
 #include "common.cuh"
 #include "epilogue.cuh"
+#include "profile.cuh"
 
 namespace uotk {
 
@@ -105,6 +106,7 @@ void direct_sum_epi(int d, int64_t n_src, const double* src, const double* w, in
     DevBuf<double> partial;
     if (nsplit > 1) partial.alloc((size_t)nsplit * n_tgt, s);
     dim3 grid((unsigned)tb, (unsigned)nsplit);
+    ProfScope ps_(kProfDirect, s);
 #define UOTK_DIRECT_LAUNCH(DD)                                                                           \
     direct_k<DD, Epi><<<grid, kDT, 0, s>>>(n_src, src, w, n_tgt, tgt, kind, arg, slice, partial.p, epi, dmax)
     if (d == 1) UOTK_DIRECT_LAUNCH(1);

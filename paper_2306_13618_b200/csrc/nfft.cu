@@ -4,6 +4,7 @@
 // thread-per-point kernels; the tuned d = 3 fused kernels live in fused3d.cu.
 #include "common.cuh"
 #include "epilogue.cuh"
+#include "profile.cuh"
 #include "window.cuh"
 
 namespace uotk {
@@ -138,6 +139,7 @@ __global__ void scale_spectrum_k(double2* __restrict__ spec, const double* __res
 template <int D, int M>
 void spread_dm(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
     KBWindow win = make_window(fp.b, M);
+    ProfScope ps_(kProfSpread, s);
     spread_simple_k<D, M><<<blocks_for(ps.n, 128), 128, 0, s>>>(ps.u.p, w, ps.n, fp.ng, win, grid);
     UOTK_LAUNCHED();
 }
@@ -146,6 +148,7 @@ template <int D, int M, class Epi>
 void gather_dm(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,
                unsigned long long* dmax, cudaStream_t s) {
     KBWindow win = make_window(fp.b, M);
+    ProfScope ps_(kProfGather, s);
     gather_simple_k<D, M, Epi><<<blocks_for(ps.n, 128), 128, 0, s>>>(ps.u.p, ps.n, fp.ng, win, grid, epi, dmax);
     UOTK_LAUNCHED();
 }
@@ -205,6 +208,7 @@ void gather(const PointSet& ps, const double* grid, double* out_sorted, const Fa
 
 void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
+    ProfScope ps_(kProfFft, s);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftSetStream(sp.c2r, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
