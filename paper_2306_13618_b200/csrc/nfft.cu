@@ -10,6 +10,13 @@
 namespace uotk {
 
 void comm_allreduce_spectrum(double2* buf, size_t count, void* comm, cudaStream_t s);  // comm.cu
+// tuned d = 3 passes (fused3d.cu)
+bool fused3d_available(const FastParams& fp);
+void fused3d_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s);
+void fused3d_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
+                          cudaStream_t s);
+void fused3d_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
+                        cudaStream_t s);
 
 namespace {
 
@@ -185,6 +192,10 @@ void gather_dm(const PointSet& ps, const double* grid, const FastParams& fp, con
 
 void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s) {
     if (ps.n == 0) return;
+    if (fused3d_available(fp)) {
+        fused3d_spread(ps, w_sorted, grid, fp, s);
+        return;
+    }
     UOTK_DISPATCH_DM(fp.d, fp.m, (spread_dm<DD, MM>(ps, w_sorted, grid, fp, s)));
 }
 
@@ -192,6 +203,18 @@ template <class Epi>
 void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,
                 unsigned long long* dmax, cudaStream_t s) {
     if (ps.n == 0) return;
+    if constexpr (std::is_same<Epi, EpiStore>::value) {
+        if (fused3d_available(fp)) {
+            fused3d_gather_store(ps, grid, fp, epi, s);
+            return;
+        }
+    }
+    if constexpr (std::is_same<Epi, EpiDot>::value) {
+        if (fused3d_available(fp)) {
+            fused3d_gather_dot(ps, grid, fp, epi, s);
+            return;
+        }
+    }
     UOTK_DISPATCH_DM(fp.d, fp.m, (gather_dm<DD, MM, Epi>(ps, grid, fp, epi, dmax, s)));
 }
 
