@@ -251,7 +251,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         const size_t ge = grid_elems(fp);
         DevBuf<double> grid(ge, s), grid2;
         DevBuf<double2> spec(ns.sp.spec_elems, s);
-        const bool fused = fused3d_available(fp);
+        const bool fused = fused3d_available(fp) && PX.chunked && PY.chunked;
         if (fused) grid2.alloc(ge, s);
         grid.zero();
         spread(PY, wy.p, grid.p, fp, s);  // adjoint NFFT of nu (.) v at y

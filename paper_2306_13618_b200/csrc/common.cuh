@@ -101,6 +101,12 @@ struct PointSet {
     DevBuf<double> u;        // d * n, SoA, grid units: u_t = (x_t - c_t)/h * ng
     DevBuf<int32_t> key;     // n, linear cell key (sorted ascending)
     DevBuf<int32_t> perm;    // n, sorted position -> caller index
+    // chunked layout of the d = 3 cell-group kernels (fused3d.cu): runs of equal keys
+    // split into chunks of <= 32 points, with the window values precomputed per chunk
+    bool chunked = false;
+    int64_t nchunks = 0;
+    DevBuf<int4> chunk_desc;  // {first point, count, key, 0}
+    DevBuf<double> chunk_win; // nchunks x 3 x 32 x 2m window values (zero for empty slots)
 };
 
 // Fourier-side plan: the D_k table and the cuFFT handles.

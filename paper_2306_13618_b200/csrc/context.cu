@@ -64,6 +64,7 @@ template struct DevBuf<uint32_t>;
 template struct DevBuf<int64_t>;
 template struct DevBuf<unsigned long long>;
 template struct DevBuf<uint8_t>;
+template struct DevBuf<int4>;
 
 bool is_device_pointer(const void* ptr) {
     if (!ptr) return false;

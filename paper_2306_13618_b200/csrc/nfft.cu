@@ -192,7 +192,7 @@ void gather_dm(const PointSet& ps, const double* grid, const FastParams& fp, con
 
 void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s) {
     if (ps.n == 0) return;
-    if (fused3d_available(fp)) {
+    if (fused3d_available(fp) && ps.chunked) {
         fused3d_spread(ps, w_sorted, grid, fp, s);
         return;
     }
@@ -204,13 +204,13 @@ void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, co
                 unsigned long long* dmax, cudaStream_t s) {
     if (ps.n == 0) return;
     if constexpr (std::is_same<Epi, EpiStore>::value) {
-        if (fused3d_available(fp)) {
+        if (fused3d_available(fp) && ps.chunked) {
             fused3d_gather_store(ps, grid, fp, epi, s);
             return;
         }
     }
     if constexpr (std::is_same<Epi, EpiDot>::value) {
-        if (fused3d_available(fp)) {
+        if (fused3d_available(fp) && ps.chunked) {
             fused3d_gather_dot(ps, grid, fp, epi, s);
             return;
         }
