@@ -40,6 +40,12 @@ struct EpiSinkhorn {
         if (t_store) t_store[i] = t;
         return dd;
     }
+    // the same next weight without side effects (bit-identical to operator()'s w_next)
+    __device__ __forceinline__ double weight(int64_t i, double t) const {
+        if (!(t > 0.0) || !isfinite(t)) t = 1.0;
+        const double pnew = -c * log(t);
+        return mass[i] * exp(lam * pnew);
+    }
 };
 
 // prod[i] = w[i] * t (MMD^2 quadratic form sum_i w_i (K w)_i, reduced afterwards).

@@ -85,10 +85,12 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
+    // owned columns: (b, c) for b in {cb0, cb0 + 1} (one 16-byte load of Y_p[b..b+1])
     const int cc = tid % kT;
+    const int cb0 = kNJ * (tid / kT);
     int cb[kNJ];
 #pragma unroll
-    for (int j = 0; j < kNJ; ++j) cb[j] = tid / kT + j * (kThreads / kT);
+    for (int j = 0; j < kNJ; ++j) cb[j] = cb0 + j;
 
     const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
     const int64_t cbeg = min((int64_t)blockIdx.x * per, nchunks);
@@ -147,7 +149,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64
                 }
             }
         }
-        if (!GATHER && tid < kChunk) sm.wn[tid] = tid < cnt ? w_in[p0 + tid] : 0.0;
+        double wn_reg;  // spread weight of slot `lane` (broadcast by shuffles in the spread)
         mbar_wait(&sm.bar[buf], (k >> 1) & 1);
         const double(*wx)[kT] = sm.win[buf][0];
         const double(*wy)[kT] = sm.win[buf][1];
@@ -176,9 +178,8 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64
                 }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    double v = 0.0;
-#pragma unroll
-                    for (int j = 0; j < kNJ; ++j) v = fma(e[q][j][0] + e[q][j][1], wy[p + q][cb[j]], v);
+                    const double2 yv = *reinterpret_cast<const double2*>(&wy[p + q][cb0]);
+                    const double v = fma(e[q][0][0] + e[q][0][1], yv.x, (e[q][1][0] + e[q][1][1]) * yv.y);
                     r[p + q] = v * wz[p + q][cc];
                 }
             }
@@ -195,28 +196,35 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64
             }
             sm.red[warp][lane] = r[0];
             __syncthreads();
-            if (warp == 0) {
-                double wn = 0.0;
-                if (lane < cnt) {
-                    double t = 0.0;
+            // every warp sums the 4 warp partials of slot `lane`; warp 0 applies the
+            // epilogue (writes), the others evaluate the same update to obtain the
+            // spread weight in registers — no second barrier
+            double wn = 0.0;
+            if (lane < cnt) {
+                double t = 0.0;
 #pragma unroll
-                    for (int w = 0; w < kThreads / 32; ++w) t += sm.red[w][lane];
+                for (int w = 0; w < kThreads / 32; ++w) t += sm.red[w][lane];
+                if (warp == 0) {
                     const double dd = epi(p0 + lane, t);
                     ddmax = fmax(ddmax, dd);
                     if (SPREAD) wn = epi.w_next[p0 + lane];
+                } else if (SPREAD) {
+                    wn = epi.weight(p0 + lane, t);
                 }
-                if (SPREAD) sm.wn[lane] = wn;
             }
+            wn_reg = wn;
+        } else {
+            wn_reg = (lane < cnt) ? w_in[p0 + lane] : 0.0;
         }
-        __syncthreads();
 
         if (SPREAD) {
 #pragma unroll 2
             for (int p = 0; p < kChunk; ++p) {
-                const double wzp = sm.wn[p] * wz[p][cc];
+                const double wzp = __shfl_sync(0xffffffffu, wn_reg, p) * wz[p][cc];
+                const double2 yv = *reinterpret_cast<const double2*>(&wy[p][cb0]);
                 double wj[kNJ];
-#pragma unroll
-                for (int j = 0; j < kNJ; ++j) wj[j] = wzp * wy[p][cb[j]];
+                wj[0] = wzp * yv.x;
+                wj[1] = wzp * yv.y;
 #pragma unroll
                 for (int a = 0; a < kT; a += 2) {
                     const double2 xv = *reinterpret_cast<const double2*>(&wx[p][a]);
@@ -290,14 +298,16 @@ __global__ void chunk_window_k(const int4* __restrict__ desc, const double* __re
 
 inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
 
-// The Sinkhorn epilogue exposes w_next; the plain gathers do not spread.
+// The Sinkhorn epilogue exposes w_next / weight(); the plain gathers do not spread.
 struct EpiNone {
     double* w_next = nullptr;
     __device__ double operator()(int64_t, double) const { return 0.0; }
+    __device__ double weight(int64_t, double) const { return 0.0; }
 };
 template <class Epi>
 struct EpiGatherOnly : Epi {
     double* w_next = nullptr;
+    __device__ double weight(int64_t, double) const { return 0.0; }
 };
 
 template <int MODE, class Epi>
