@@ -107,6 +107,8 @@ struct PointSet {
     int64_t nchunks = 0;
     DevBuf<int4> chunk_desc;  // {first point, count, key, 0}
     DevBuf<double> chunk_win; // nchunks x 3 x 32 x 2m window values (zero for empty slots)
+    DevBuf<int32_t> chunk_bounds;  // chunk_blocks + 1 cost-balanced CTA boundaries
+    int chunk_blocks = 0;
 };
 
 // Fourier-side plan: the D_k table and the cuFFT handles.

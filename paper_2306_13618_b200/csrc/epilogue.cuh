@@ -12,6 +12,7 @@ struct EpiStore {
         out[perm ? perm[i] : i] = t;
         return 0.0;
     }
+    __device__ __forceinline__ void prefetch(int64_t) const {}
 };
 
 // One Sinkhorn half-step, (3.3) / (3.4) in scaling form:
@@ -40,6 +41,10 @@ struct EpiSinkhorn {
         if (t_store) t_store[i] = t;
         return dd;
     }
+    __device__ __forceinline__ void prefetch(int64_t i) const {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(mass + i));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pot + i));
+    }
     // the same next weight without side effects (bit-identical to operator()'s w_next)
     __device__ __forceinline__ double weight(int64_t i, double t) const {
         if (!(t > 0.0) || !isfinite(t)) t = 1.0;
@@ -56,6 +61,7 @@ struct EpiDot {
         prod[i] = w[i] * t;
         return 0.0;
     }
+    __device__ __forceinline__ void prefetch(int64_t) const {}
 };
 
 // warp max of non-negative doubles, one atomicMax per warp on the uint64 bit pattern

@@ -75,9 +75,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
 template <int MODE, class Epi>
 __global__ void __launch_bounds__(kThreads, kBlocksPerSM)
-chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64_t nchunks, int ng,
-            const double* __restrict__ grid_in, double* __restrict__ grid_out, const double* __restrict__ w_in,
-            Epi epi, unsigned long long* dmax) {
+chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
+            int64_t nchunks, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
+            const double* __restrict__ w_in, Epi epi, unsigned long long* dmax) {
     constexpr bool GATHER = MODE != 1;
     constexpr bool SPREAD = MODE != 2;
     __shared__ Smem sm;
@@ -92,10 +92,11 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) cb[j] = cb0 + j;
 
-    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-    const int64_t cbeg = min((int64_t)blockIdx.x * per, nchunks);
-    const int64_t cend = min(cbeg + per, nchunks);
+    // cost-balanced contiguous chunk range of this CTA (fused3d_prepare)
+    const int64_t cbeg = bounds[blockIdx.x];
+    const int64_t cend = bounds[blockIdx.x + 1];
     const int64_t ng2 = (int64_t)ng * ng;
+    (void)nchunks;
 
     if (tid == 0) {
         mbar_init(&sm.bar[0], 1);
@@ -146,6 +147,25 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, int64
                 for (int a = 0; a < kT; ++a) {
                     if (GATHER) g[j][a] = __ldg(grid_in + col + a * ng2);
                     if (SPREAD) s[j][a] = 0.0;
+                }
+            }
+        }
+        if (GATHER) {
+            // warm L1 with the epilogue's per-point inputs and, at a group boundary, with
+            // the next group's footprint columns (hides their latency behind this chunk)
+            if (lane < cnt) epi.prefetch(p0 + lane);
+            if (c + 1 < cend) {
+                const int32_t nkey = desc[c + 1].z;
+                if (nkey != key) {
+                    const int n2 = nkey % ng, n1 = (nkey / ng) % ng, n0 = nkey / ng2;
+                    const int64_t nbase = ((int64_t)(n0 - kM + 1) * ng + (n1 - kM + 1)) * ng + (n2 - kM + 1);
+#pragma unroll
+                    for (int j = 0; j < kNJ; ++j) {
+                        const double* colp = grid_in + nbase + (int64_t)cb[j] * ng + cc;
+#pragma unroll
+                        for (int a = 0; a < kT; ++a)
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(colp + a * ng2));
+                    }
                 }
             }
         }
@@ -296,6 +316,32 @@ __global__ void chunk_window_k(const int4* __restrict__ desc, const double* __re
     }
 }
 
+// cost of a chunk for the static partition: 8 per chunk + 2 when it opens a cell group
+// (footprint load and flush), in units of 1/8 chunk
+__global__ void chunk_cost_k(const int4* __restrict__ desc, int64_t nchunks, int32_t* __restrict__ cost) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < nchunks) cost[c] = 8 + ((c == 0 || desc[c].z != desc[c - 1].z) ? 2 : 0);
+}
+
+// bounds[b] = first chunk whose inclusive cost prefix exceeds b * total / nb
+__global__ void chunk_bounds_k(const int32_t* __restrict__ prefix, int64_t nchunks, int nb,
+                               int32_t* __restrict__ bounds) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    if (b == nb) {
+        bounds[b] = (int32_t)nchunks;
+        return;
+    }
+    const double target = (double)prefix[nchunks - 1] * b / nb;
+    int64_t lo = 0, hi = nchunks;  // first c with prefix[c] > target
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if ((double)prefix[mid] > target) hi = mid;
+        else lo = mid + 1;
+    }
+    bounds[b] = (int32_t)(b == 0 ? 0 : lo);
+}
+
 inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
 
 // The Sinkhorn epilogue exposes w_next / weight(); the plain gathers do not spread.
@@ -303,6 +349,7 @@ struct EpiNone {
     double* w_next = nullptr;
     __device__ double operator()(int64_t, double) const { return 0.0; }
     __device__ double weight(int64_t, double) const { return 0.0; }
+    __device__ void prefetch(int64_t) const {}
 };
 template <class Epi>
 struct EpiGatherOnly : Epi {
@@ -314,11 +361,10 @@ template <int MODE, class Epi>
 void launch(const PointSet& ps, const double* gin, double* gout, const double* w, const FastParams& fp,
             const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
     if (ps.n == 0 || ps.nchunks == 0) return;
-    int blocks = 148 * kBlocksPerSM;
-    if (ps.nchunks < blocks) blocks = (int)ps.nchunks;
     ProfScope prof(tag, s);
-    chunked3d_k<MODE, Epi><<<blocks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p, ps.nchunks, fp.ng, gin,
-                                                       gout, w, epi, dmax);
+    chunked3d_k<MODE, Epi><<<ps.chunk_blocks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                ps.chunk_bounds.p, ps.nchunks, fp.ng, gin, gout,
+                                                                w, epi, dmax);
     UOTK_LAUNCHED();
 }
 
@@ -368,6 +414,26 @@ void fused3d_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
         chunk_window_k<<<(unsigned)nchunks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
         UOTK_LAUNCHED();
     }
+    // cost-balanced static partition of the chunks over the CTAs
+    int sms = 148;
+    {
+        int dev = 0;
+        UOTK_CUDA(cudaGetDevice(&dev));
+        UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int nb = (int)std::min<int64_t>((int64_t)sms * kBlocksPerSM, nchunks);
+    DevBuf<int32_t> cost(nchunks, s), prefix(nchunks, s);
+    chunk_cost_k<<<blocks_for(nchunks, 256), 256, 0, s>>>(ps.chunk_desc.p, nchunks, cost.p);
+    UOTK_LAUNCHED();
+    size_t t4 = 0;
+    UOTK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t4, cost.p, prefix.p, (int)nchunks, s));
+    DevBuf<uint8_t> tmp2(t4, s);
+    UOTK_CUDA(cub::DeviceScan::InclusiveSum(tmp2.p, t4, cost.p, prefix.p, (int)nchunks, s));
+    add_launches(1);
+    ps.chunk_bounds.alloc(nb + 1, s);
+    chunk_bounds_k<<<blocks_for(nb + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nb, ps.chunk_bounds.p);
+    UOTK_LAUNCHED();
+    ps.chunk_blocks = nb;
     ps.nchunks = nchunks;
     ps.chunked = true;
 }
