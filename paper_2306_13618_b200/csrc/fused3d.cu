@@ -73,12 +73,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
-// Thread -> footprint ownership (128 threads): warp w handles the a-half ah = w >> 1
-// (a in [8 ah, 8 ah + 8)); within the two warps of a half, the 64 (b-pair, c-pair)
-// blocks bp = combo >> 3, cp = combo & 7 (combo = (w & 1) * 32 + lane).  A thread owns
-// the 4 columns (b, c) in {2bp, 2bp+1} x {2cp, 2cp+1} for its 8 values of a: per point it
-// needs 4 + 1 + 1 sixteen-byte window loads (X half, Y pair, Z pair) for 32 FMAs, and the
-// X loads are warp-uniform (shared-memory broadcasts).
 template <int MODE, class Epi>
 __global__ void __launch_bounds__(kThreads, kBlocksPerSM)
 chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
@@ -86,17 +80,17 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             const double* __restrict__ w_in, Epi epi, unsigned long long* dmax) {
     constexpr bool GATHER = MODE != 1;
     constexpr bool SPREAD = MODE != 2;
-    constexpr int kA = kT / 2;  // a-values per thread
     __shared__ Smem sm;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int a0 = (warp >> 1) * kA;
-    const int combo = (warp & 1) * 32 + lane;
-    const int b0 = 2 * (combo >> 3);
-    const int c0 = 2 * (combo & 7);
-    // column j = 2 * bi + ci  ->  (b0 + bi, c0 + ci)
+    // owned columns: (b, c) for b in {cb0, cb0 + 1} (one 16-byte load of Y_p[b..b+1])
+    const int cc = tid % kT;
+    const int cb0 = kNJ * (tid / kT);
+    int cb[kNJ];
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) cb[j] = cb0 + j;
 
     // cost-balanced contiguous chunk range of this CTA (fused3d_prepare)
     const int64_t cbeg = bounds[blockIdx.x];
@@ -117,16 +111,11 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         }
     }
 
-    double g[4][kA];  // footprint of the current group (gather source)
-    double s[4][kA];  // spread accumulators of the current group
+    double g[kNJ][kT];  // footprint of the current group (gather source)
+    double s[kNJ][kT];  // spread accumulators of the current group
     int32_t cur_key = -1;
-    int64_t gbase = 0;  // grid index of footprint (a, b, c) = (a0, b0, c0)
+    int64_t gbase = 0;
     double ddmax = 0.0;
-
-    auto origin = [&](int32_t kk) -> int64_t {
-        const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
-        return ((int64_t)(k0 - kM + 1 + a0) * ng + (k1 - kM + 1 + b0)) * ng + (k2 - kM + 1 + c0);
-    };
 
     for (int64_t c = cbeg; c < cend; ++c) {
         const int k = (int)(c - cbeg);
@@ -139,21 +128,24 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         if (key != cur_key) {
             if (SPREAD && cur_key >= 0) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    double* col = grid_out + gbase + (int64_t)(j >> 1) * ng + (j & 1);
+                for (int j = 0; j < kNJ; ++j) {
+                    const int64_t col = gbase + (int64_t)cb[j] * ng + cc;
 #pragma unroll
-                    for (int a = 0; a < kA; ++a)
-                        if (s[j][a] != 0.0) atomicAdd(col + a * ng2, s[j][a]);
+                    for (int a = 0; a < kT; ++a)
+                        if (s[j][a] != 0.0) atomicAdd(grid_out + col + a * ng2, s[j][a]);
                 }
             }
             cur_key = key;
-            gbase = origin(key);
+            const int c2 = key % ng;
+            const int c1 = (key / ng) % ng;
+            const int c0 = key / ng2;
+            gbase = ((int64_t)(c0 - kM + 1) * ng + (c1 - kM + 1)) * ng + (c2 - kM + 1);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double* col = grid_in + gbase + (int64_t)(j >> 1) * ng + (j & 1);
+            for (int j = 0; j < kNJ; ++j) {
+                const int64_t col = gbase + (int64_t)cb[j] * ng + cc;
 #pragma unroll
-                for (int a = 0; a < kA; ++a) {
-                    if (GATHER) g[j][a] = __ldg(col + a * ng2);
+                for (int a = 0; a < kT; ++a) {
+                    if (GATHER) g[j][a] = __ldg(grid_in + col + a * ng2);
                     if (SPREAD) s[j][a] = 0.0;
                 }
             }
@@ -165,12 +157,13 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             if (c + 1 < cend) {
                 const int32_t nkey = desc[c + 1].z;
                 if (nkey != key) {
-                    const int64_t nbase = origin(nkey);
+                    const int n2 = nkey % ng, n1 = (nkey / ng) % ng, n0 = nkey / ng2;
+                    const int64_t nbase = ((int64_t)(n0 - kM + 1) * ng + (n1 - kM + 1)) * ng + (n2 - kM + 1);
 #pragma unroll
-                    for (int bi = 0; bi < 2; ++bi) {
-                        const double* colp = grid_in + nbase + (int64_t)bi * ng;
+                    for (int j = 0; j < kNJ; ++j) {
+                        const double* colp = grid_in + nbase + (int64_t)cb[j] * ng + cc;
 #pragma unroll
-                        for (int a = 0; a < kA; ++a)
+                        for (int a = 0; a < kT; ++a)
                             asm volatile("prefetch.global.L1 [%0];" ::"l"(colp + a * ng2));
                     }
                 }
@@ -186,33 +179,28 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             double r[kChunk];
 #pragma unroll
             for (int p = 0; p < kChunk; p += 2) {
-                double e[2][4];
+                double e[2][kNJ][2];
 #pragma unroll
                 for (int q = 0; q < 2; ++q)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) e[q][j] = 0.0;
+                    for (int j = 0; j < kNJ; ++j) e[q][j][0] = e[q][j][1] = 0.0;
 #pragma unroll
-                for (int a = 0; a < kA; a += 2) {
-                    const double2 x0 = *reinterpret_cast<const double2*>(&wx[p][a0 + a]);
-                    const double2 x1 = *reinterpret_cast<const double2*>(&wx[p + 1][a0 + a]);
+                for (int a = 0; a < kT; a += 2) {
+                    const double2 x0 = *reinterpret_cast<const double2*>(&wx[p][a]);
+                    const double2 x1 = *reinterpret_cast<const double2*>(&wx[p + 1][a]);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        e[0][j] = fma(g[j][a], x0.x, e[0][j]);
-                        e[1][j] = fma(g[j][a], x1.x, e[1][j]);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        e[0][j] = fma(g[j][a + 1], x0.y, e[0][j]);
-                        e[1][j] = fma(g[j][a + 1], x1.y, e[1][j]);
+                    for (int j = 0; j < kNJ; ++j) {
+                        e[0][j][0] = fma(g[j][a], x0.x, e[0][j][0]);
+                        e[0][j][1] = fma(g[j][a + 1], x0.y, e[0][j][1]);
+                        e[1][j][0] = fma(g[j][a], x1.x, e[1][j][0]);
+                        e[1][j][1] = fma(g[j][a + 1], x1.y, e[1][j][1]);
                     }
                 }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const double2 yv = *reinterpret_cast<const double2*>(&wy[p + q][b0]);
-                    const double2 zv = *reinterpret_cast<const double2*>(&wz[p + q][c0]);
-                    const double v0 = fma(e[q][0], yv.x, e[q][2] * yv.y);  // c = c0
-                    const double v1 = fma(e[q][1], yv.x, e[q][3] * yv.y);  // c = c0 + 1
-                    r[p + q] = fma(v0, zv.x, v1 * zv.y);
+                    const double2 yv = *reinterpret_cast<const double2*>(&wy[p + q][cb0]);
+                    const double v = fma(e[q][0][0] + e[q][0][1], yv.x, (e[q][1][0] + e[q][1][1]) * yv.y);
+                    r[p + q] = v * wz[p + q][cc];
                 }
             }
             // transposing butterfly: lane l ends with this warp's sum for slot l
@@ -252,27 +240,23 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         if (SPREAD) {
 #pragma unroll 2
             for (int p = 0; p < kChunk; ++p) {
-                const double wp = __shfl_sync(0xffffffffu, wn_reg, p);
-                const double2 yv = *reinterpret_cast<const double2*>(&wy[p][b0]);
-                const double2 zv = *reinterpret_cast<const double2*>(&wz[p][c0]);
-                const double z0 = wp * zv.x, z1 = wp * zv.y;
-                double wj[4];
-                wj[0] = yv.x * z0;
-                wj[1] = yv.x * z1;
-                wj[2] = yv.y * z0;
-                wj[3] = yv.y * z1;
+                const double wzp = __shfl_sync(0xffffffffu, wn_reg, p) * wz[p][cc];
+                const double2 yv = *reinterpret_cast<const double2*>(&wy[p][cb0]);
+                double wj[kNJ];
+                wj[0] = wzp * yv.x;
+                wj[1] = wzp * yv.y;
 #pragma unroll
-                for (int a = 0; a < kA; a += 2) {
-                    const double2 xv = *reinterpret_cast<const double2*>(&wx[p][a0 + a]);
+                for (int a = 0; a < kT; a += 2) {
+                    const double2 xv = *reinterpret_cast<const double2*>(&wx[p][a]);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int j = 0; j < kNJ; ++j) {
                         s[j][a] = fma(wj[j], xv.x, s[j][a]);
                         s[j][a + 1] = fma(wj[j], xv.y, s[j][a + 1]);
                     }
                 }
             }
         }
-        __syncthreads();  // every thread is done with win[buf] and red
+        __syncthreads();  // every thread is done with win[buf] and wn
         if (tid == 0 && c + 2 < cend) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&sm.bar[buf], kWinBytes);
@@ -281,11 +265,11 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     }
     if (SPREAD && cur_key >= 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            double* col = grid_out + gbase + (int64_t)(j >> 1) * ng + (j & 1);
+        for (int j = 0; j < kNJ; ++j) {
+            const int64_t col = gbase + (int64_t)cb[j] * ng + cc;
 #pragma unroll
-            for (int a = 0; a < kA; ++a)
-                if (s[j][a] != 0.0) atomicAdd(col + a * ng2, s[j][a]);
+            for (int a = 0; a < kT; ++a)
+                if (s[j][a] != 0.0) atomicAdd(grid_out + col + a * ng2, s[j][a]);
         }
     }
     if (GATHER && warp == 0) warp_max_atomic(dmax, ddmax);
