@@ -227,10 +227,11 @@ class Comm:
     @classmethod
     def from_torch_distributed(cls):
         import torch.distributed as dist
+
+        from .dist import broadcast_bytes
         rank, world = dist.get_rank(), dist.get_world_size()
-        obj = [cls.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        return cls(obj[0], world, rank)
+        uid = broadcast_bytes(cls.unique_id() if rank == 0 else None)
+        return cls(uid, world, rank)
 
     def close(self):
         if self.handle:

@@ -97,7 +97,7 @@ def launch_list(path, out):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = re.sub(r"\(.*", "", r[ki])[:90]
         tot[name] += v
         cnt[name] += 1

@@ -208,3 +208,27 @@ def test_mmd2_identities(uk):
                     opts={"method": method})
         r2 = float(np.sum((x[0] - x[1]) ** 2))
         assert abs(v - (2 - 2 * np.exp(-r2 / 0.0025))) <= 1e-9
+
+
+# ------------------------------------------------------------------ NCCL exchange path
+def test_one_rank_nccl_communicator_matches(uk):
+    """The multi-GPU code path (bbox min/max, per-sum spectrum all-reduce, scalar sums)
+    through a real 1-rank NCCL communicator gives the single-GPU results."""
+    comm = uk.Comm(uk.Comm.unique_id(), 1, 0)
+    try:
+        pr = W.random_sum(3, 3001, 1999, kind=W.GAUSS, param=0.0025, seed=9)
+        a = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"})
+        b = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"},
+                          comm=comm)
+        assert torch.equal(a, b)
+        u = W.c3_uot(n=1500, m=1300, iters=5)
+        r1 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5)
+        r2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, comm=comm)
+        assert torch.equal(r1[0], r2[0]) and torch.equal(r1[1], r2[1])
+        assert r1[2].primal == r2[2].primal
+        m = W.c2_mmd(n=2000, m=1800)
+        v1 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts={"method": "nfft"})
+        v2 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts={"method": "nfft"}, comm=comm)
+        assert v1 == v2
+    finally:
+        comm.close()
