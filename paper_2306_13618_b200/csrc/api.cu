@@ -19,6 +19,9 @@ void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, c
 int comm_nranks(void* comm);
 void ensure_pool();
 
+void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
+                     void* comm);  // nfft.cu
+
 // Optimised NFFT half-step for d = 3 (fused3d.cu); returns false if not applicable.
 bool fused3d_available(const FastParams& fp);
 void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
@@ -370,22 +373,25 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     if (method == UOTK_DIRECT) {
         fill_info(info, method, nullptr);
         direct_sum_epi(d, nz, z.p, w.p, nz, z.p, kind, param, EpiDot{w.p, prod.p}, nullptr, s);
+        sum_columns(prod.p, nz, 1, sum.p, s);
     } else {
+        // spread w on the grid, FFT, and sum_k D_k |G_k|^2 (= sum_i w_i t_i of the gather
+        // form exactly; no inverse FFT or interpolation needed).  With a communicator the
+        // spectrum is all-reduced first, so every rank forms the same global value.
         NfftSetup ns;
         setup_nfft(ns, d, kind, param, z.p, nz, nullptr, 0, o, comm, s);
         fill_info(info, method, &ns.fp);
         PointSet PZ;
         make_pointset(PZ, z.p, nz, ns.fp, s);
-        DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s);
+        constexpr int kParts = 296;
+        DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s), part(kParts, s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
         permute_values(ws.p, w.p, PZ.perm.p, nz, s);
         grid.zero();
         spread(PZ, ws.p, grid.p, ns.fp, s);
-        fft_chain(ns.sp, grid.p, spec.p, s, comm);
-        gather_epi(PZ, grid.p, ns.fp, EpiDot{ws.p, prod.p}, nullptr, s);
+        spectrum_energy(ns.sp, grid.p, spec.p, part.p, kParts, s, comm);
+        sum_columns(part.p, kParts, 1, sum.p, s);
     }
-    sum_columns(prod.p, nz, 1, sum.p, s);
-    if (comm) comm_allreduce(sum.p, 1, 0, comm, s);
     UOTK_CUDA(cudaMemcpyAsync(mmd2, sum.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     UOTK_CUDA(cudaStreamSynchronize(s));
 }

@@ -244,4 +244,63 @@ void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, vo
     UOTK_CUFFT(cufftExecZ2D(sp.c2r, (cufftDoubleComplex*)spec, grid));
 }
 
+namespace {
+
+// partial sums of  sum_k D_k |G_k|^2  over the half spectrum (weight 2 for the
+// conjugate-symmetric interior of the last axis, 1 for k_last = 0 and n_g/2)
+template <int D>
+__global__ void spectrum_energy_k(const double2* __restrict__ spec, const double* __restrict__ Dk, int ng, int N,
+                                  int64_t total, double* __restrict__ part) {
+    __shared__ double sm[256];
+    double acc = 0.0;
+    const int nh = ng / 2 + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rem = i / nh;
+        const int kl = (int)(i % nh);
+        bool inside = kl <= N / 2;
+        int64_t didx = kl;
+        int64_t dstride = N / 2 + 1;
+#pragma unroll
+        for (int t = D - 2; t >= 0; --t) {
+            const int q = (int)(rem % ng);
+            rem /= ng;
+            const int k = q < ng / 2 ? q : q - ng;
+            inside = inside && (k >= -N / 2) && (k <= N / 2);
+            didx += (int64_t)(k + N / 2) * dstride;
+            dstride *= (N + 1);
+        }
+        if (inside) {
+            const double2 v = spec[i];
+            const double wgt = (kl == 0 || 2 * kl == ng) ? 1.0 : 2.0;
+            acc += wgt * Dk[didx] * (v.x * v.x + v.y * v.y);
+        }
+    }
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+}  // namespace
+
+// <g', g> for g' = the NFFT interpolant of the spread grid g: the quadratic form
+// sum_ij w_i w_j K_RK(z_i - z_j) of (3.5) in the Fourier domain, sum_k D_k |G_k|^2
+// (identical to spreading, FFT, D_k, inverse FFT, gathering and summing w_i t_i).
+void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
+                     void* comm) {
+    const FastParams& fp = sp.fp;
+    ProfScope ps_(kProfFft, s);
+    UOTK_CUFFT(cufftSetStream(sp.r2c, s));
+    UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
+    if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
+    const int64_t total = (int64_t)sp.spec_elems;
+    if (fp.d == 1) spectrum_energy_k<1><<<nparts, 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total, part);
+    else if (fp.d == 2) spectrum_energy_k<2><<<nparts, 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total, part);
+    else spectrum_energy_k<3><<<nparts, 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total, part);
+    UOTK_LAUNCHED();
+}
+
 }  // namespace uotk

@@ -222,13 +222,44 @@ def test_one_rank_nccl_communicator_matches(uk):
                           comm=comm)
         assert torch.equal(a, b)
         u = W.c3_uot(n=1500, m=1300, iters=5)
-        r1 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5)
-        r2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, comm=comm)
+        nf = {"method": "nfft"}
+        r1 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf)
+        r2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf, comm=comm)
         assert torch.equal(r1[0], r2[0]) and torch.equal(r1[1], r2[1])
         assert r1[2].primal == r2[2].primal
         m = W.c2_mmd(n=2000, m=1800)
-        v1 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts={"method": "nfft"})
-        v2 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts={"method": "nfft"}, comm=comm)
+        v1 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts=nf)
+        v2 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts=nf, comm=comm)
         assert v1 == v2
     finally:
         comm.close()
+
+
+# ------------------------------------------------------------------ full-size cross-checks
+def test_uot_c3_full_size_nfft_vs_direct(uk):
+    """C3 at full size (n = m = 1e6): the NFFT path as bench.py runs it against the GPU
+    direct kernel (K6, itself oracle-validated above) for 2 iterations (1e12 pairs/sum)."""
+    pr = W.c3_uot(iters=2)
+    args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
+    b1, g1, r1 = uk.uot_sinkhorn(*args, iters=2, opts={"method": "nfft"})
+    b2, g2, r2 = uk.uot_sinkhorn(*args, iters=2, opts={"method": "direct"})
+    resid = float(torch.linalg.norm(b1 - b2) / torch.linalg.norm(b2) + torch.linalg.norm(g1 - g2) / torch.linalg.norm(g2))
+    assert resid <= 1e-8, resid
+    assert abs(r1.primal - r2.primal) <= 1e-8 * abs(r2.primal)
+    assert abs(r1.dual - r2.dual) <= 1e-8 * abs(r2.dual)
+    assert abs(r1.plan_mass - r2.plan_mass) <= 1e-8 * r2.plan_mass
+
+
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+def test_mmd2_c2_full_size_nfft_vs_direct(uk, kind):
+    """C2 at full size (n = m = 1e5, 4e10 pairs): Fourier-domain NFFT MMD^2 vs the GPU
+    direct kernel, with the cancellation-aware denominator of reading R13."""
+    pr = W.c2_mmd()
+    param = dict(pr.kernels)[kind]
+    x, a, y, b = cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b)
+    v1, info = uk.mmd2(x, a, y, b, kind, param, opts={"method": "nfft"}, return_info=True)
+    v2 = uk.mmd2(x, a, y, b, kind, param, opts={"method": "direct"})
+    xx = uk.mmd2(x, a, x[:0], b[:0], kind, param, opts={"method": "direct"})
+    yy = uk.mmd2(y, b, y[:0], b[:0], kind, param, opts={"method": "direct"})
+    denom = max(abs(v2), 1e-3 * (abs(xx) + abs(yy)))
+    assert abs(v1 - v2) / denom <= 1e-8, (v1, v2, info)
