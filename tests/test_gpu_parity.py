@@ -213,24 +213,30 @@ def test_mmd2_identities(uk):
 # ------------------------------------------------------------------ NCCL exchange path
 def test_one_rank_nccl_communicator_matches(uk):
     """The multi-GPU code path (bbox min/max, per-sum spectrum all-reduce, scalar sums)
-    through a real 1-rank NCCL communicator gives the single-GPU results."""
+    through a real 1-rank NCCL communicator gives the single-GPU results (up to the
+    summation order of the fp64 atomics that flush the spread, ~1e-16 relative)."""
     comm = uk.Comm(uk.Comm.unique_id(), 1, 0)
+
+    def close(p, q, tol=1e-13):
+        p, q = torch.as_tensor(p, dtype=torch.float64), torch.as_tensor(q, dtype=torch.float64)
+        return bool(torch.max(torch.abs(p - q)) <= tol * torch.max(torch.abs(q)))
+
     try:
         pr = W.random_sum(3, 3001, 1999, kind=W.GAUSS, param=0.0025, seed=9)
         a = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"})
         b = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"},
                           comm=comm)
-        assert torch.equal(a, b)
+        assert close(a, b)
         u = W.c3_uot(n=1500, m=1300, iters=5)
         nf = {"method": "nfft"}
         r1 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf)
         r2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf, comm=comm)
-        assert torch.equal(r1[0], r2[0]) and torch.equal(r1[1], r2[1])
-        assert r1[2].primal == r2[2].primal
+        assert close(r1[0], r2[0], 1e-12) and close(r1[1], r2[1], 1e-12)
+        assert close(r1[2].primal, r2[2].primal)
         m = W.c2_mmd(n=2000, m=1800)
         v1 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts=nf)
         v2 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts=nf, comm=comm)
-        assert v1 == v2
+        assert close(v1, v2, 1e-12)
     finally:
         comm.close()
 
