@@ -1,21 +1,27 @@
-// Tuned d = 3 NFFT passes.
+// Tuned d = 3 NFFT passes on the FP64 tensor cores (DESIGN.md §7 "cell-group kernel").
 //
 // Points are sorted by grid cell (points.cu), so every run of equal keys shares one
-// (2m)^3 window footprint on the oversampled grid.  Runs are cut into chunks of <= 32
-// points and the window values of every chunk (3 axes x 32 slots x 2m taps, zero for
-// empty slots) are computed ONCE per point set (fused3d_prepare) — the points do not
-// move between Sinkhorn iterations.  A 128-thread CTA then walks a contiguous,
-// chunk-balanced range of chunks, streaming each chunk's 12 KB window block into
-// shared memory with a TMA bulk copy (cp.async.bulk + mbarrier, double buffered).
-// For each cell group the threads own fixed footprint columns (b, c) x all 2m values
-// of a, so that
-//   gather  (outer sum of (4.6)):  t_p = sum_abc g[a,b,c] X_p[a] Y_p[b] Z_p[c]
-//   spread  (inner sum of (4.6)):  S[a,b,c] += w_p X_p[a] Y_p[b] Z_p[c]
-// are register-blocked FMA loops (window values broadcast from shared memory).  The
-// per-point partial gathers are reduced with a transposing warp butterfly and a
-// 4-warp shared-memory sum, the Sinkhorn update (3.3)/(3.4) runs on t_p, and the new
-// weight w_p = mass_p u_p is spread into registers at once — one pass over the points
-// per half-step; the footprint is read once and flushed once (fp64 RED) per group.
+// 16^3 window footprint on the oversampled grid (m = 8, 2m taps per axis).  Runs are cut
+// into chunks of <= 32 points and the window values of every chunk (3 axes x 32 slots x
+// 16 taps, zero for empty slots) are computed ONCE per point set (fused3d_prepare) —
+// points do not move between Sinkhorn iterations.  A 128-thread CTA walks a contiguous,
+// cost-balanced range of chunks, streaming each chunk's window block into shared memory
+// with a TMA bulk copy (cp.async.bulk + mbarrier, double buffered).
+//
+// Per chunk, with X_p, Y_p, Z_p the windows of point p along the three axes and F the
+// group's footprint (outer / inner sums of (4.6)):
+//   gather  t_p = sum_a X_p[a] sum_b Y_p[b] sum_c F[a,b,c] Z_p[c]
+//           -> the c-contraction is a GEMM  G[p,(a,b)] = sum_c Z[p,c] F[(a,b),c]  (32x256x16)
+//              on DMMA (mma.sync.m8n8k4.f64); b and a are contracted per point in registers
+//   spread  S[(a,b),c] += sum_p (X_p[a] Y_p[b]) (w_p Z_p[c])        (GEMM 256x16x32 on DMMA)
+// Warp w owns the a-quarter {4w..4w+3}: its F (gather B operand) and S (spread
+// accumulators) stay in registers for the whole cell group — the footprint is read once
+// and flushed once (fp64 RED) per group.  Between the two GEMMs the per-warp partial
+// gathers are summed in shared memory, every warp evaluates the Sinkhorn update (3.3)/
+// (3.4) for the 32 slots (warp 0 writes the potentials), and the new weights are
+// broadcast by shuffles into the spread's B operand: one pass over the points per
+// half-step.  On B200 DMMA runs at the full FP64 rate (37 TFLOP/s measured,
+// scripts/dmma_probe.cu) from 1/8 of the instructions of a DFMA formulation.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -27,20 +33,19 @@ namespace uotk {
 
 namespace {
 
-constexpr int kM = 8;                  // window half-width of the tuned kernels
-constexpr int kT = 2 * kM;             // taps per axis
-constexpr int kThreads = 128;          // 4 warps
-constexpr int kChunk = 32;             // points per chunk (one per lane in the butterfly)
-constexpr int kNJ = kT * kT / kThreads;  // owned (b, c) columns per thread
-constexpr int kWinDoubles = 3 * kChunk * kT;
-constexpr uint32_t kWinBytes = kWinDoubles * sizeof(double);  // 12 KB
+constexpr int kM = 8;               // window half-width of the tuned kernels
+constexpr int kT = 2 * kM;          // taps per axis
+constexpr int kThreads = 128;       // 4 warps
+constexpr int kChunk = 32;          // points per chunk
+constexpr int kStride = 20;         // padded row stride (doubles) of a window matrix: conflict-free fragments
+constexpr int kWinDoubles = 3 * kChunk * kStride;
+constexpr uint32_t kWinBytes = kWinDoubles * sizeof(double);  // 15 KB
 constexpr int kBlocksPerSM = 2;
 
 struct __align__(128) Smem {
-    double win[2][3][kChunk][kT];  // double-buffered window blocks (TMA destination)
-    double wn[kChunk];             // spread weights of the chunk
-    double red[kThreads / 32][kChunk];
-    unsigned long long bar[2];     // mbarriers of the two buffers
+    double win[2][3][kChunk][kStride];  // double-buffered window blocks (TMA destination)
+    double red[kThreads / 32][kChunk];  // per-warp partial gathers
+    unsigned long long bar[2];          // mbarriers of the two buffers
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -71,6 +76,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// D[8x8] += A[8x4] B[4x8] in fp64 on the tensor cores.  Fragments (verified by
+// scripts/dmma_layout.cu): a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// {d0, d1} = D[lane>>2][2(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 // MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
 template <int MODE, class Epi>
@@ -85,14 +98,10 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    // owned columns: (b, c) for b in {cb0, cb0 + 1} (one 16-byte load of Y_p[b..b+1])
-    const int cc = tid % kT;
-    const int cb0 = kNJ * (tid / kT);
-    int cb[kNJ];
-#pragma unroll
-    for (int j = 0; j < kNJ; ++j) cb[j] = cb0 + j;
+    const int gq = lane >> 2;  // fragment "group" (row of A / D, column of B)
+    const int tq = lane & 3;   // thread in group
+    const int a0 = 4 * warp;   // this warp's a-quarter
 
-    // cost-balanced contiguous chunk range of this CTA (fused3d_prepare)
     const int64_t cbeg = bounds[blockIdx.x];
     const int64_t cend = bounds[blockIdx.x + 1];
     const int64_t ng2 = (int64_t)ng * ng;
@@ -111,11 +120,29 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         }
     }
 
-    double g[kNJ][kT];  // footprint of the current group (gather source)
-    double s[kNJ][kT];  // spread accumulators of the current group
+    // gather B operand: Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
+    double Fb[8][4];
+    // spread accumulators: S[mt][nt2] = {S[a0 + (mt>>1)][8(mt&1) + gq][8nt2 + 2tq + i]}
+    double S[8][2][2];
     int32_t cur_key = -1;
-    int64_t gbase = 0;
+    int64_t gorg = 0;  // grid index of footprint (0,0,0) for the current group
     double ddmax = 0.0;
+
+    auto origin = [&](int32_t kk) -> int64_t {
+        const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
+        return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
+    };
+    auto flush = [&]() {
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (S[mt][nt][i] != 0.0) atomicAdd(grid_out + row + 8 * nt + 2 * tq + i, S[mt][nt][i]);
+        }
+    };
 
     for (int64_t c = cbeg; c < cend; ++c) {
         const int k = (int)(c - cbeg);
@@ -126,100 +153,81 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         const int32_t key = dsc.z;
 
         if (key != cur_key) {
-            if (SPREAD && cur_key >= 0) {
-#pragma unroll
-                for (int j = 0; j < kNJ; ++j) {
-                    const int64_t col = gbase + (int64_t)cb[j] * ng + cc;
-#pragma unroll
-                    for (int a = 0; a < kT; ++a)
-                        if (s[j][a] != 0.0) atomicAdd(grid_out + col + a * ng2, s[j][a]);
-                }
-            }
+            if (SPREAD && cur_key >= 0) flush();
             cur_key = key;
-            const int c2 = key % ng;
-            const int c1 = (key / ng) % ng;
-            const int c0 = key / ng2;
-            gbase = ((int64_t)(c0 - kM + 1) * ng + (c1 - kM + 1)) * ng + (c2 - kM + 1);
+            gorg = origin(key);
 #pragma unroll
-            for (int j = 0; j < kNJ; ++j) {
-                const int64_t col = gbase + (int64_t)cb[j] * ng + cc;
+            for (int nt = 0; nt < 8; ++nt) {
+                const int64_t row = gorg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
 #pragma unroll
-                for (int a = 0; a < kT; ++a) {
-                    if (GATHER) g[j][a] = __ldg(grid_in + col + a * ng2);
-                    if (SPREAD) s[j][a] = 0.0;
-                }
+                for (int ks = 0; ks < 4; ++ks)
+                    if (GATHER) Fb[nt][ks] = __ldg(grid_in + row + 4 * ks + tq);
+            }
+            if (SPREAD) {
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
         }
         if (GATHER) {
             // warm L1 with the epilogue's per-point inputs and, at a group boundary, with
-            // the next group's footprint columns (hides their latency behind this chunk)
+            // the next group's footprint (hides their latency behind this chunk)
             if (lane < cnt) epi.prefetch(p0 + lane);
             if (c + 1 < cend) {
                 const int32_t nkey = desc[c + 1].z;
                 if (nkey != key) {
-                    const int n2 = nkey % ng, n1 = (nkey / ng) % ng, n0 = nkey / ng2;
-                    const int64_t nbase = ((int64_t)(n0 - kM + 1) * ng + (n1 - kM + 1)) * ng + (n2 - kM + 1);
+                    const int64_t norg = origin(nkey);
 #pragma unroll
-                    for (int j = 0; j < kNJ; ++j) {
-                        const double* colp = grid_in + nbase + (int64_t)cb[j] * ng + cc;
-#pragma unroll
-                        for (int a = 0; a < kT; ++a)
-                            asm volatile("prefetch.global.L1 [%0];" ::"l"(colp + a * ng2));
+                    for (int nt = 0; nt < 8; ++nt) {
+                        const double* rowp =
+                            grid_in + norg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(rowp + 4 * tq));
                     }
                 }
             }
         }
-        double wn_reg;  // spread weight of slot `lane` (broadcast by shuffles in the spread)
         mbar_wait(&sm.bar[buf], (k >> 1) & 1);
-        const double(*wx)[kT] = sm.win[buf][0];
-        const double(*wy)[kT] = sm.win[buf][1];
-        const double(*wz)[kT] = sm.win[buf][2];
+        const double(*wx)[kStride] = sm.win[buf][0];
+        const double(*wy)[kStride] = sm.win[buf][1];
+        const double(*wz)[kStride] = sm.win[buf][2];
 
+        double wn = 0.0;  // spread weight of slot `lane`
         if (GATHER) {
-            double r[kChunk];
 #pragma unroll
-            for (int p = 0; p < kChunk; p += 2) {
-                double e[2][kNJ][2];
+            for (int mt = 0; mt < 4; ++mt) {  // 8 points per m-tile
+                const int p = 8 * mt + gq;
+                double acc[8][2];
 #pragma unroll
-                for (int q = 0; q < 2; ++q)
+                for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
-                    for (int j = 0; j < kNJ; ++j) e[q][j][0] = e[q][j][1] = 0.0;
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double az = wz[p][4 * ks + tq];  // A[p][c] = Z_p[c]
 #pragma unroll
-                for (int a = 0; a < kT; a += 2) {
-                    const double2 x0 = *reinterpret_cast<const double2*>(&wx[p][a]);
-                    const double2 x1 = *reinterpret_cast<const double2*>(&wx[p + 1][a]);
-#pragma unroll
-                    for (int j = 0; j < kNJ; ++j) {
-                        e[0][j][0] = fma(g[j][a], x0.x, e[0][j][0]);
-                        e[0][j][1] = fma(g[j][a + 1], x0.y, e[0][j][1]);
-                        e[1][j][0] = fma(g[j][a], x1.x, e[1][j][0]);
-                        e[1][j][1] = fma(g[j][a + 1], x1.y, e[1][j][1]);
-                    }
+                    for (int nt = 0; nt < 8; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
                 }
+                // acc[nt][i] = G[p][a = a0 + (nt>>1)][b = 8(nt&1) + 2tq + i]
+                const double2 ylo = *reinterpret_cast<const double2*>(&wy[p][2 * tq]);
+                const double2 yhi = *reinterpret_cast<const double2*>(&wy[p][8 + 2 * tq]);
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                double part = 0.0;
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const double2 yv = *reinterpret_cast<const double2*>(&wy[p + q][cb0]);
-                    const double v = fma(e[q][0][0] + e[q][0][1], yv.x, (e[q][1][0] + e[q][1][1]) * yv.y);
-                    r[p + q] = v * wz[p + q][cc];
+                for (int al = 0; al < 4; ++al) {
+                    double q = acc[2 * al][0] * ylo.x;
+                    q = fma(acc[2 * al][1], ylo.y, q);
+                    q = fma(acc[2 * al + 1][0], yhi.x, q);
+                    q = fma(acc[2 * al + 1][1], yhi.y, q);
+                    part = fma(q, xv[al], part);
                 }
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                if (tq == 0) sm.red[warp][p] = part;
             }
-            // transposing butterfly: lane l ends with this warp's sum for slot l
-#pragma unroll
-            for (int sh = 16; sh >= 1; sh >>= 1) {
-                const bool upper = lane & sh;
-#pragma unroll
-                for (int kk = 0; kk < sh; ++kk) {
-                    const double send = upper ? r[kk] : r[kk + sh];
-                    const double keep = upper ? r[kk + sh] : r[kk];
-                    r[kk] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
-                }
-            }
-            sm.red[warp][lane] = r[0];
             __syncthreads();
             // every warp sums the 4 warp partials of slot `lane`; warp 0 applies the
-            // epilogue (writes), the others evaluate the same update to obtain the
-            // spread weight in registers — no second barrier
-            double wn = 0.0;
+            // epilogue (writes), the others evaluate the same update for the weights
             if (lane < cnt) {
                 double t = 0.0;
 #pragma unroll
@@ -232,46 +240,39 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                     wn = epi.weight(p0 + lane, t);
                 }
             }
-            wn_reg = wn;
         } else {
-            wn_reg = (lane < cnt) ? w_in[p0 + lane] : 0.0;
+            wn = (lane < cnt) ? w_in[p0 + lane] : 0.0;
         }
 
         if (SPREAD) {
-#pragma unroll 2
-            for (int p = 0; p < kChunk; ++p) {
-                const double wzp = __shfl_sync(0xffffffffu, wn_reg, p) * wz[p][cc];
-                const double2 yv = *reinterpret_cast<const double2*>(&wy[p][cb0]);
-                double wj[kNJ];
-                wj[0] = wzp * yv.x;
-                wj[1] = wzp * yv.y;
 #pragma unroll
-                for (int a = 0; a < kT; a += 2) {
-                    const double2 xv = *reinterpret_cast<const double2*>(&wx[p][a]);
+            for (int ks = 0; ks < 8; ++ks) {  // 4 points per k-step
+                const int p = 4 * ks + tq;
+                const double wp = __shfl_sync(0xffffffffu, wn, p);
+                // B[p][c] = w_p Z_p[c] for c = 8 nt2 + gq
+                const double b0 = wp * wz[p][gq];
+                const double b1 = wp * wz[p][8 + gq];
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
-                    for (int j = 0; j < kNJ; ++j) {
-                        s[j][a] = fma(wj[j], xv.x, s[j][a]);
-                        s[j][a + 1] = fma(wj[j], xv.y, s[j][a + 1]);
-                    }
+                for (int mt = 0; mt < 8; ++mt) {
+                    // A[(a,b)][p] = X_p[a] Y_p[b], a = a0 + (mt>>1), b = 8(mt&1) + gq
+                    const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
+                    dmma(S[mt][0][0], S[mt][0][1], am, b0);
+                    dmma(S[mt][1][0], S[mt][1][1], am, b1);
                 }
             }
         }
-        __syncthreads();  // every thread is done with win[buf] and wn
+        __syncthreads();  // every thread is done with win[buf] and red
         if (tid == 0 && c + 2 < cend) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&sm.bar[buf], kWinBytes);
             bulk_g2s(&sm.win[buf][0][0][0], win + (c + 2) * kWinDoubles, kWinBytes, &sm.bar[buf]);
         }
     }
-    if (SPREAD && cur_key >= 0) {
-#pragma unroll
-        for (int j = 0; j < kNJ; ++j) {
-            const int64_t col = gbase + (int64_t)cb[j] * ng + cc;
-#pragma unroll
-            for (int a = 0; a < kT; ++a)
-                if (s[j][a] != 0.0) atomicAdd(grid_out + col + a * ng2, s[j][a]);
-        }
-    }
+    if (SPREAD && cur_key >= 0) flush();
     if (GATHER && warp == 0) warp_max_atomic(dmax, ddmax);
 }
 
@@ -293,26 +294,24 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
         desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r], 0);
 }
 
-// window values of every chunk: [chunk][axis][slot][tap], zero for empty slots
+// window values of every chunk: [chunk][axis][slot][tap (row stride kStride)], zero for
+// empty slots and for the row padding
 __global__ void chunk_window_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
                                KBWindow w, double* __restrict__ out) {
     const int64_t c = blockIdx.x;
     const int4 dsc = desc[c];
-    const int a = threadIdx.x % kT;
-    const int q = threadIdx.x / kT;
     double* o = out + c * kWinDoubles;
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-#pragma unroll
-        for (int pp = 0; pp < kChunk / (kThreads / kT); ++pp) {
-            const int p = q + pp * (kThreads / kT);
-            double val = 0.0;
-            if (p < dsc.y) {
-                const double ut = u[ax * n + dsc.x + p];
-                val = kb_phi(ut - floor(ut) + (double)(kM - 1 - a), w);
-            }
-            o[(ax * kChunk + p) * kT + a] = val;
+    for (int e = threadIdx.x; e < kWinDoubles; e += blockDim.x) {
+        const int ax = e / (kChunk * kStride);
+        const int r = e - ax * kChunk * kStride;
+        const int p = r / kStride;
+        const int a = r - p * kStride;
+        double val = 0.0;
+        if (p < dsc.y && a < kT) {
+            const double ut = u[ax * n + dsc.x + p];
+            val = kb_phi(ut - floor(ut) + (double)(kM - 1 - a), w);
         }
+        o[e] = val;
     }
 }
 
