@@ -14,7 +14,7 @@
 //           -> the c-contraction is a GEMM  G[p,(a,b)] = sum_c Z[p,c] F[(a,b),c]  (32x256x16)
 //              on DMMA (mma.sync.m8n8k4.f64); b and a are contracted per point in registers
 //   spread  S[(a,b),c] += sum_p (X_p[a] Y_p[b]) (w_p Z_p[c])        (GEMM 256x16x32 on DMMA)
-// Warp w owns the a-quarter {4w..4w+3}: its F (gather B operand) and S (spread
+// Warp w owns the a-pair {2w, 2w+1}: its F (gather B operand) and S (spread
 // accumulators) stay in registers for the whole cell group — the footprint is read once
 // and flushed once (fp64 RED) per group.  Between the two GEMMs the per-warp partial
 // gathers are summed in shared memory, every warp evaluates the Sinkhorn update (3.3)/
@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kM = 8;               // window half-width of the tuned kernels
 constexpr int kT = 2 * kM;          // taps per axis
-constexpr int kThreads = 128;       // 4 warps
+constexpr int kThreads = 256;       // 8 warps
 constexpr int kChunk = 32;          // points per chunk
 constexpr int kStride = 20;         // padded row stride (doubles) of a window matrix: conflict-free fragments
 constexpr int kWinDoubles = 3 * kChunk * kStride;
@@ -100,7 +100,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     const int warp = tid >> 5;
     const int gq = lane >> 2;  // fragment "group" (row of A / D, column of B)
     const int tq = lane & 3;   // thread in group
-    const int a0 = 4 * warp;   // this warp's a-quarter
+    const int a0 = 2 * warp;   // this warp's a-pair
 
     const int64_t cbeg = bounds[blockIdx.x];
     const int64_t cend = bounds[blockIdx.x + 1];
@@ -121,9 +121,9 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     }
 
     // gather B operand: Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
-    double Fb[8][4];
+    double Fb[4][4];
     // spread accumulators: S[mt][nt2] = {S[a0 + (mt>>1)][8(mt&1) + gq][8nt2 + 2tq + i]}
-    double S[8][2][2];
+    double S[4][2][2];
     int32_t cur_key = -1;
     int64_t gorg = 0;  // grid index of footprint (0,0,0) for the current group
     double ddmax = 0.0;
@@ -134,7 +134,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     };
     auto flush = [&]() {
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
+        for (int mt = 0; mt < 4; ++mt) {
             const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
@@ -157,7 +157,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             cur_key = key;
             gorg = origin(key);
 #pragma unroll
-            for (int nt = 0; nt < 8; ++nt) {
+            for (int nt = 0; nt < 4; ++nt) {
                 const int64_t row = gorg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
@@ -165,7 +165,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             }
             if (SPREAD) {
 #pragma unroll
-                for (int mt = 0; mt < 8; ++mt)
+                for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
@@ -179,7 +179,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 if (nkey != key) {
                     const int64_t norg = origin(nkey);
 #pragma unroll
-                    for (int nt = 0; nt < 8; ++nt) {
+                    for (int nt = 0; nt < 4; ++nt) {
                         const double* rowp =
                             grid_in + norg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
                         asm volatile("prefetch.global.L1 [%0];" ::"l"(rowp + 4 * tq));
@@ -197,24 +197,23 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {  // 8 points per m-tile
                 const int p = 8 * mt + gq;
-                double acc[8][2];
+                double acc[4][2];
 #pragma unroll
-                for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+                for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double az = wz[p][4 * ks + tq];  // A[p][c] = Z_p[c]
 #pragma unroll
-                    for (int nt = 0; nt < 8; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
+                    for (int nt = 0; nt < 4; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
                 }
                 // acc[nt][i] = G[p][a = a0 + (nt>>1)][b = 8(nt&1) + 2tq + i]
                 const double2 ylo = *reinterpret_cast<const double2*>(&wy[p][2 * tq]);
                 const double2 yhi = *reinterpret_cast<const double2*>(&wy[p][8 + 2 * tq]);
                 const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
-                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                const double xv[2] = {xa.x, xa.y};
                 double part = 0.0;
 #pragma unroll
-                for (int al = 0; al < 4; ++al) {
+                for (int al = 0; al < 2; ++al) {
                     double q = acc[2 * al][0] * ylo.x;
                     q = fma(acc[2 * al][1], ylo.y, q);
                     q = fma(acc[2 * al + 1][0], yhi.x, q);
@@ -253,11 +252,10 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 const double b0 = wp * wz[p][gq];
                 const double b1 = wp * wz[p][8 + gq];
                 const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
-                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                const double xv[2] = {xa.x, xa.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
-                for (int mt = 0; mt < 8; ++mt) {
+                for (int mt = 0; mt < 4; ++mt) {
                     // A[(a,b)][p] = X_p[a] Y_p[b], a = a0 + (mt>>1), b = 8(mt&1) + gq
                     const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
                     dmma(S[mt][0][0], S[mt][0][1], am, b0);
