@@ -144,10 +144,12 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         }
     };
 
+    int4 dsc_next = cbeg < cend ? desc[cbeg] : make_int4(0, 0, -1, 0);
     for (int64_t c = cbeg; c < cend; ++c) {
         const int k = (int)(c - cbeg);
         const int buf = k & 1;
-        const int4 dsc = desc[c];  // {first point, count, key, 0}
+        const int4 dsc = dsc_next;  // {first point, count, key, 0}
+        if (c + 1 < cend) dsc_next = desc[c + 1];  // loaded one chunk ahead
         const int64_t p0 = dsc.x;
         const int cnt = dsc.y;
         const int32_t key = dsc.z;
@@ -175,7 +177,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             // the next group's footprint (hides their latency behind this chunk)
             if (lane < cnt) epi.prefetch(p0 + lane);
             if (c + 1 < cend) {
-                const int32_t nkey = desc[c + 1].z;
+                const int32_t nkey = dsc_next.z;
                 if (nkey != key) {
                     const int64_t norg = origin(nkey);
 #pragma unroll
