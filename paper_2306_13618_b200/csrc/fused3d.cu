@@ -45,7 +45,6 @@ constexpr int kBlocksPerSM = 2;
 struct __align__(128) Smem {
     double win[2][3][kChunk][kStride];  // double-buffered window blocks (TMA destination)
     double red[kThreads / 32][kChunk];  // per-warp partial gathers
-    double xw[kChunk][kStride];         // w_p X_p[a]: weighted spread rows (Sinkhorn half-step)
     unsigned long long bar[2];          // mbarriers of the two buffers
 };
 
@@ -228,29 +227,20 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 if (tq == 0) sm.red[warp][p] = part;
             }
             __syncthreads();
-            // warp w evaluates the update for slots 4w..4w+3 (8 lanes per slot: lane
-            // 8j handles slot 4w+j and writes the potentials) and stores the weighted
-            // window row w_p X_p[.] for the spread's A operand
-            {
-                const int j = lane >> 3, r = lane & 7;
-                const int p = 4 * warp + j;
-                double wp = 0.0;
-                if (p < cnt) {
-                    double t = 0.0;
+            // every warp sums the 4 warp partials of slot `lane`; warp 0 applies the
+            // epilogue (writes), the others evaluate the same update for the weights
+            if (lane < cnt) {
+                double t = 0.0;
 #pragma unroll
-                    for (int w = 0; w < kThreads / 32; ++w) t += sm.red[w][p];
-                    if (r == 0) {
-                        const double dd = epi(p0 + p, t);
-                        ddmax = fmax(ddmax, dd);
-                    }
-                    if (SPREAD) wp = epi.weight(p0 + p, t);
-                }
-                if (SPREAD) {
-                    sm.xw[p][2 * r] = wp * wx[p][2 * r];
-                    sm.xw[p][2 * r + 1] = wp * wx[p][2 * r + 1];
+                for (int w = 0; w < kThreads / 32; ++w) t += sm.red[w][lane];
+                if (warp == 0) {
+                    const double dd = epi(p0 + lane, t);
+                    ddmax = fmax(ddmax, dd);
+                    if (SPREAD) wn = epi.w_next[p0 + lane];
+                } else if (SPREAD) {
+                    wn = epi.weight(p0 + lane, t);
                 }
             }
-            if (SPREAD) __syncthreads();
         } else {
             wn = (lane < cnt) ? w_in[p0 + lane] : 0.0;
         }
@@ -259,22 +249,12 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {  // 4 points per k-step
                 const int p = 4 * ks + tq;
-                double b0, b1;
-                double xv[2];
-                if (GATHER) {  // weights already folded into xw
-                    b0 = wz[p][gq];
-                    b1 = wz[p][8 + gq];
-                    const double2 xa = *reinterpret_cast<const double2*>(&sm.xw[p][a0]);
-                    xv[0] = xa.x;
-                    xv[1] = xa.y;
-                } else {
-                    const double wp = __shfl_sync(0xffffffffu, wn, p);
-                    b0 = wp * wz[p][gq];
-                    b1 = wp * wz[p][8 + gq];
-                    const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
-                    xv[0] = xa.x;
-                    xv[1] = xa.y;
-                }
+                const double wp = __shfl_sync(0xffffffffu, wn, p);
+                // B[p][c] = w_p Z_p[c] for c = 8 nt2 + gq
+                const double b0 = wp * wz[p][gq];
+                const double b1 = wp * wz[p][8 + gq];
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double xv[2] = {xa.x, xa.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) {
@@ -293,7 +273,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         }
     }
     if (SPREAD && cur_key >= 0) flush();
-    if (GATHER) warp_max_atomic(dmax, ddmax);
+    if (GATHER && warp == 0) warp_max_atomic(dmax, ddmax);
 }
 
 // ---------------------------------------------------------------- chunk preparation
