@@ -24,6 +24,8 @@ KEYS = [
     ("sm__cycles_active.avg", "SM active cycles (avg)"),
     ("gpc__cycles_elapsed.max", "elapsed cycles"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe busy (% of active)"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA subpipe busy (% of active)"),
+    ("sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed", "tensor FP64 ops (% of peak, elapsed)"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy (%)"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy (%)"),
     ("launch__registers_per_thread", "registers/thread"),
