@@ -276,6 +276,230 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     if (GATHER && warp == 0) warp_max_atomic(dmax, ddmax);
 }
 
+// ---------------------------------------------------------------- warp-specialised half-step
+// The Sinkhorn half-step with the gather and the spread on different warps of the CTA:
+//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions), sum the 4
+//                    warp partials, run the update (3.3)/(3.4), and publish the weighted
+//                    rows xw[p][a] = w_p X_p[a] of chunk k;
+//   warps 4-7 ("S"): spread chunk k from xw (A = xw Y, B = Z on DMMA) while G already
+//                    gathers chunk k+1.
+// Each group's scalar phases (contractions, log/exp of the update, fragment products) then
+// overlap the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
+// mbarriers: win_full[3] (TMA ring of window blocks, refilled by S when it releases a
+// slot), xw_full[2] / xw_empty[2] (the weighted rows); each group synchronises
+// internally with its own named barrier (ids 1 and 2), never with __syncthreads.
+constexpr int kRing = 3;
+struct __align__(128) SmemWS {
+    double win[kRing][3][kChunk][kStride];
+    double xw[2][kChunk][kStride];
+    double red[2][4][kChunk];
+    unsigned long long win_full[kRing];
+    unsigned long long xw_full[2];
+    unsigned long long xw_empty[2];
+};
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void group_sync(int id) {  // named barrier over one 4-warp group
+    asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+__global__ void __launch_bounds__(256, kBlocksPerSM)
+sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
+                int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out, EpiSinkhorn epi,
+                unsigned long long* dmax) {
+    extern __shared__ __align__(128) unsigned char ws_raw[];
+    SmemWS& sm = *reinterpret_cast<SmemWS*>(ws_raw);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const bool is_g = warp < 4;
+    const int gw = warp & 3;  // warp index within its group
+    const int gq = lane >> 2;
+    const int tq = lane & 3;
+    const int a0 = 4 * gw;  // the group-warp's a-quarter
+    const int64_t cbeg = bounds[blockIdx.x];
+    const int64_t cend = bounds[blockIdx.x + 1];
+    const int64_t nck = cend - cbeg;
+    const int64_t ng2 = (int64_t)ng * ng;
+
+    if (tid == 0) {
+        for (int i = 0; i < kRing; ++i) mbar_init(&sm.win_full[i], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sm.xw_full[i], 128);
+            mbar_init(&sm.xw_empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 0; k < kRing && k < nck; ++k) {
+            mbar_expect_tx(&sm.win_full[k], kWinBytes);
+            bulk_g2s(&sm.win[k][0][0][0], win + (cbeg + k) * kWinDoubles, kWinBytes, &sm.win_full[k]);
+        }
+    }
+    auto origin = [&](int32_t kk) -> int64_t {
+        const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
+        return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
+    };
+
+    if (is_g) {
+        // ------------------------------------------------------------ gather + update
+        double Fb[8][4];  // Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
+        int32_t cur_key = -1;
+        double ddmax = 0.0;
+        int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
+        for (int64_t k = 0; k < nck; ++k) {
+            const int64_t c = cbeg + k;
+            const int slot = (int)(k % kRing);
+            const int4 dsc = dsc_next;
+            if (k + 1 < nck) dsc_next = desc[c + 1];
+            const int64_t p0 = dsc.x;
+            const int cnt = dsc.y;
+            if (dsc.z != cur_key) {
+                cur_key = dsc.z;
+                const int64_t org = origin(cur_key);
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    const double* row = grid_in + org + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) Fb[nt][ks] = __ldg(row + 4 * ks + tq);
+                }
+            }
+            if (lane < cnt) epi.prefetch(p0 + lane);
+            if (k + 1 < nck && dsc_next.z != cur_key) {
+                const int64_t norg = origin(dsc_next.z);
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    const double* rowp =
+                        grid_in + norg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(rowp + 4 * tq));
+                }
+            }
+            mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
+            const double(*wx)[kStride] = sm.win[slot][0];
+            const double(*wy)[kStride] = sm.win[slot][1];
+            const double(*wz)[kStride] = sm.win[slot][2];
+            double(*red)[kChunk] = sm.red[k & 1];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+                double acc[8][2];
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double az = wz[p][4 * ks + tq];
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
+                }
+                const double2 ylo = *reinterpret_cast<const double2*>(&wy[p][2 * tq]);
+                const double2 yhi = *reinterpret_cast<const double2*>(&wy[p][8 + 2 * tq]);
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                double part = 0.0;
+#pragma unroll
+                for (int al = 0; al < 4; ++al) {
+                    double q = acc[2 * al][0] * ylo.x;
+                    q = fma(acc[2 * al][1], ylo.y, q);
+                    q = fma(acc[2 * al + 1][0], yhi.x, q);
+                    q = fma(acc[2 * al + 1][1], yhi.y, q);
+                    part = fma(q, xv[al], part);
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                if (tq == 0) red[gw][p] = part;
+            }
+            group_sync(1);
+            // lane p: t_p; warp 0 writes the potentials, all G warps form w_p
+            double wp = 0.0;
+            if (lane < cnt) {
+                const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
+                if (gw == 0) {
+                    ddmax = fmax(ddmax, epi(p0 + lane, t));
+                    wp = epi.w_next[p0 + lane];
+                } else {
+                    wp = epi.weight(p0 + lane, t);
+                }
+            }
+            // publish xw[p][a0..a0+3] = w_p X_p[a] for chunk k
+            if (k >= 2) mbar_wait(&sm.xw_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
+            {
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[lane][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[lane][a0 + 2]);
+                double2* dst = reinterpret_cast<double2*>(&sm.xw[k & 1][lane][a0]);
+                dst[0] = make_double2(wp * xa.x, wp * xa.y);
+                dst[1] = make_double2(wp * xb.x, wp * xb.y);
+            }
+            mbar_arrive(&sm.xw_full[k & 1]);
+        }
+        if (gw == 0) warp_max_atomic(dmax, ddmax);
+    } else {
+        // ------------------------------------------------------------ spread
+        double S[8][2][2];  // S[mt][nt] = S[a0 + (mt>>1)][8(mt&1) + gq][8nt + 2tq + i]
+        int32_t cur_key = -1;
+        int64_t org = 0;
+        auto flush = [&]() {
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                const int64_t row = org + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        if (S[mt][nt][i] != 0.0) atomicAdd(grid_out + row + 8 * nt + 2 * tq + i, S[mt][nt][i]);
+            }
+        };
+        for (int64_t k = 0; k < nck; ++k) {
+            const int64_t c = cbeg + k;
+            const int slot = (int)(k % kRing);
+            const int32_t key = desc[c].z;
+            if (key != cur_key) {
+                if (cur_key >= 0) flush();
+                cur_key = key;
+                org = origin(key);
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
+            }
+            mbar_wait(&sm.xw_full[k & 1], (uint32_t)((k >> 1) & 1));
+            mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
+            const double(*wy)[kStride] = sm.win[slot][1];
+            const double(*wz)[kStride] = sm.win[slot][2];
+            const double(*xw)[kStride] = sm.xw[k & 1];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int p = 4 * ks + tq;
+                const double b0 = wz[p][gq];
+                const double b1 = wz[p][8 + gq];
+                const double2 xa = *reinterpret_cast<const double2*>(&xw[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&xw[p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt) {
+                    const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
+                    dmma(S[mt][0][0], S[mt][0][1], am, b0);
+                    dmma(S[mt][1][0], S[mt][1][1], am, b1);
+                }
+            }
+            group_sync(2);  // all S warps are done with xw[k&1] and window slot
+            if (warp == 4 && lane == 0) {
+                mbar_arrive(&sm.xw_empty[k & 1]);
+                if (k + kRing < nck) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&sm.win_full[slot], kWinBytes);
+                    bulk_g2s(&sm.win[slot][0][0][0], win + (c + kRing) * kWinDoubles, kWinBytes, &sm.win_full[slot]);
+                }
+            }
+        }
+        if (cur_key >= 0) flush();
+    }
+}
+
 // ---------------------------------------------------------------- chunk preparation
 __global__ void chunk_count_k(const int32_t* __restrict__ run_len, const int32_t* __restrict__ nruns,
                               int32_t* __restrict__ nchunk) {
@@ -439,7 +663,26 @@ void fused3d_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
 
 void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
                            const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s) {
-    launch<0, EpiSinkhorn>(ps, grid_in, grid_out, nullptr, fp, epi, dmax, s, kProfFused);
+    // warp-specialised kernel by default; UOTK_FUSED_WS=0 selects the phase-locked one
+    static const bool ws = [] {
+        const char* e = getenv("UOTK_FUSED_WS");
+        return !(e && e[0] == '0');
+    }();
+    if (!ws) {
+        launch<0, EpiSinkhorn>(ps, grid_in, grid_out, nullptr, fp, epi, dmax, s, kProfFused);
+        return;
+    }
+    if (ps.n == 0 || ps.nchunks == 0) return;
+    static bool attr_set = false;
+    if (!attr_set) {
+        UOTK_CUDA(cudaFuncSetAttribute(sinkhorn3d_ws_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(SmemWS)));
+        attr_set = true;
+    }
+    ProfScope prof(kProfFused, s);
+    sinkhorn3d_ws_k<<<ps.chunk_blocks, 256, sizeof(SmemWS), s>>>(ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p,
+                                                                 fp.ng, grid_in, grid_out, epi, dmax);
+    UOTK_LAUNCHED();
 }
 
 void fused3d_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
