@@ -278,24 +278,23 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 
 // ---------------------------------------------------------------- warp-specialised half-step
 // The Sinkhorn half-step with the gather and the spread on different warps of the CTA:
-//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions), sum the 4
-//                    warp partials, run the update (3.3)/(3.4), and publish the weighted
-//                    rows xw[p][a] = w_p X_p[a] of chunk k;
-//   warps 4-7 ("S"): spread chunk k from xw (A = xw Y, B = Z on DMMA) while G already
-//                    gathers chunk k+1.
-// Each group's scalar phases (contractions, log/exp of the update, fragment products) then
-// overlap the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
-// mbarriers: win_full[3] (TMA ring of window blocks, refilled by S when it releases a
-// slot), xw_full[2] / xw_empty[2] (the weighted rows); each group synchronises
-// internally with its own named barrier (ids 1 and 2), never with __syncthreads.
+//   warps 0-3 ("G"): gather chunk k — the DMMA GEMM over c and the b/a contractions —
+//                    and publish the 4 x 32 per-warp partial sums;
+//   warps 4-7 ("S"): sum the partials into t_p, run the update (3.3)/(3.4) (warp 4 writes
+//                    the potentials; every S warp forms the weights it needs), and spread
+//                    chunk k (A = w X Y, B = Z on DMMA) while G already gathers chunk k+1.
+// The log/exp chains of the update and the fragment products of one group then overlap
+// the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
+// mbarriers only: win_full[3] (TMA ring of window blocks; S refills a slot when it
+// releases it), red_full[2] / red_empty[2] (the partial sums); the S warps synchronise
+// among themselves with named barrier 2 — never with __syncthreads inside the loop.
 constexpr int kRing = 3;
 struct __align__(128) SmemWS {
     double win[kRing][3][kChunk][kStride];
-    double xw[2][kChunk][kStride];
     double red[2][4][kChunk];
     unsigned long long win_full[kRing];
-    unsigned long long xw_full[2];
-    unsigned long long xw_empty[2];
+    unsigned long long red_full[2];
+    unsigned long long red_empty[2];
 };
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
@@ -327,8 +326,8 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     if (tid == 0) {
         for (int i = 0; i < kRing; ++i) mbar_init(&sm.win_full[i], 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&sm.xw_full[i], 128);
-            mbar_init(&sm.xw_empty[i], 1);
+            mbar_init(&sm.red_full[i], 128);
+            mbar_init(&sm.red_empty[i], 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -345,18 +344,15 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     };
 
     if (is_g) {
-        // ------------------------------------------------------------ gather + update
+        // ------------------------------------------------------------ gather
         double Fb[8][4];  // Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
         int32_t cur_key = -1;
-        double ddmax = 0.0;
         int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
             const int4 dsc = dsc_next;
             if (k + 1 < nck) dsc_next = desc[c + 1];
-            const int64_t p0 = dsc.x;
-            const int cnt = dsc.y;
             if (dsc.z != cur_key) {
                 cur_key = dsc.z;
                 const int64_t org = origin(cur_key);
@@ -367,7 +363,6 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     for (int ks = 0; ks < 4; ++ks) Fb[nt][ks] = __ldg(row + 4 * ks + tq);
                 }
             }
-            if (lane < cnt) epi.prefetch(p0 + lane);
             if (k + 1 < nck && dsc_next.z != cur_key) {
                 const int64_t norg = origin(dsc_next.z);
 #pragma unroll
@@ -378,6 +373,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 }
             }
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
+            if (k >= 2) mbar_wait(&sm.red_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
             const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
@@ -412,35 +408,14 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 part += __shfl_xor_sync(0xffffffffu, part, 2);
                 if (tq == 0) red[gw][p] = part;
             }
-            group_sync(1);
-            // lane p: t_p; warp 0 writes the potentials, all G warps form w_p
-            double wp = 0.0;
-            if (lane < cnt) {
-                const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
-                if (gw == 0) {
-                    ddmax = fmax(ddmax, epi(p0 + lane, t));
-                    wp = epi.w_next[p0 + lane];
-                } else {
-                    wp = epi.weight(p0 + lane, t);
-                }
-            }
-            // publish xw[p][a0..a0+3] = w_p X_p[a] for chunk k
-            if (k >= 2) mbar_wait(&sm.xw_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
-            {
-                const double2 xa = *reinterpret_cast<const double2*>(&wx[lane][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&wx[lane][a0 + 2]);
-                double2* dst = reinterpret_cast<double2*>(&sm.xw[k & 1][lane][a0]);
-                dst[0] = make_double2(wp * xa.x, wp * xa.y);
-                dst[1] = make_double2(wp * xb.x, wp * xb.y);
-            }
-            mbar_arrive(&sm.xw_full[k & 1]);
+            mbar_arrive(&sm.red_full[k & 1]);
         }
-        if (gw == 0) warp_max_atomic(dmax, ddmax);
     } else {
-        // ------------------------------------------------------------ spread
+        // ------------------------------------------------------------ update + spread
         double S[8][2][2];  // S[mt][nt] = S[a0 + (mt>>1)][8(mt&1) + gq][8nt + 2tq + i]
         int32_t cur_key = -1;
         int64_t org = 0;
+        double ddmax = 0.0;
         auto flush = [&]() {
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
@@ -452,32 +427,54 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                         if (S[mt][nt][i] != 0.0) atomicAdd(grid_out + row + 8 * nt + 2 * tq + i, S[mt][nt][i]);
             }
         };
+        int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
-            const int32_t key = desc[c].z;
-            if (key != cur_key) {
+            const int4 dsc = dsc_next;
+            if (k + 1 < nck) dsc_next = desc[c + 1];
+            const int64_t p0 = dsc.x;
+            const int cnt = dsc.y;
+            if (dsc.z != cur_key) {
                 if (cur_key >= 0) flush();
-                cur_key = key;
-                org = origin(key);
+                cur_key = dsc.z;
+                org = origin(cur_key);
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
-            mbar_wait(&sm.xw_full[k & 1], (uint32_t)((k >> 1) & 1));
+            if (lane < cnt) epi.prefetch(p0 + lane);
+            // t_p from the gather partials; the update; the spread weight of slot `lane`
+            mbar_wait(&sm.red_full[k & 1], (uint32_t)((k >> 1) & 1));
+            double t = 0.0;
+            if (lane < cnt) {
+                const double(*red)[kChunk] = sm.red[k & 1];
+                t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
+            }
+            mbar_arrive(&sm.red_empty[k & 1]);
+            double wn = 0.0;
+            if (lane < cnt) {
+                if (gw == 0) {
+                    ddmax = fmax(ddmax, epi(p0 + lane, t));
+                    wn = epi.w_next[p0 + lane];
+                } else {
+                    wn = epi.weight(p0 + lane, t);
+                }
+            }
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
+            const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
-            const double(*xw)[kStride] = sm.xw[k & 1];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 const int p = 4 * ks + tq;
+                const double wp = __shfl_sync(0xffffffffu, wn, p);
                 const double b0 = wz[p][gq];
                 const double b1 = wz[p][8 + gq];
-                const double2 xa = *reinterpret_cast<const double2*>(&xw[p][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&xw[p][a0 + 2]);
-                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
+                const double xv[4] = {wp * xa.x, wp * xa.y, wp * xb.x, wp * xb.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
@@ -486,17 +483,15 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     dmma(S[mt][1][0], S[mt][1][1], am, b1);
                 }
             }
-            group_sync(2);  // all S warps are done with xw[k&1] and window slot
-            if (warp == 4 && lane == 0) {
-                mbar_arrive(&sm.xw_empty[k & 1]);
-                if (k + kRing < nck) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_expect_tx(&sm.win_full[slot], kWinBytes);
-                    bulk_g2s(&sm.win[slot][0][0][0], win + (c + kRing) * kWinDoubles, kWinBytes, &sm.win_full[slot]);
-                }
+            group_sync(2);  // all S warps are done with the window slot
+            if (warp == 4 && lane == 0 && k + kRing < nck) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&sm.win_full[slot], kWinBytes);
+                bulk_g2s(&sm.win[slot][0][0][0], win + (c + kRing) * kWinDoubles, kWinBytes, &sm.win_full[slot]);
             }
         }
         if (cur_key >= 0) flush();
+        if (gw == 0) warp_max_atomic(dmax, ddmax);
     }
 }
 
