@@ -278,23 +278,24 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 
 // ---------------------------------------------------------------- warp-specialised half-step
 // The Sinkhorn half-step with the gather and the spread on different warps of the CTA:
-//   warps 0-3 ("G"): gather chunk k — the DMMA GEMM over c and the b/a contractions —
-//                    and publish the 4 x 32 per-warp partial sums;
-//   warps 4-7 ("S"): sum the partials into t_p, run the update (3.3)/(3.4) (warp 4 writes
-//                    the potentials; every S warp forms the weights it needs), and spread
-//                    chunk k (A = w X Y, B = Z on DMMA) while G already gathers chunk k+1.
-// The log/exp chains of the update and the fragment products of one group then overlap
-// the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
-// mbarriers only: win_full[3] (TMA ring of window blocks; S refills a slot when it
-// releases it), red_full[2] / red_empty[2] (the partial sums); the S warps synchronise
-// among themselves with named barrier 2 — never with __syncthreads inside the loop.
+//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions), sum the 4
+//                    warp partials, run the update (3.3)/(3.4), and publish the weighted
+//                    rows xw[p][a] = w_p X_p[a] of chunk k;
+//   warps 4-7 ("S"): spread chunk k from xw (A = xw Y, B = Z on DMMA) while G already
+//                    gathers chunk k+1.
+// Each group's scalar phases (contractions, log/exp of the update, fragment products) then
+// overlap the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
+// mbarriers: win_full[3] (TMA ring of window blocks, refilled by S when it releases a
+// slot), xw_full[2] / xw_empty[2] (the weighted rows); each group synchronises
+// internally with its own named barrier (ids 1 and 2), never with __syncthreads.
 constexpr int kRing = 3;
 struct __align__(128) SmemWS {
     double win[kRing][3][kChunk][kStride];
+    double xw[2][kChunk][kStride];
     double red[2][4][kChunk];
     unsigned long long win_full[kRing];
-    unsigned long long red_full[2];
-    unsigned long long red_empty[2];
+    unsigned long long xw_full[2];
+    unsigned long long xw_empty[2];
 };
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
@@ -326,8 +327,8 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     if (tid == 0) {
         for (int i = 0; i < kRing; ++i) mbar_init(&sm.win_full[i], 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&sm.red_full[i], 128);
-            mbar_init(&sm.red_empty[i], 128);
+            mbar_init(&sm.xw_full[i], 128);
+            mbar_init(&sm.xw_empty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -344,15 +345,18 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     };
 
     if (is_g) {
-        // ------------------------------------------------------------ gather
+        // ------------------------------------------------------------ gather + update
         double Fb[8][4];  // Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
         int32_t cur_key = -1;
+        double ddmax = 0.0;
         int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
             const int4 dsc = dsc_next;
             if (k + 1 < nck) dsc_next = desc[c + 1];
+            const int64_t p0 = dsc.x;
+            const int cnt = dsc.y;
             if (dsc.z != cur_key) {
                 cur_key = dsc.z;
                 const int64_t org = origin(cur_key);
@@ -363,6 +367,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     for (int ks = 0; ks < 4; ++ks) Fb[nt][ks] = __ldg(row + 4 * ks + tq);
                 }
             }
+            if (lane < cnt) epi.prefetch(p0 + lane);
             if (k + 1 < nck && dsc_next.z != cur_key) {
                 const int64_t norg = origin(dsc_next.z);
 #pragma unroll
@@ -373,49 +378,84 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 }
             }
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
-            if (k >= 2) mbar_wait(&sm.red_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
             const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
             double(*red)[kChunk] = sm.red[k & 1];
+            // 8 steps s = (m-tile mt = s>>1, a-half h = s&1: n-tiles 4h..4h+3), software
+            // pipelined: the DMMAs of step s+1 are issued before step s is contracted, so
+            // the contraction never waits for its own DMMAs to drain
+            double acc[2][4][2];
+            double part = 0.0;
+            auto issue = [&](const int s) {
+                const int p = 8 * (s >> 1) + gq;
+                double(&ac)[4][2] = acc[s & 1];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int p = 8 * mt + gq;
-                double acc[8][2];
-#pragma unroll
-                for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+                for (int j = 0; j < 4; ++j) ac[j][0] = ac[j][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double az = wz[p][4 * ks + tq];
 #pragma unroll
-                    for (int nt = 0; nt < 8; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
+                    for (int j = 0; j < 4; ++j) dmma(ac[j][0], ac[j][1], az, Fb[4 * (s & 1) + j][ks]);
                 }
+            };
+            auto contract = [&](const int s) {
+                const int p = 8 * (s >> 1) + gq;
+                const double(&ac)[4][2] = acc[s & 1];
                 const double2 ylo = *reinterpret_cast<const double2*>(&wy[p][2 * tq]);
                 const double2 yhi = *reinterpret_cast<const double2*>(&wy[p][8 + 2 * tq]);
-                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
-                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
-                double part = 0.0;
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0 + 2 * (s & 1)]);
+                const double xv[2] = {xa.x, xa.y};
 #pragma unroll
-                for (int al = 0; al < 4; ++al) {
-                    double q = acc[2 * al][0] * ylo.x;
-                    q = fma(acc[2 * al][1], ylo.y, q);
-                    q = fma(acc[2 * al + 1][0], yhi.x, q);
-                    q = fma(acc[2 * al + 1][1], yhi.y, q);
+                for (int al = 0; al < 2; ++al) {
+                    double q = ac[2 * al][0] * ylo.x;
+                    q = fma(ac[2 * al][1], ylo.y, q);
+                    q = fma(ac[2 * al + 1][0], yhi.x, q);
+                    q = fma(ac[2 * al + 1][1], yhi.y, q);
                     part = fma(q, xv[al], part);
                 }
-                part += __shfl_xor_sync(0xffffffffu, part, 1);
-                part += __shfl_xor_sync(0xffffffffu, part, 2);
-                if (tq == 0) red[gw][p] = part;
+                if (s & 1) {
+                    part += __shfl_xor_sync(0xffffffffu, part, 1);
+                    part += __shfl_xor_sync(0xffffffffu, part, 2);
+                    if (tq == 0) red[gw][p] = part;
+                    part = 0.0;
+                }
+            };
+            issue(0);
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                if (s + 1 < 8) issue(s + 1);
+                contract(s);
             }
-            mbar_arrive(&sm.red_full[k & 1]);
+            group_sync(1);
+            // lane p: t_p; warp 0 writes the potentials, all G warps form w_p
+            double wp = 0.0;
+            if (lane < cnt) {
+                const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
+                if (gw == 0) {
+                    ddmax = fmax(ddmax, epi(p0 + lane, t));
+                    wp = epi.w_next[p0 + lane];
+                } else {
+                    wp = epi.weight(p0 + lane, t);
+                }
+            }
+            // publish xw[p][a0..a0+3] = w_p X_p[a] for chunk k
+            if (k >= 2) mbar_wait(&sm.xw_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
+            {
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[lane][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[lane][a0 + 2]);
+                double2* dst = reinterpret_cast<double2*>(&sm.xw[k & 1][lane][a0]);
+                dst[0] = make_double2(wp * xa.x, wp * xa.y);
+                dst[1] = make_double2(wp * xb.x, wp * xb.y);
+            }
+            mbar_arrive(&sm.xw_full[k & 1]);
         }
+        if (gw == 0) warp_max_atomic(dmax, ddmax);
     } else {
-        // ------------------------------------------------------------ update + spread
+        // ------------------------------------------------------------ spread
         double S[8][2][2];  // S[mt][nt] = S[a0 + (mt>>1)][8(mt&1) + gq][8nt + 2tq + i]
         int32_t cur_key = -1;
         int64_t org = 0;
-        double ddmax = 0.0;
         auto flush = [&]() {
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
@@ -427,71 +467,58 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                         if (S[mt][nt][i] != 0.0) atomicAdd(grid_out + row + 8 * nt + 2 * tq + i, S[mt][nt][i]);
             }
         };
-        int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
-            const int4 dsc = dsc_next;
-            if (k + 1 < nck) dsc_next = desc[c + 1];
-            const int64_t p0 = dsc.x;
-            const int cnt = dsc.y;
-            if (dsc.z != cur_key) {
+            const int32_t key = desc[c].z;
+            if (key != cur_key) {
                 if (cur_key >= 0) flush();
-                cur_key = dsc.z;
-                org = origin(cur_key);
+                cur_key = key;
+                org = origin(key);
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
-            if (lane < cnt) epi.prefetch(p0 + lane);
-            // t_p from the gather partials; the update; the spread weight of slot `lane`
-            mbar_wait(&sm.red_full[k & 1], (uint32_t)((k >> 1) & 1));
-            double t = 0.0;
-            if (lane < cnt) {
-                const double(*red)[kChunk] = sm.red[k & 1];
-                t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
-            }
-            mbar_arrive(&sm.red_empty[k & 1]);
-            double wn = 0.0;
-            if (lane < cnt) {
-                if (gw == 0) {
-                    ddmax = fmax(ddmax, epi(p0 + lane, t));
-                    wn = epi.w_next[p0 + lane];
-                } else {
-                    wn = epi.weight(p0 + lane, t);
-                }
-            }
+            mbar_wait(&sm.xw_full[k & 1], (uint32_t)((k >> 1) & 1));
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
-            const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
+            const double(*xw)[kStride] = sm.xw[k & 1];
+            // fragments of k-step ks+1 are formed before the DMMAs of k-step ks are issued
+            double am[2][8], bf[2][2];
+            auto form = [&](const int ks) {
                 const int p = 4 * ks + tq;
-                const double wp = __shfl_sync(0xffffffffu, wn, p);
-                const double b0 = wz[p][gq];
-                const double b1 = wz[p][8 + gq];
-                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
-                const double xv[4] = {wp * xa.x, wp * xa.y, wp * xb.x, wp * xb.y};
+                bf[ks & 1][0] = wz[p][gq];
+                bf[ks & 1][1] = wz[p][8 + gq];
+                const double2 xa = *reinterpret_cast<const double2*>(&xw[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&xw[p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
+                for (int mt = 0; mt < 8; ++mt) am[ks & 1][mt] = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
+            };
+            form(0);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                if (ks + 1 < 8) form(ks + 1);
+#pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
-                    const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
-                    dmma(S[mt][0][0], S[mt][0][1], am, b0);
-                    dmma(S[mt][1][0], S[mt][1][1], am, b1);
+                    dmma(S[mt][0][0], S[mt][0][1], am[ks & 1][mt], bf[ks & 1][0]);
+                    dmma(S[mt][1][0], S[mt][1][1], am[ks & 1][mt], bf[ks & 1][1]);
                 }
             }
-            group_sync(2);  // all S warps are done with the window slot
-            if (warp == 4 && lane == 0 && k + kRing < nck) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&sm.win_full[slot], kWinBytes);
-                bulk_g2s(&sm.win[slot][0][0][0], win + (c + kRing) * kWinDoubles, kWinBytes, &sm.win_full[slot]);
+            group_sync(2);  // all S warps are done with xw[k&1] and window slot
+            if (warp == 4 && lane == 0) {
+                mbar_arrive(&sm.xw_empty[k & 1]);
+                if (k + kRing < nck) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&sm.win_full[slot], kWinBytes);
+                    bulk_g2s(&sm.win[slot][0][0][0], win + (c + kRing) * kWinDoubles, kWinBytes, &sm.win_full[slot]);
+                }
             }
         }
         if (cur_key >= 0) flush();
-        if (gw == 0) warp_max_atomic(dmax, ddmax);
     }
 }
 
