@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libuotk.so")
+LIB_PATH = os.environ.get("UOTK_LIB_PATH") or os.path.join(HERE, "libuotk.so")  # override: A/B builds
 
 UOTK_OK = 0
 STATUS = {
