@@ -382,50 +382,35 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
             double(*red)[kChunk] = sm.red[k & 1];
-            // 8 steps s = (m-tile mt = s>>1, a-half h = s&1: n-tiles 4h..4h+3), software
-            // pipelined: the DMMAs of step s+1 are issued before step s is contracted, so
-            // the contraction never waits for its own DMMAs to drain
-            double acc[2][4][2];
-            double part = 0.0;
-            auto issue = [&](const int s) {
-                const int p = 8 * (s >> 1) + gq;
-                double(&ac)[4][2] = acc[s & 1];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) ac[j][0] = ac[j][1] = 0.0;
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+                double acc[8][2];
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double az = wz[p][4 * ks + tq];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(ac[j][0], ac[j][1], az, Fb[4 * (s & 1) + j][ks]);
+                    for (int nt = 0; nt < 8; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
                 }
-            };
-            auto contract = [&](const int s) {
-                const int p = 8 * (s >> 1) + gq;
-                const double(&ac)[4][2] = acc[s & 1];
                 const double2 ylo = *reinterpret_cast<const double2*>(&wy[p][2 * tq]);
                 const double2 yhi = *reinterpret_cast<const double2*>(&wy[p][8 + 2 * tq]);
-                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0 + 2 * (s & 1)]);
-                const double xv[2] = {xa.x, xa.y};
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                double part = 0.0;
 #pragma unroll
-                for (int al = 0; al < 2; ++al) {
-                    double q = ac[2 * al][0] * ylo.x;
-                    q = fma(ac[2 * al][1], ylo.y, q);
-                    q = fma(ac[2 * al + 1][0], yhi.x, q);
-                    q = fma(ac[2 * al + 1][1], yhi.y, q);
+                for (int al = 0; al < 4; ++al) {
+                    double q = acc[2 * al][0] * ylo.x;
+                    q = fma(acc[2 * al][1], ylo.y, q);
+                    q = fma(acc[2 * al + 1][0], yhi.x, q);
+                    q = fma(acc[2 * al + 1][1], yhi.y, q);
                     part = fma(q, xv[al], part);
                 }
-                if (s & 1) {
-                    part += __shfl_xor_sync(0xffffffffu, part, 1);
-                    part += __shfl_xor_sync(0xffffffffu, part, 2);
-                    if (tq == 0) red[gw][p] = part;
-                    part = 0.0;
-                }
-            };
-            issue(0);
-#pragma unroll
-            for (int s = 0; s < 8; ++s) {
-                if (s + 1 < 8) issue(s + 1);
-                contract(s);
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                if (tq == 0) red[gw][p] = part;
             }
             group_sync(1);
             // lane p: t_p; warp 0 writes the potentials, all G warps form w_p
@@ -485,27 +470,20 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
             const double(*xw)[kStride] = sm.xw[k & 1];
-            // fragments of k-step ks+1 are formed before the DMMAs of k-step ks are issued
-            double am[2][8], bf[2][2];
-            auto form = [&](const int ks) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
                 const int p = 4 * ks + tq;
-                bf[ks & 1][0] = wz[p][gq];
-                bf[ks & 1][1] = wz[p][8 + gq];
+                const double b0 = wz[p][gq];
+                const double b1 = wz[p][8 + gq];
                 const double2 xa = *reinterpret_cast<const double2*>(&xw[p][a0]);
                 const double2 xb = *reinterpret_cast<const double2*>(&xw[p][a0 + 2]);
                 const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
-                for (int mt = 0; mt < 8; ++mt) am[ks & 1][mt] = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
-            };
-            form(0);
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                if (ks + 1 < 8) form(ks + 1);
-#pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
-                    dmma(S[mt][0][0], S[mt][0][1], am[ks & 1][mt], bf[ks & 1][0]);
-                    dmma(S[mt][1][0], S[mt][1][1], am[ks & 1][mt], bf[ks & 1][1]);
+                    const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
+                    dmma(S[mt][0][0], S[mt][0][1], am, b0);
+                    dmma(S[mt][1][0], S[mt][1][1], am, b1);
                 }
             }
             group_sync(2);  // all S warps are done with xw[k&1] and window slot
