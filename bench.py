@@ -278,7 +278,8 @@ def fp64_peak():
     try:
         with open(FP64_PEAK_FILE) as f:
             j = json.load(f)
-        return float(j["tflops"]), f"measured DFMA microbenchmark ({j.get('when', '?')})"
+        return float(j["tflops"]), (f"measured FP64 peak, max of DMMA {j.get('dmma_tflops')} and DFMA "
+                                    f"{j.get('dfma_tflops')} TFLOP/s microbenchmarks (profiles/fp64_peak.json)")
     except (OSError, ValueError, KeyError):
         return FP64_PEAK_TFLOPS_NOMINAL, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
 
