@@ -83,9 +83,17 @@ typedef struct {
     double eps_B;     /* IMQ boundary band width in torus units; 0 = auto                 */
     double h;         /* torus scaling h (Eq. 4.7, Rem. 4.3 P:610); 0 = auto        */
     double tol;       /* target truncation tolerance of the auto rules; 0 = 1e-16        */
-    int32_t flags;    /* reserved, must be 0                                             */
+    int32_t flags;    /* UOTK_FLAG_* bits below; 0 = automatic                           */
     int32_t reserved; /* must be 0                                                       */
 } uotk_opts;
+
+/* opts.flags: which spread/gather kernels the NFFT path may use (results agree to
+ * rounding; for cross-checks and benchmarks).  By default the cell-group kernels
+ * (points sorted by cell, chunks of <= 32 points sharing one window footprint,
+ * DESIGN.md §7) run whenever m = 8 and the point set is dense enough, else the
+ * generic thread-per-point kernels.  At most one of the two bits may be set. */
+#define UOTK_FLAG_GENERIC 1  /* always the generic thread-per-point kernels          */
+#define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m must be 8)     */
 
 /* What a call actually used (any pointer to it may be NULL). */
 typedef struct {

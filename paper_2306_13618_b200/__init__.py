@@ -23,6 +23,7 @@ from ._native import UotkError, UotkOpts, UotkInfo, UotkUotResult  # noqa: F401
 GAUSS = 0
 IMQ = 1
 AUTO, NFFT, DIRECT = 0, 1, 2
+FLAG_GENERIC, FLAG_CHUNKED = 1, 2  # opts["flags"]: kernel family of the NFFT passes (uotk.h)
 _KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, GAUSS: GAUSS, IMQ: IMQ}
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 

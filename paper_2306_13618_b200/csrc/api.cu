@@ -22,9 +22,9 @@ void ensure_pool();
 void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
                      void* comm);  // nfft.cu
 
-// Optimised NFFT half-step for d = 3 (fused3d.cu); returns false if not applicable.
-bool fused3d_available(const FastParams& fp);
-void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
+// Fused NFFT half-step on chunked point sets (fused12d.cu / fused3d.cu).
+bool chunked_available(const FastParams& fp);
+void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
                            const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s);
 
 namespace {
@@ -53,7 +53,10 @@ uotk_opts resolve(const uotk_opts* o) {
     uotk_opts r;
     memset(&r, 0, sizeof r);
     if (o) r = *o;
-    if (r.flags != 0 || r.reserved != 0) fail(UOTK_EINVAL, "opts.flags / opts.reserved must be 0");
+    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED)) != 0 || r.reserved != 0)
+        fail(UOTK_EINVAL, "unknown opts.flags bits, or opts.reserved != 0");
+    if ((r.flags & UOTK_FLAG_GENERIC) && (r.flags & UOTK_FLAG_CHUNKED))
+        fail(UOTK_EINVAL, "opts.flags: UOTK_FLAG_GENERIC and UOTK_FLAG_CHUNKED are exclusive");
     if (r.method < 0 || r.method > 2) fail(UOTK_EINVAL, "opts.method must be AUTO, NFFT or DIRECT");
     if (r.N < 0 || r.m < 0 || r.p < 0 || r.sigma < 0 || r.eps_B < 0 || r.h < 0 || r.tol < 0 || r.tol >= 1)
         fail(UOTK_EINVAL, "negative option value");
@@ -254,7 +257,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         const size_t ge = grid_elems(fp);
         DevBuf<double> grid(ge, s), grid2;
         DevBuf<double2> spec(ns.sp.spec_elems, s);
-        const bool fused = fused3d_available(fp) && PX.chunked && PY.chunked;
+        const bool fused = chunked_available(fp) && PX.chunked && PY.chunked;
         if (fused) grid2.alloc(ge, s);
         grid.zero();
         spread(PY, wy.p, grid.p, fp, s);  // adjoint NFFT of nu (.) v at y
@@ -266,10 +269,10 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                 // beta-step at x: gather t from g', update, spread mu (.) u into the other grid
                 fft_chain(ns.sp, grid.p, spec.p, s, comm);
                 grid2.zero();
-                fused3d_gather_spread(PX, grid.p, grid2.p, fp, ex, last ? dmax.p : nullptr, s);
+                chunked_gather_spread(PX, grid.p, grid2.p, fp, ex, last ? dmax.p : nullptr, s);
                 fft_chain(ns.sp, grid2.p, spec.p, s, comm);
                 grid.zero();
-                fused3d_gather_spread(PY, grid2.p, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
+                chunked_gather_spread(PY, grid2.p, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
             } else {
                 fft_chain(ns.sp, grid.p, spec.p, s, comm);
                 gather_epi(PX, grid.p, fp, ex, last ? dmax.p : nullptr, s);  // (3.3)

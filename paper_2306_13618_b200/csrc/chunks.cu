@@ -1,0 +1,171 @@
+// Chunk preparation for the tuned cell-group kernels (layout: chunks.cuh): run-length
+// encoding of the sorted cell keys, chunk descriptors, the precomputed window blocks
+// (Kaiser-Bessel values of (4.6)'s phi at every tap), and a cost-balanced static
+// partition of the chunks over the kernels' work units (CTAs for d = 3, warps for d <= 2).
+#include <cub/cub.cuh>
+
+#include "chunks.cuh"
+#include "common.cuh"
+#include "profile.cuh"
+#include "window.cuh"
+
+namespace uotk {
+
+namespace {
+
+inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
+
+__global__ void chunk_count_k(const int32_t* __restrict__ run_len, const int32_t* __restrict__ nruns,
+                              int32_t* __restrict__ nchunk) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < *nruns) nchunk[r] = (run_len[r] + kChunk - 1) / kChunk;
+}
+
+__global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t* __restrict__ run_len,
+                             const int32_t* __restrict__ run_start, const int32_t* __restrict__ chunk_off,
+                             const int32_t* __restrict__ nruns, int4* __restrict__ desc) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= *nruns) return;
+    const int len = run_len[r];
+    const int nc = (len + kChunk - 1) / kChunk;
+    for (int k = 0; k < nc; ++k)
+        desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r], 0);
+}
+
+// window block of every chunk (layout per d: chunks.cuh)
+template <int D>
+__global__ void chunk_window_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
+                               KBWindow w, double* __restrict__ out) {
+    constexpr int kW = chunk_win_doubles(D);
+    constexpr int kRow = D == 3 ? kStride3 : kChunkT;
+    const int64_t c = blockIdx.x;
+    const int4 dsc = desc[c];
+    double* o = out + c * kW;
+    for (int e = threadIdx.x; e < kW; e += blockDim.x) {
+        const int ax = e / (kChunk * kRow);
+        const int r = e - ax * kChunk * kRow;
+        const int p = r / kRow;
+        const int col = r - p * kRow;
+        // tap stored at this column
+        const int a = D == 2 ? ((col - 4 * p) & 15) : col;
+        double val = 0.0;
+        if (p < dsc.y && a < kChunkT) {
+            const double ut = u[ax * n + dsc.x + p];
+            val = kb_phi(ut - floor(ut) + (double)(kChunkM - 1 - a), w);
+        }
+        o[e] = val;
+    }
+}
+
+// cost of a chunk for the static partition: 8 per chunk + g when it opens a cell group
+// (footprint load and flush), in units of 1/8 chunk
+__global__ void chunk_cost_k(const int4* __restrict__ desc, int64_t nchunks, int group_cost,
+                             int32_t* __restrict__ cost) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < nchunks) cost[c] = 8 + ((c == 0 || desc[c].z != desc[c - 1].z) ? group_cost : 0);
+}
+
+// bounds[b] = first chunk whose inclusive cost prefix exceeds b * total / nb
+__global__ void chunk_bounds_k(const int32_t* __restrict__ prefix, int64_t nchunks, int nb,
+                               int32_t* __restrict__ bounds) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    if (b == nb) {
+        bounds[b] = (int32_t)nchunks;
+        return;
+    }
+    const double target = (double)prefix[nchunks - 1] * b / nb;
+    int64_t lo = 0, hi = nchunks;  // first c with prefix[c] > target
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if ((double)prefix[mid] > target) hi = mid;
+        else lo = mid + 1;
+    }
+    bounds[b] = (int32_t)(b == 0 ? 0 : lo);
+}
+
+}  // namespace
+
+bool chunked_available(const FastParams& fp) { return fp.m == kChunkM && fp.d >= 1 && fp.d <= 3; }
+
+// Build the chunk list and the per-chunk window blocks (once per point set).  Chunks pad
+// runs to multiples of 32 slots; when the padding would waste too much work (sparse
+// clouds: d = 3 below 1/4 fill, d = 2 below 1/16) or the window blocks would not fit
+// comfortably in free device memory, the point set stays on the generic kernels
+// (ps.chunked = false).
+void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
+    ps.chunked = false;
+    ps.nchunks = 0;
+    if (!chunked_available(fp) || ps.n == 0 || (fp.flags & UOTK_FLAG_GENERIC)) return;
+    const int d = fp.d;
+    const int n = (int)ps.n;
+    DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(2, s);
+    size_t tmp_bytes = 0, t2 = 0, t3 = 0;
+    UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
+    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_len.p, run_start.p, n, s));
+    tmp_bytes = std::max(tmp_bytes, t2);
+    DevBuf<uint8_t> tmp(tmp_bytes, s);
+    UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
+    add_launches(2);
+    int32_t nruns = 0;
+    UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    UOTK_CUDA(cudaStreamSynchronize(s));
+    t3 = tmp_bytes;
+    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, run_len.p, run_start.p, nruns, s));
+    chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
+    UOTK_LAUNCHED();
+    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, nchunk.p, chunk_off.p, nruns, s));
+    add_launches(2);
+    int32_t last[2];
+    UOTK_CUDA(cudaMemcpyAsync(&last[0], chunk_off.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    UOTK_CUDA(cudaMemcpyAsync(&last[1], nchunk.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    UOTK_CUDA(cudaStreamSynchronize(s));
+    const int64_t nchunks = (int64_t)last[0] + last[1];
+    const double min_fill = d == 3 ? 0.25 : (d == 2 ? 1.0 / 16 : 0.0);
+    const bool forced = fp.flags & UOTK_FLAG_CHUNKED;
+    if (!forced && (double)n < min_fill * kChunk * (double)nchunks) return;  // too sparse for the chunked kernels
+    const size_t win_bytes = (size_t)nchunks * chunk_win_doubles(d) * sizeof(double);
+    size_t free_b = 0, total_b = 0;
+    UOTK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (win_bytes > free_b / 2) {  // keep the generic path rather than exhaust HBM
+        if (forced) fail(UOTK_ENOMEM, "UOTK_FLAG_CHUNKED: window blocks do not fit in device memory");
+        return;
+    }
+    ps.chunk_desc.alloc(nchunks, s);
+    ps.chunk_win.alloc((size_t)nchunks * chunk_win_doubles(d), s);
+    chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
+                                                        ps.chunk_desc.p);
+    UOTK_LAUNCHED();
+    const KBWindow win = make_window(fp.b, kChunkM);
+    {
+        ProfScope prof(kProfSetup, s);
+        if (d == 3) chunk_window_k<3><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
+        else if (d == 2) chunk_window_k<2><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
+        else chunk_window_k<1><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
+        UOTK_LAUNCHED();
+    }
+    // cost-balanced static partition of the chunks over the work units
+    int sms = 148;
+    {
+        int dev = 0;
+        UOTK_CUDA(cudaGetDevice(&dev));
+        UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int nb = (int)std::min<int64_t>((int64_t)sms * chunk_units_per_sm(d), nchunks);
+    DevBuf<int32_t> cost(nchunks, s), prefix(nchunks, s);
+    chunk_cost_k<<<blocks_for(nchunks, 256), 256, 0, s>>>(ps.chunk_desc.p, nchunks, d == 3 ? 2 : 1, cost.p);
+    UOTK_LAUNCHED();
+    size_t t4 = 0;
+    UOTK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t4, cost.p, prefix.p, (int)nchunks, s));
+    DevBuf<uint8_t> tmp2(t4, s);
+    UOTK_CUDA(cub::DeviceScan::InclusiveSum(tmp2.p, t4, cost.p, prefix.p, (int)nchunks, s));
+    add_launches(1);
+    ps.chunk_bounds.alloc(nb + 1, s);
+    chunk_bounds_k<<<blocks_for(nb + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nb, ps.chunk_bounds.p);
+    UOTK_LAUNCHED();
+    ps.chunk_blocks = nb;
+    ps.nchunks = nchunks;
+    ps.chunked = true;
+}
+
+}  // namespace uotk

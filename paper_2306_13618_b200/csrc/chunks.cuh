@@ -1,0 +1,36 @@
+// Chunked point layout shared by the tuned cell-group kernels (fused3d.cu, fused12d.cu)
+// and their preparation (chunks.cu).
+//
+// Points are sorted by grid cell (points.cu); every run of equal keys shares one (2m)^d
+// window footprint.  Runs are cut into chunks of <= 32 points and the window values of
+// every chunk are precomputed once per point set (points do not move between Sinkhorn
+// iterations) into a fixed-size block per chunk, zero for empty slots:
+//   d = 3: [axis 3][slot 32][tap, row stride 20]      (padded: conflict-free fragments)
+//   d = 2: [axis 2][slot 32][16 taps, swizzled]       (tap a of slot p at (a + 4p) & 15)
+//   d = 1: [slot 32][16 taps]                          (each lane reads its own row)
+#pragma once
+#include <cstdint>
+
+namespace uotk {
+
+constexpr int kChunkM = 8;              // window half-width of the tuned kernels
+constexpr int kChunkT = 2 * kChunkM;    // taps per axis
+constexpr int kChunk = 32;              // points per chunk
+constexpr int kStride3 = 20;            // d = 3 padded row stride (doubles)
+// work units of the kernels: d = 3 one CTA (8 warps) per unit, kCtas3 CTAs per SM;
+// d <= 2 one warp per unit, kWarpsD warps per CTA, kCtasD CTAs per SM
+constexpr int kCtas3 = 2;
+constexpr int kWarps2 = 4, kCtas2 = 3;
+constexpr int kWarps1 = 8, kCtas1 = 2;
+__host__ __device__ constexpr int chunk_units_per_sm(int d) {
+    return d == 3 ? kCtas3 : (d == 2 ? kWarps2 * kCtas2 : kWarps1 * kCtas1);
+}
+
+__host__ __device__ constexpr int chunk_win_doubles(int d) {
+    return d == 3 ? 3 * kChunk * kStride3 : d * kChunk * kChunkT;
+}
+
+// d = 2 swizzle: column of tap a in slot row p
+__host__ __device__ __forceinline__ int swz2(int p, int a) { return (a + 4 * p) & 15; }
+
+}  // namespace uotk

@@ -92,6 +92,7 @@ struct FastParams {
     double eps_B = 0;      // IMQ boundary band
     int p = 0;             // IMQ boundary order
     std::vector<double> poly;  // IMQ boundary polynomial in t = (r - r0)/eps_B (torus units), ascending
+    int flags = 0;         // uotk_opts.flags (kernel family policy)
 };
 
 // Sorted, scaled point set on device.
@@ -101,14 +102,14 @@ struct PointSet {
     DevBuf<double> u;        // d * n, SoA, grid units: u_t = (x_t - c_t)/h * ng
     DevBuf<int32_t> key;     // n, linear cell key (sorted ascending)
     DevBuf<int32_t> perm;    // n, sorted position -> caller index
-    // chunked layout of the d = 3 cell-group kernels (fused3d.cu): runs of equal keys
-    // split into chunks of <= 32 points, with the window values precomputed per chunk
+    // chunked layout of the cell-group kernels (chunks.cuh): runs of equal keys split
+    // into chunks of <= 32 points, with the window values precomputed per chunk
     bool chunked = false;
     int64_t nchunks = 0;
     DevBuf<int4> chunk_desc;  // {first point, count, key, 0}
-    DevBuf<double> chunk_win; // nchunks x 3 x 32 x 2m window values (zero for empty slots)
-    DevBuf<int32_t> chunk_bounds;  // chunk_blocks + 1 cost-balanced CTA boundaries
-    int chunk_blocks = 0;
+    DevBuf<double> chunk_win; // nchunks x chunk_win_doubles(d) window values (zero for empty slots)
+    DevBuf<int32_t> chunk_bounds;  // chunk_blocks + 1 cost-balanced work-unit boundaries
+    int chunk_blocks = 0;     // work units: CTAs (d = 3) or warps (d <= 2)
 };
 
 // Fourier-side plan: the D_k table and the cuFFT handles.

@@ -64,6 +64,20 @@ struct EpiDot {
     __device__ __forceinline__ void prefetch(int64_t) const {}
 };
 
+// Chunked-kernel adaptors: the Sinkhorn epilogue exposes w_next / weight(); the plain
+// gathers do not spread, and a spread-only pass has no epilogue at all.
+struct EpiNone {
+    double* w_next = nullptr;
+    __device__ double operator()(int64_t, double) const { return 0.0; }
+    __device__ double weight(int64_t, double) const { return 0.0; }
+    __device__ void prefetch(int64_t) const {}
+};
+template <class Epi>
+struct EpiGatherOnly : Epi {
+    double* w_next = nullptr;
+    __device__ double weight(int64_t, double) const { return 0.0; }
+};
+
 // warp max of non-negative doubles, one atomicMax per warp on the uint64 bit pattern
 __device__ __forceinline__ void warp_max_atomic(unsigned long long* dst, double v) {
     if (!dst) return;

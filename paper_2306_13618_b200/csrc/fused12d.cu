@@ -1,0 +1,350 @@
+// Tuned d = 2 and d = 1 NFFT passes: cell-group kernels with one warp per work unit
+// (DESIGN.md §7).  Same chunked layout as the d = 3 kernels (chunks.cuh): points sorted by
+// cell, runs of equal keys cut into chunks of <= 32 points, window values precomputed per
+// chunk.  A warp walks a contiguous, cost-balanced range of chunks; the footprint of the
+// current cell group — (2m)^d grid values, 16 x 16 in d = 2 — lives in the warp's
+// registers: the gather operand F is loaded once per group and the spread accumulators S
+// are flushed once per group (fp64 RED), so the grid sees one read and one atomic flush
+// per group instead of (2m)^d atomics per point.
+//
+// d = 2, with X_p, Y_p the windows of point p along the two axes (outer / inner sums of
+// (4.6)):
+//   gather  G[p, b] = sum_a X_p[a] F[a, b]         (32x16x16 GEMM on DMMA, mma.sync f64)
+//           t_p     = sum_b G[p, b] Y_p[b]          (per point, quad shuffle reduction)
+//   spread  S[a, b] += sum_p (w_p X_p[a]) Y_p[b]   (16x16x32 GEMM on DMMA)
+// The window block of a chunk (8 KB) is streamed into the warp's shared-memory ring by a
+// TMA bulk copy; its swizzle (tap a of slot p at column (a + 4p) & 15) makes every
+// fragment load hit the minimum number of shared-memory wavefronts.
+//
+// d = 1: lane p holds the 16 window values of point p in registers (loaded straight from
+// the chunk's block); t_p = sum_a X_p[a] F[a] in-lane, and the spread accumulates
+// w_p X_p[a] per lane, reduced across the warp by a transpose-reduction only when the
+// group is flushed.
+#include "chunks.cuh"
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "profile.cuh"
+#include "ptx.cuh"
+
+namespace uotk {
+
+bool chunked_available(const FastParams& fp);  // chunks.cu
+// d = 3 kernels (fused3d.cu)
+void fused3d_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s);
+void fused3d_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
+                          cudaStream_t s);
+void fused3d_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
+                        cudaStream_t s);
+void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
+                           const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s);
+
+namespace {
+
+constexpr int kM = kChunkM;
+constexpr int kW2 = chunk_win_doubles(2);  // 1024 doubles = 8 KB per chunk
+constexpr uint32_t kW2Bytes = kW2 * sizeof(double);
+constexpr int kW1 = chunk_win_doubles(1);  // 512 doubles per chunk
+constexpr int kRing2 = 2;
+
+struct __align__(128) Smem2 {
+    double win[kWarps2][kRing2][kW2];  // per-warp TMA ring of window blocks
+    double red[kWarps2][kChunk];       // per-warp gathered t of the current chunk
+    unsigned long long bar[kWarps2][kRing2];
+};
+
+// MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
+template <int MODE, class Epi>
+__global__ void __launch_bounds__(kWarps2 * 32, kCtas2)
+chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
+            int nunits, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
+            const double* __restrict__ w_in, Epi epi, unsigned long long* dmax) {
+    constexpr bool GATHER = MODE != 1;
+    constexpr bool SPREAD = MODE != 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem2& sm = *reinterpret_cast<Smem2*>(smem_raw);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gq = lane >> 2;  // fragment group: row of A / D, column of B
+    const int tq = lane & 3;   // thread in group
+    const int unit = blockIdx.x * kWarps2 + warp;
+    if (unit >= nunits) return;  // warps are independent: no CTA-wide barrier below
+    const int64_t cbeg = bounds[unit];
+    const int64_t nck = bounds[unit + 1] - cbeg;
+    if (nck <= 0) return;
+    double* swin = &sm.win[warp][0][0];
+    unsigned long long* bar = sm.bar[warp];
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init_fence();
+    }
+    __syncwarp();
+    if (lane == 0) {
+        for (int k = 0; k < kRing2 && k < nck; ++k) {
+            mbar_expect_tx(&bar[k], kW2Bytes);
+            bulk_g2s(swin + k * kW2, win + (cbeg + k) * kW2, kW2Bytes, &bar[k]);
+        }
+    }
+
+    double Fb[2][4];     // Fb[nt][ks] = F[4ks + tq][8nt + gq]          (gather B operand)
+    double S[2][2][2];   // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]  (spread accumulators)
+    int32_t cur_key = -1;
+    int64_t org = 0;  // grid index of footprint (0, 0) of the current group
+    double ddmax = 0.0;
+    auto flush = [&]() {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            double* row = grid_out + org + (int64_t)(8 * mt + gq) * ng + 2 * tq;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (S[mt][nt][i] != 0.0) atomicAdd(row + 8 * nt + i, S[mt][nt][i]);
+        }
+    };
+
+    for (int64_t k = 0; k < nck; ++k) {
+        const int64_t c = cbeg + k;
+        const int buf = (int)(k & 1);
+        const int4 dsc = desc[c];  // {first point, count, key, 0}
+        const int64_t p0 = dsc.x;
+        const int cnt = dsc.y;
+        if (dsc.z != cur_key) {
+            if (SPREAD && cur_key >= 0) flush();
+            cur_key = dsc.z;
+            org = (int64_t)(cur_key / ng - kM + 1) * ng + (cur_key % ng - kM + 1);
+            if (GATHER) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double* row = grid_in + org + (int64_t)(4 * ks + tq) * ng + gq;
+                    Fb[0][ks] = __ldg(row);
+                    Fb[1][ks] = __ldg(row + 8);
+                }
+            }
+            if (SPREAD) {
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
+            }
+        }
+        if (GATHER && lane < cnt) epi.prefetch(p0 + lane);
+        mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
+        const double* X = swin + buf * kW2;
+        const double* Y = X + kChunk * kChunkT;
+
+        double wn = 0.0;  // spread weight of slot `lane`
+        if (GATHER) {
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+                const double* xr = X + p * kChunkT;
+                const double* yr = Y + p * kChunkT;
+                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double a = xr[swz2(p, 4 * ks + tq)];
+                    dmma(acc[0][0], acc[0][1], a, Fb[0][ks]);
+                    dmma(acc[1][0], acc[1][1], a, Fb[1][ks]);
+                }
+                // acc[nt][i] = G[p][8nt + 2tq + i]
+                double part = 0.0;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const double2 y = *reinterpret_cast<const double2*>(yr + swz2(p, 8 * nt + 2 * tq));
+                    part = fma(acc[nt][0], y.x, part);
+                    part = fma(acc[nt][1], y.y, part);
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                if (tq == 0) sm.red[warp][p] = part;
+            }
+            __syncwarp();
+            const double t = sm.red[warp][lane];
+            if (lane < cnt) {
+                ddmax = fmax(ddmax, epi(p0 + lane, t));
+                if (SPREAD) wn = epi.w_next[p0 + lane];
+            }
+        } else {
+            wn = lane < cnt ? w_in[p0 + lane] : 0.0;
+        }
+
+        if (SPREAD) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {  // 4 points per k-step
+                const int p = 4 * ks + tq;
+                const double wp = __shfl_sync(0xffffffffu, wn, p);
+                const double* xr = X + p * kChunkT;
+                const double* yr = Y + p * kChunkT;
+                const double xa0 = wp * xr[swz2(p, gq)];
+                const double xa1 = wp * xr[swz2(p, 8 + gq)];
+                const double yb0 = yr[swz2(p, gq)];
+                const double yb1 = yr[swz2(p, 8 + gq)];
+                dmma(S[0][0][0], S[0][0][1], xa0, yb0);
+                dmma(S[0][1][0], S[0][1][1], xa0, yb1);
+                dmma(S[1][0][0], S[1][0][1], xa1, yb0);
+                dmma(S[1][1][0], S[1][1][1], xa1, yb1);
+            }
+        }
+        __syncwarp();  // the warp is done with window slot `buf` and red
+        if (lane == 0 && k + kRing2 < nck) {
+            fence_proxy_async();
+            mbar_expect_tx(&bar[buf], kW2Bytes);
+            bulk_g2s(swin + buf * kW2, win + (c + kRing2) * kW2, kW2Bytes, &bar[buf]);
+        }
+    }
+    if (SPREAD && cur_key >= 0) flush();
+    if (GATHER) warp_max_atomic(dmax, ddmax);
+}
+
+// transpose-reduction of v[0..15] over the 32 lanes: returns sum_lanes v[lane >> 1]
+__device__ __forceinline__ double warp_transpose_reduce16(double (&v)[16], int lane) {
+    double v8[8], v4[4], v2[2];
+    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double send = h16 ? v[j] : v[j + 8];
+        const double keep = h16 ? v[j + 8] : v[j];
+        v8[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double send = h8 ? v8[j] : v8[j + 4];
+        const double keep = h8 ? v8[j + 4] : v8[j];
+        v4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const double send = h4 ? v4[j] : v4[j + 2];
+        const double keep = h4 ? v4[j + 2] : v4[j];
+        v2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    const double send = h2 ? v2[0] : v2[1];
+    double r = (h2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    return r;
+}
+
+template <int MODE, class Epi>
+__global__ void __launch_bounds__(kWarps1 * 32, kCtas1)
+chunked1d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
+            int nunits, const double* __restrict__ grid_in, double* __restrict__ grid_out,
+            const double* __restrict__ w_in, Epi epi, unsigned long long* dmax) {
+    constexpr bool GATHER = MODE != 1;
+    constexpr bool SPREAD = MODE != 2;
+    const int lane = threadIdx.x & 31;
+    const int unit = blockIdx.x * kWarps1 + (threadIdx.x >> 5);
+    if (unit >= nunits) return;
+    const int64_t cbeg = bounds[unit];
+    const int64_t cend = bounds[unit + 1];
+    double F[kChunkT], S[kChunkT];
+    int32_t cur_key = -1;
+    double ddmax = 0.0;
+    auto flush = [&]() {
+        const double v = warp_transpose_reduce16(S, lane);
+        if (!(lane & 1) && v != 0.0) atomicAdd(grid_out + (cur_key - kM + 1) + (lane >> 1), v);
+    };
+    for (int64_t c = cbeg; c < cend; ++c) {
+        const int4 dsc = desc[c];
+        const int64_t p0 = dsc.x;
+        const int cnt = dsc.y;
+        if (dsc.z != cur_key) {
+            if (SPREAD && cur_key >= 0) flush();
+            cur_key = dsc.z;
+            if (GATHER) {
+                const double* f = grid_in + (cur_key - kM + 1);
+#pragma unroll
+                for (int a = 0; a < kChunkT; ++a) F[a] = __ldg(f + a);
+            }
+            if (SPREAD) {
+#pragma unroll
+                for (int a = 0; a < kChunkT; ++a) S[a] = 0.0;
+            }
+        }
+        // this lane's window row (zero for empty slots)
+        double X[kChunkT];
+        const double2* xr = reinterpret_cast<const double2*>(win + c * kW1 + lane * kChunkT);
+#pragma unroll
+        for (int a = 0; a < kChunkT / 2; ++a) {
+            const double2 v = __ldg(xr + a);
+            X[2 * a] = v.x;
+            X[2 * a + 1] = v.y;
+        }
+        double wn = 0.0;
+        if (GATHER) {
+            double t = 0.0;
+#pragma unroll
+            for (int a = 0; a < kChunkT; ++a) t = fma(X[a], F[a], t);
+            if (lane < cnt) {
+                ddmax = fmax(ddmax, epi(p0 + lane, t));
+                if (SPREAD) wn = epi.w_next[p0 + lane];
+            }
+        } else {
+            wn = lane < cnt ? w_in[p0 + lane] : 0.0;
+        }
+        if (SPREAD) {
+#pragma unroll
+            for (int a = 0; a < kChunkT; ++a) S[a] = fma(wn, X[a], S[a]);
+        }
+    }
+    if (SPREAD && cur_key >= 0) flush();
+    if (GATHER) warp_max_atomic(dmax, ddmax);
+}
+
+template <int MODE, class Epi>
+void launch12(const PointSet& ps, const double* gin, double* gout, const double* w, const FastParams& fp,
+              const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
+    if (ps.n == 0 || ps.nchunks == 0) return;
+    const int nunits = ps.chunk_blocks;
+    ProfScope prof(tag, s);
+    if (fp.d == 2) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            UOTK_CUDA(cudaFuncSetAttribute(chunked2d_k<MODE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sizeof(Smem2)));
+            attr_set = true;
+        }
+        const int blocks = (nunits + kWarps2 - 1) / kWarps2;
+        chunked2d_k<MODE, Epi><<<blocks, kWarps2 * 32, sizeof(Smem2), s>>>(
+            ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, gin, gout, w, epi, dmax);
+    } else {
+        const int blocks = (nunits + kWarps1 - 1) / kWarps1;
+        chunked1d_k<MODE, Epi><<<blocks, kWarps1 * 32, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p,
+                                                                nunits, gin, gout, w, epi, dmax);
+    }
+    UOTK_LAUNCHED();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ dispatch over d (nfft.cu, api.cu)
+void chunked_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
+    if (fp.d == 3) return fused3d_spread(ps, w, grid, fp, s);
+    launch12<1, EpiNone>(ps, nullptr, grid, w, fp, EpiNone{}, nullptr, s, kProfSpread);
+}
+
+void chunked_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
+                          cudaStream_t s) {
+    if (fp.d == 3) return fused3d_gather_store(ps, grid, fp, epi, s);
+    EpiGatherOnly<EpiStore> e;
+    static_cast<EpiStore&>(e) = epi;
+    launch12<2, EpiGatherOnly<EpiStore>>(ps, grid, nullptr, nullptr, fp, e, nullptr, s, kProfGather);
+}
+
+void chunked_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
+                        cudaStream_t s) {
+    if (fp.d == 3) return fused3d_gather_dot(ps, grid, fp, epi, s);
+    EpiGatherOnly<EpiDot> e;
+    static_cast<EpiDot&>(e) = epi;
+    launch12<2, EpiGatherOnly<EpiDot>>(ps, grid, nullptr, nullptr, fp, e, nullptr, s, kProfGather);
+}
+
+// one Sinkhorn half-step at the points of ps: gather from grid_in, update (3.3)/(3.4),
+// spread the new weights into grid_out
+void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
+                           const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s) {
+    if (fp.d == 3) return fused3d_gather_spread(ps, grid_in, grid_out, fp, epi, dmax, s);
+    launch12<0, EpiSinkhorn>(ps, grid_in, grid_out, nullptr, fp, epi, dmax, s, kProfFused);
+}
+
+}  // namespace uotk

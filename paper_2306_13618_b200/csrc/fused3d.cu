@@ -24,66 +24,29 @@
 // scripts/dmma_probe.cu) from 1/8 of the instructions of a DFMA formulation.
 #include <cub/cub.cuh>
 
+#include "chunks.cuh"
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "profile.cuh"
+#include "ptx.cuh"
 #include "window.cuh"
 
 namespace uotk {
 
 namespace {
 
-constexpr int kM = 8;               // window half-width of the tuned kernels
-constexpr int kT = 2 * kM;          // taps per axis
-constexpr int kThreads = 256;       // 8 warps
-constexpr int kChunk = 32;          // points per chunk
-constexpr int kStride = 20;         // padded row stride (doubles) of a window matrix: conflict-free fragments
-constexpr int kWinDoubles = 3 * kChunk * kStride;
+constexpr int kM = kChunkM;          // window half-width of the tuned kernels
+constexpr int kThreads = 256;        // 8 warps
+constexpr int kStride = kStride3;    // padded row stride (doubles) of a window matrix: conflict-free fragments
+constexpr int kWinDoubles = chunk_win_doubles(3);
 constexpr uint32_t kWinBytes = kWinDoubles * sizeof(double);  // 15 KB
-constexpr int kBlocksPerSM = 2;
+constexpr int kBlocksPerSM = kCtas3;
 
 struct __align__(128) Smem {
     double win[2][3][kChunk][kStride];  // double-buffered window blocks (TMA destination)
     double red[kThreads / 32][kChunk];  // per-warp partial gathers
     unsigned long long bar[2];          // mbarriers of the two buffers
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// TMA bulk copy global -> shared, completion signalled on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// D[8x8] += A[8x4] B[4x8] in fp64 on the tensor cores.  Fragments (verified by
-// scripts/dmma_layout.cu): a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
-// {d0, d1} = D[lane>>2][2(lane&3) + {0,1}].
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
 
 // MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
 template <int MODE, class Epi>
@@ -298,13 +261,6 @@ struct __align__(128) SmemWS {
     unsigned long long xw_empty[2];
 };
 
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void group_sync(int id) {  // named barrier over one 4-warp group
-    asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
-}
-
 __global__ void __launch_bounds__(256, kBlocksPerSM)
 sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
                 int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out, EpiSinkhorn epi,
@@ -500,86 +456,6 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     }
 }
 
-// ---------------------------------------------------------------- chunk preparation
-__global__ void chunk_count_k(const int32_t* __restrict__ run_len, const int32_t* __restrict__ nruns,
-                              int32_t* __restrict__ nchunk) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < *nruns) nchunk[r] = (run_len[r] + kChunk - 1) / kChunk;
-}
-
-__global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t* __restrict__ run_len,
-                             const int32_t* __restrict__ run_start, const int32_t* __restrict__ chunk_off,
-                             const int32_t* __restrict__ nruns, int4* __restrict__ desc) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= *nruns) return;
-    const int len = run_len[r];
-    const int nc = (len + kChunk - 1) / kChunk;
-    for (int k = 0; k < nc; ++k)
-        desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r], 0);
-}
-
-// window values of every chunk: [chunk][axis][slot][tap (row stride kStride)], zero for
-// empty slots and for the row padding
-__global__ void chunk_window_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
-                               KBWindow w, double* __restrict__ out) {
-    const int64_t c = blockIdx.x;
-    const int4 dsc = desc[c];
-    double* o = out + c * kWinDoubles;
-    for (int e = threadIdx.x; e < kWinDoubles; e += blockDim.x) {
-        const int ax = e / (kChunk * kStride);
-        const int r = e - ax * kChunk * kStride;
-        const int p = r / kStride;
-        const int a = r - p * kStride;
-        double val = 0.0;
-        if (p < dsc.y && a < kT) {
-            const double ut = u[ax * n + dsc.x + p];
-            val = kb_phi(ut - floor(ut) + (double)(kM - 1 - a), w);
-        }
-        o[e] = val;
-    }
-}
-
-// cost of a chunk for the static partition: 8 per chunk + 2 when it opens a cell group
-// (footprint load and flush), in units of 1/8 chunk
-__global__ void chunk_cost_k(const int4* __restrict__ desc, int64_t nchunks, int32_t* __restrict__ cost) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < nchunks) cost[c] = 8 + ((c == 0 || desc[c].z != desc[c - 1].z) ? 2 : 0);
-}
-
-// bounds[b] = first chunk whose inclusive cost prefix exceeds b * total / nb
-__global__ void chunk_bounds_k(const int32_t* __restrict__ prefix, int64_t nchunks, int nb,
-                               int32_t* __restrict__ bounds) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b > nb) return;
-    if (b == nb) {
-        bounds[b] = (int32_t)nchunks;
-        return;
-    }
-    const double target = (double)prefix[nchunks - 1] * b / nb;
-    int64_t lo = 0, hi = nchunks;  // first c with prefix[c] > target
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) / 2;
-        if ((double)prefix[mid] > target) hi = mid;
-        else lo = mid + 1;
-    }
-    bounds[b] = (int32_t)(b == 0 ? 0 : lo);
-}
-
-inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
-
-// The Sinkhorn epilogue exposes w_next / weight(); the plain gathers do not spread.
-struct EpiNone {
-    double* w_next = nullptr;
-    __device__ double operator()(int64_t, double) const { return 0.0; }
-    __device__ double weight(int64_t, double) const { return 0.0; }
-    __device__ void prefetch(int64_t) const {}
-};
-template <class Epi>
-struct EpiGatherOnly : Epi {
-    double* w_next = nullptr;
-    __device__ double weight(int64_t, double) const { return 0.0; }
-};
-
 template <int MODE, class Epi>
 void launch(const PointSet& ps, const double* gin, double* gout, const double* w, const FastParams& fp,
             const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
@@ -592,74 +468,6 @@ void launch(const PointSet& ps, const double* gin, double* gout, const double* w
 }
 
 }  // namespace
-
-bool fused3d_available(const FastParams& fp) { return fp.d == 3 && fp.m == kM; }
-
-// Build the chunk list and the per-chunk window blocks (once per point set).  Chunks
-// pad runs to multiples of 32 slots; when the padding would waste more than 3/4 of the
-// work (sparse clouds) the point set stays on the generic kernels (ps.chunked = false).
-void fused3d_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
-    ps.chunked = false;
-    ps.nchunks = 0;
-    if (!fused3d_available(fp) || ps.n == 0) return;
-    const int n = (int)ps.n;
-    DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(2, s);
-    size_t tmp_bytes = 0, t2 = 0, t3 = 0;
-    UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
-    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_len.p, run_start.p, n, s));
-    tmp_bytes = std::max(tmp_bytes, t2);
-    DevBuf<uint8_t> tmp(tmp_bytes, s);
-    UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
-    add_launches(2);
-    int32_t nruns = 0;
-    UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    UOTK_CUDA(cudaStreamSynchronize(s));
-    t3 = tmp_bytes;
-    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, run_len.p, run_start.p, nruns, s));
-    chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
-    UOTK_LAUNCHED();
-    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, nchunk.p, chunk_off.p, nruns, s));
-    add_launches(2);
-    int32_t last[2];
-    UOTK_CUDA(cudaMemcpyAsync(&last[0], chunk_off.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    UOTK_CUDA(cudaMemcpyAsync(&last[1], nchunk.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    UOTK_CUDA(cudaStreamSynchronize(s));
-    const int64_t nchunks = (int64_t)last[0] + last[1];
-    if ((double)n < 0.25 * kChunk * (double)nchunks) return;  // too sparse for the chunked kernel
-    ps.chunk_desc.alloc(nchunks, s);
-    ps.chunk_win.alloc((size_t)nchunks * kWinDoubles, s);
-    chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
-                                                        ps.chunk_desc.p);
-    UOTK_LAUNCHED();
-    const KBWindow win = make_window(fp.b, kM);
-    {
-        ProfScope prof(kProfSetup, s);
-        chunk_window_k<<<(unsigned)nchunks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
-        UOTK_LAUNCHED();
-    }
-    // cost-balanced static partition of the chunks over the CTAs
-    int sms = 148;
-    {
-        int dev = 0;
-        UOTK_CUDA(cudaGetDevice(&dev));
-        UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    const int nb = (int)std::min<int64_t>((int64_t)sms * kBlocksPerSM, nchunks);
-    DevBuf<int32_t> cost(nchunks, s), prefix(nchunks, s);
-    chunk_cost_k<<<blocks_for(nchunks, 256), 256, 0, s>>>(ps.chunk_desc.p, nchunks, cost.p);
-    UOTK_LAUNCHED();
-    size_t t4 = 0;
-    UOTK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t4, cost.p, prefix.p, (int)nchunks, s));
-    DevBuf<uint8_t> tmp2(t4, s);
-    UOTK_CUDA(cub::DeviceScan::InclusiveSum(tmp2.p, t4, cost.p, prefix.p, (int)nchunks, s));
-    add_launches(1);
-    ps.chunk_bounds.alloc(nb + 1, s);
-    chunk_bounds_k<<<blocks_for(nb + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nb, ps.chunk_bounds.p);
-    UOTK_LAUNCHED();
-    ps.chunk_blocks = nb;
-    ps.nchunks = nchunks;
-    ps.chunked = true;
-}
 
 void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
                            const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s) {

@@ -1,7 +1,7 @@
 // Generic NFFT passes (any d, any m): window spreading (adjoint NFFT, inner sum of
 // (4.6)), the FFT chain with the fused D_k multiplication, and interpolation
 // (forward NFFT, outer sum of (4.6)) — P:590-592.  These are the simple
-// thread-per-point kernels; the tuned d = 3 fused kernels live in fused3d.cu.
+// thread-per-point kernels; the tuned cell-group kernels live in fused3d.cu / fused12d.cu.
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "profile.cuh"
@@ -10,12 +10,12 @@
 namespace uotk {
 
 void comm_allreduce_spectrum(double2* buf, size_t count, void* comm, cudaStream_t s);  // comm.cu
-// tuned d = 3 passes (fused3d.cu)
-bool fused3d_available(const FastParams& fp);
-void fused3d_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s);
-void fused3d_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
+// tuned cell-group passes for chunked point sets (fused12d.cu dispatches over d)
+bool chunked_available(const FastParams& fp);
+void chunked_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s);
+void chunked_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
                           cudaStream_t s);
-void fused3d_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
+void chunked_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
                         cudaStream_t s);
 
 namespace {
@@ -192,8 +192,8 @@ void gather_dm(const PointSet& ps, const double* grid, const FastParams& fp, con
 
 void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s) {
     if (ps.n == 0) return;
-    if (fused3d_available(fp) && ps.chunked) {
-        fused3d_spread(ps, w_sorted, grid, fp, s);
+    if (chunked_available(fp) && ps.chunked) {
+        chunked_spread(ps, w_sorted, grid, fp, s);
         return;
     }
     UOTK_DISPATCH_DM(fp.d, fp.m, (spread_dm<DD, MM>(ps, w_sorted, grid, fp, s)));
@@ -204,14 +204,14 @@ void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, co
                 unsigned long long* dmax, cudaStream_t s) {
     if (ps.n == 0) return;
     if constexpr (std::is_same<Epi, EpiStore>::value) {
-        if (fused3d_available(fp) && ps.chunked) {
-            fused3d_gather_store(ps, grid, fp, epi, s);
+        if (chunked_available(fp) && ps.chunked) {
+            chunked_gather_store(ps, grid, fp, epi, s);
             return;
         }
     }
     if constexpr (std::is_same<Epi, EpiDot>::value) {
-        if (fused3d_available(fp) && ps.chunked) {
-            fused3d_gather_dot(ps, grid, fp, epi, s);
+        if (chunked_available(fp) && ps.chunked) {
+            chunked_gather_dot(ps, grid, fp, epi, s);
             return;
         }
     }

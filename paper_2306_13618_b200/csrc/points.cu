@@ -10,7 +10,7 @@
 namespace uotk {
 
 void comm_allreduce_minmax(double* dmin, int nmin, double* dmax, int nmax, void* comm, cudaStream_t s);  // comm.cu
-void fused3d_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s);  // fused3d.cu
+void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s);  // chunks.cu
 
 namespace {
 
@@ -232,7 +232,7 @@ void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams&
     else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
     else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
     UOTK_LAUNCHED();
-    fused3d_prepare(ps, fp, s);  // chunk list + precomputed windows (d = 3 tuned kernels)
+    chunked_prepare(ps, fp, s);  // chunk list + precomputed windows (tuned cell-group kernels)
 }
 
 void permute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s) {

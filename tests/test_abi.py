@@ -84,10 +84,11 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     with pytest.raises(uk.UotkError) as e:
         uk.mmd2(x, np.ones(4), x, np.ones(4), "imq", 0.0)
     assert e.value.code == -1
-    with pytest.raises(uk.UotkError) as e:
-        uk.kernel_sum(x, np.ones(4), x, "gauss", 0.1, opts={"flags": 1})
-    assert e.value.code == -1
-    assert "flags" in _native.load().uotk_last_error().decode()
+    for bad in (4, uk.FLAG_GENERIC | uk.FLAG_CHUNKED):
+        with pytest.raises(uk.UotkError) as e:
+            uk.kernel_sum(x, np.ones(4), x, "gauss", 0.1, opts={"flags": bad})
+        assert e.value.code == -1
+        assert "flags" in _native.load().uotk_last_error().decode()
 
 
 def test_dtype_and_shape_checks():

@@ -269,3 +269,82 @@ def test_mmd2_c2_full_size_nfft_vs_direct(uk, kind):
     yy = uk.mmd2(y, b, y[:0], b[:0], kind, param, opts={"method": "direct"})
     denom = max(abs(v2), 1e-3 * (abs(xx) + abs(yy)))
     assert abs(v1 - v2) / denom <= 1e-8, (v1, v2, info)
+
+
+# ------------------------------------------------------------------ cell-group kernels in d = 1, 2
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+@pytest.mark.parametrize("signed", [False, True])
+def test_kernel_sum_cell_group_kernels(uk, d, kind, signed):
+    """The cell-group (chunked) kernels forced at any density and the generic
+    thread-per-point kernels, both against the oracle; ragged sizes (chunks of 32 with a
+    ragged tail in every cell)."""
+    pr = W.random_sum(d, 6001, 3001, kind=kind, param=(0.0025 if kind == W.GAUSS else 0.05), seed=20 + d,
+                      signed=signed)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    for flags in (uk.FLAG_CHUNKED, uk.FLAG_GENERIC):
+        got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), kind, pr.param,
+                            opts={"method": "nfft", "flags": flags})
+        err = rel_err(got.cpu().numpy(), ref, signed)
+        assert err <= 1e-9, (flags, err)
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_kernel_sum_dense_cloud_auto(uk, d):
+    """A dense cloud (wide Gaussian, C1's eps = 0.05) takes the cell-group kernels by
+    default (hundreds of points per cell)."""
+    pr = W.random_sum(d, 40_000, 2_003, kind=W.GAUSS, param=0.05, seed=31)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"})
+    assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9
+
+
+@pytest.mark.parametrize("flags", ["chunked", "generic"])
+def test_uot_c4_like_reduced(uk, flags):
+    """C4's parameters (d = 2, eps = 0.002, lam = 2) at reduced n: the fused d = 2
+    half-step (gather -> update -> spread in one launch) and the generic path."""
+    pr = W.c4_uot(n=5003, m=4001, iters=12)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    f = uk.FLAG_CHUNKED if flags == "chunked" else uk.FLAG_GENERIC
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": "nfft", "flags": f})
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+def test_uot_c1_chunked_nfft(uk):
+    """C1 exactly through the d = 2 fused half-step (forced; AUTO picks DIRECT at C1)."""
+    pr = W.c1_uot()
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": "nfft", "flags": uk.FLAG_CHUNKED})
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+def test_uot_c4_full_size_sampled(uk):
+    """C4 at full size (d = 2, n = m = 16M, eps = 0.002, lam = 2; NFFT on the cell-group
+    kernels) for 3 iterations: the last gamma-step identity (3.4) checked by the oracle at
+    24 sampled j with the returned beta."""
+    pr = W.c4_uot(iters=3)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": "nfft"})
+    b = beta.cpu().numpy()
+    g = gamma.cpu().numpy()
+    lam = 1.0 / pr.eps
+    c2 = pr.lam / (1.0 + pr.lam * lam)
+    idx = np.random.default_rng(4).choice(len(pr.y), 24, replace=False)
+    tt = oracle.kernel_sum_direct(pr.x, pr.a * np.exp(lam * b), pr.y[idx], W.GAUSS, pr.eps)
+    ref = -c2 * np.log(tt)
+    assert np.max(np.abs(g[idx] - ref)) <= 1e-9 * np.max(np.abs(ref))
+    assert abs(res.mass_a - pr.a.sum()) <= 1e-12 * pr.a.sum()
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_kernel_sum_c5_dense_sampled(uk, d):
+    """C5 in d = 1, 2 at n = m = 1e6 (signed N(0,1) weights; cell-group kernels), checked
+    on 64 sampled targets by the oracle."""
+    pr = W.c5_sum(d, 1_000_000, kind=W.GAUSS)
+    got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"})
+    idx = np.random.default_rng(5).choice(len(pr.tgt), 64, replace=False)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt[idx], pr.kind, pr.param)
+    g = got.cpu().numpy()[idx]
+    assert np.max(np.abs(g - ref)) / np.max(np.abs(ref)) <= 1e-9
