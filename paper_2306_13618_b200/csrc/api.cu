@@ -102,10 +102,14 @@ struct NfftSetup {
 
 void setup_nfft(NfftSetup& ns, int d, int kind, double param, const double* p1, int64_t n1, const double* p2,
                 int64_t n2, const uotk_opts& o, void* comm, cudaStream_t s) {
+    trace_mark("setup_nfft: start");
     Geometry g = compute_geometry(d, p1, n1, p2, n2, s, comm);
+    trace_mark("geometry");
     ns.fp = choose_params(d, kind, param, g, o);
+    trace_mark("choose_params");
     ns.sp.fp = ns.fp;
     build_spectral_plan(ns.sp, s);
+    trace_mark("spectral_plan");
 }
 
 size_t grid_elems(const FastParams& fp) {
@@ -157,7 +161,9 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         fill_info(info, method, &ns.fp);
         PointSet PS, PT;
         make_pointset(PS, S.d, n_src, ns.fp, s);
+        trace_mark("pointset src");
         make_pointset(PT, T.d, n_tgt, ns.fp, s);
+        trace_mark("pointset tgt");
         DevBuf<double> w(n_src, s), grid(grid_elems(ns.fp), s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
         permute_values(w.p, A.d, PS.perm.p, n_src, s);
@@ -165,6 +171,7 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         spread(PS, w.p, grid.p, ns.fp, s);
         fft_chain(ns.sp, grid.p, spec.p, s, comm);
         gather_epi(PT, grid.p, ns.fp, EpiStore{O.d, PT.perm.p}, nullptr, s);
+        trace_mark("passes enqueued");
     }
     O.flush();
     if (O.host) UOTK_CUDA(cudaStreamSynchronize(s));

@@ -90,7 +90,7 @@ bool chunked_available(const FastParams& fp) { return fp.m == kChunkM && fp.d >=
 
 // Build the chunk list and the per-chunk window blocks (once per point set).  Chunks pad
 // runs to multiples of 32 slots; when the padding would waste too much work (sparse
-// clouds: d = 3 below 1/4 fill, d = 2 below 1/16) or the window blocks would not fit
+// clouds: d = 3 below ~3 points per chunk, d = 2 below 2) or the window blocks would not fit
 // comfortably in free device memory, the point set stays on the generic kernels
 // (ps.chunked = false).
 void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
@@ -110,6 +110,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     int32_t nruns = 0;
     UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     UOTK_CUDA(cudaStreamSynchronize(s));
+    trace_mark("chunks: rle + sync");
     t3 = tmp_bytes;
     UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, run_len.p, run_start.p, nruns, s));
     chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
@@ -121,12 +122,17 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     UOTK_CUDA(cudaMemcpyAsync(&last[1], nchunk.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     UOTK_CUDA(cudaStreamSynchronize(s));
     const int64_t nchunks = (int64_t)last[0] + last[1];
-    const double min_fill = d == 3 ? 0.25 : (d == 2 ? 1.0 / 16 : 0.0);
+    trace_mark("chunks: count + sync");
+    // minimum mean fill of the 32-slot chunks: below it the padded GEMM work and the
+    // per-group footprint flush cost more than the generic kernels' per-tap atomics
+    // (d = 3: ~3 points per chunk, measured on C5/C2 clouds; d = 2: ~2; d = 1: any)
+    const double min_fill = d == 3 ? 0.09 : (d == 2 ? 1.0 / 16 : 0.0);
     const bool forced = fp.flags & UOTK_FLAG_CHUNKED;
     if (!forced && (double)n < min_fill * kChunk * (double)nchunks) return;  // too sparse for the chunked kernels
     const size_t win_bytes = (size_t)nchunks * chunk_win_doubles(d) * sizeof(double);
     size_t free_b = 0, total_b = 0;
     UOTK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    trace_mark("chunks: memgetinfo");
     if (win_bytes > free_b / 2) {  // keep the generic path rather than exhaust HBM
         if (forced) fail(UOTK_ENOMEM, "UOTK_FLAG_CHUNKED: window blocks do not fit in device memory");
         return;
@@ -163,6 +169,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     ps.chunk_bounds.alloc(nb + 1, s);
     chunk_bounds_k<<<blocks_for(nb + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nb, ps.chunk_bounds.p);
     UOTK_LAUNCHED();
+    trace_mark("chunks: windows + bounds");
     ps.chunk_blocks = nb;
     ps.nchunks = nchunks;
     ps.chunked = true;

@@ -20,7 +20,7 @@ constexpr int kStride3 = 20;            // d = 3 padded row stride (doubles)
 // work units of the kernels: d = 3 one CTA (8 warps) per unit, kCtas3 CTAs per SM;
 // d <= 2 one warp per unit, kWarpsD warps per CTA, kCtasD CTAs per SM
 constexpr int kCtas3 = 2;
-constexpr int kWarps2 = 4, kCtas2 = 3;
+constexpr int kWarps2 = 3, kCtas2 = 3;
 constexpr int kWarps1 = 8, kCtas1 = 2;
 __host__ __device__ constexpr int chunk_units_per_sm(int d) {
     return d == 3 ? kCtas3 : (d == 2 ? kWarps2 * kCtas2 : kWarps1 * kCtas1);

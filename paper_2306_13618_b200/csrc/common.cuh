@@ -30,6 +30,10 @@ void check_cufft(cufftResult r, const char* what, const char* file, int line);
 void note_launch(const char* file, int line);  // counts launches + checks launch errors
 void add_launches(int k);                      // launches made by library code we call (CUB)
 
+// host-side phase timing for diagnosis: with UOTK_TRACE=1 in the environment every
+// trace_mark prints the host microseconds since the previous mark to stderr
+void trace_mark(const char* what);
+
 // ------------------------------------------------------------------ device buffers
 // Stream-ordered device allocation (cudaMallocAsync on the call's stream; the
 // device's default pool keeps memory cached between calls).

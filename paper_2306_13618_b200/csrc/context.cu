@@ -1,4 +1,6 @@
 // Library context: errors, stream-ordered buffers, host/device staging, cuFFT plan cache.
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -32,6 +34,19 @@ void note_launch(const char* file, int line) {
 }
 
 void add_launches(int k) { g_launches += k; }
+
+void trace_mark(const char* what) {
+    static const bool on = [] {
+        const char* e = getenv("UOTK_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!on) return;
+    static thread_local auto last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[uotk] %-28s %9.1f us\n", what,
+            std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+}
 
 template <typename T>
 void DevBuf<T>::alloc(size_t count, cudaStream_t stream) {

@@ -97,9 +97,17 @@ void direct_sum_epi(int d, int64_t n_src, const double* src, const double* w, in
                     int kind, double param, const Epi& epi, unsigned long long* dmax, cudaStream_t s) {
     if (n_tgt == 0) return;
     const int64_t tb = (n_tgt + kDT - 1) / kDT;
-    // split the sources so that the grid has >= ~4 blocks per SM, slices >= 4 tiles
-    int64_t nsplit = 1;
-    while (tb * nsplit < 592 && n_src / (nsplit * 2) >= 4 * kTile) nsplit *= 2;
+    // split the sources over blockIdx.y until the grid has ~8 blocks per SM, keeping
+    // slices of >= 64 sources (small problems, e.g. C1's 1000 x 1000, are latency-bound:
+    // a long per-thread loop over all sources would leave the GPU idle)
+    int sms = 148;
+    {
+        int dev = 0;
+        UOTK_CUDA(cudaGetDevice(&dev));
+        UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t want = (8LL * sms + tb - 1) / tb;
+    int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(want, n_src / 64));
     if (nsplit > 65535) nsplit = 65535;
     const int64_t slice = n_src == 0 ? 1 : (n_src + nsplit - 1) / nsplit;
     const double arg = kind == UOTK_GAUSS ? 1.0 / param : param * param;

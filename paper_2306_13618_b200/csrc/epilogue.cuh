@@ -13,6 +13,14 @@ struct EpiStore {
         return 0.0;
     }
     __device__ __forceinline__ void prefetch(int64_t) const {}
+    // software-pipelined form used by the chunked kernels: load() the per-point inputs a
+    // chunk ahead, apply() them; apply returns the sup-norm change and the next weight
+    struct In {};
+    __device__ __forceinline__ In load(int64_t) const { return {}; }
+    __device__ __forceinline__ double apply(int64_t i, double t, const In&, double& w) const {
+        w = 0.0;
+        return (*this)(i, t);
+    }
 };
 
 // One Sinkhorn half-step, (3.3) / (3.4) in scaling form:
@@ -45,6 +53,24 @@ struct EpiSinkhorn {
         asm volatile("prefetch.global.L1 [%0];" ::"l"(mass + i));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pot + i));
     }
+    struct In {
+        double pot, mass;
+    };
+    __device__ __forceinline__ In load(int64_t i) const { return {pot[i], mass[i]}; }
+    // operator() with the inputs preloaded; also returns the next weight w (no re-read)
+    __device__ __forceinline__ double apply(int64_t i, double t, const In& in, double& w) const {
+        if (!(t > 0.0) || !isfinite(t)) {
+            atomicOr(flag, 1);
+            t = 1.0;
+        }
+        const double pnew = -c * log(t);
+        pot[i] = pnew;
+        w = in.mass * exp(lam * pnew);
+        if (!isfinite(w)) atomicOr(flag, 2);
+        w_next[i] = w;
+        if (t_store) t_store[i] = t;
+        return fabs(pnew - in.pot);
+    }
     // the same next weight without side effects (bit-identical to operator()'s w_next)
     __device__ __forceinline__ double weight(int64_t i, double t) const {
         if (!(t > 0.0) || !isfinite(t)) t = 1.0;
@@ -62,6 +88,15 @@ struct EpiDot {
         return 0.0;
     }
     __device__ __forceinline__ void prefetch(int64_t) const {}
+    struct In {
+        double w;
+    };
+    __device__ __forceinline__ In load(int64_t i) const { return {w[i]}; }
+    __device__ __forceinline__ double apply(int64_t i, double t, const In& in, double& wn) const {
+        wn = 0.0;
+        prod[i] = in.w * t;
+        return 0.0;
+    }
 };
 
 // Chunked-kernel adaptors: the Sinkhorn epilogue exposes w_next / weight(); the plain
@@ -71,6 +106,12 @@ struct EpiNone {
     __device__ double operator()(int64_t, double) const { return 0.0; }
     __device__ double weight(int64_t, double) const { return 0.0; }
     __device__ void prefetch(int64_t) const {}
+    struct In {};
+    __device__ In load(int64_t) const { return {}; }
+    __device__ double apply(int64_t, double, const In&, double& w) const {
+        w = 0.0;
+        return 0.0;
+    }
 };
 template <class Epi>
 struct EpiGatherOnly : Epi {

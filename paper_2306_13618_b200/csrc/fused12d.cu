@@ -44,12 +44,48 @@ constexpr int kM = kChunkM;
 constexpr int kW2 = chunk_win_doubles(2);  // 1024 doubles = 8 KB per chunk
 constexpr uint32_t kW2Bytes = kW2 * sizeof(double);
 constexpr int kW1 = chunk_win_doubles(1);  // 512 doubles per chunk
-constexpr int kRing2 = 2;
+constexpr int kRing2 = 3;  // window blocks in flight per warp
 
 struct __align__(128) Smem2 {
     double win[kWarps2][kRing2][kW2];  // per-warp TMA ring of window blocks
     double red[kWarps2][kChunk];       // per-warp gathered t of the current chunk
     unsigned long long bar[kWarps2][kRing2];
+};
+
+// chunk descriptors of a warp's range, batched: lane L holds the descriptor of chunk
+// base + L of the current batch (cur) and of the next batch (nxt, in flight)
+struct DescBatch {
+    int4 cur, nxt;
+    const int4* desc;
+    int64_t cbeg, cend;
+    __device__ __forceinline__ int4 fetch(int64_t c) const {
+        return c < cend ? desc[c] : make_int4(0, 0, -1, 0);
+    }
+    __device__ __forceinline__ void init(const int4* d, int64_t b, int64_t e, int lane) {
+        desc = d;
+        cbeg = b;
+        cend = e;
+        cur = fetch(b + lane);
+        nxt = fetch(b + 32 + lane);
+    }
+    // descriptor of chunk cbeg + k (warp-uniform k); advances the batches at k % 32 == 0
+    __device__ __forceinline__ int4 get(int64_t k, int lane) {
+        if (k > 0 && (k & 31) == 0) {
+            cur = nxt;
+            nxt = fetch(cbeg + k + 32 + lane);
+        }
+        const int src = (int)(k & 31);
+        return make_int4(__shfl_sync(0xffffffffu, cur.x, src), __shfl_sync(0xffffffffu, cur.y, src),
+                         __shfl_sync(0xffffffffu, cur.z, src), 0);
+    }
+    // descriptor of chunk cbeg + k + 1 without advancing
+    __device__ __forceinline__ int4 peek_next(int64_t k) const {
+        const int src = (int)((k + 1) & 31);
+        const bool in_nxt = ((k + 1) & 31) == 0;
+        const int4 v = in_nxt ? nxt : cur;
+        return make_int4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                         __shfl_sync(0xffffffffu, v.z, src), 0);
+    }
 };
 
 // MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
@@ -60,6 +96,7 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             const double* __restrict__ w_in, Epi epi, unsigned long long* dmax) {
     constexpr bool GATHER = MODE != 1;
     constexpr bool SPREAD = MODE != 2;
+    using In = typename Epi::In;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem2& sm = *reinterpret_cast<Smem2*>(smem_raw);
     const int lane = threadIdx.x & 31;
@@ -74,8 +111,7 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     double* swin = &sm.win[warp][0][0];
     unsigned long long* bar = sm.bar[warp];
     if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int r = 0; r < kRing2; ++r) mbar_init(&bar[r], 1);
         mbar_init_fence();
     }
     __syncwarp();
@@ -85,12 +121,15 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             bulk_g2s(swin + k * kW2, win + (cbeg + k) * kW2, kW2Bytes, &bar[k]);
         }
     }
+    DescBatch db;
+    db.init(desc, cbeg, cbeg + nck, lane);
 
     double Fb[2][4];     // Fb[nt][ks] = F[4ks + tq][8nt + gq]          (gather B operand)
     double S[2][2][2];   // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]  (spread accumulators)
     int32_t cur_key = -1;
     int64_t org = 0;  // grid index of footprint (0, 0) of the current group
     double ddmax = 0.0;
+    auto origin = [&](int32_t kk) -> int64_t { return (int64_t)(kk / ng - kM + 1) * ng + (kk % ng - kM + 1); };
     auto flush = [&]() {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
@@ -103,16 +142,28 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         }
     };
 
+    int4 dsc = db.get(0, lane);
+    In in_cur{};
+    double w_cur = 0.0;  // spread-only: source weight of slot `lane`
+    if (GATHER && lane < dsc.y) in_cur = epi.load(dsc.x + lane);
+    if (!GATHER && lane < dsc.y) w_cur = w_in[dsc.x + lane];
     for (int64_t k = 0; k < nck; ++k) {
         const int64_t c = cbeg + k;
-        const int buf = (int)(k & 1);
-        const int4 dsc = desc[c];  // {first point, count, key, 0}
+        const int slot = (int)(k % kRing2);
         const int64_t p0 = dsc.x;
         const int cnt = dsc.y;
+        // next chunk's descriptor and per-point inputs, in flight during this chunk
+        const int4 dnext = db.peek_next(k);
+        In in_next{};
+        double w_nxt = 0.0;
+        if (k + 1 < nck && lane < dnext.y) {
+            if (GATHER) in_next = epi.load(dnext.x + lane);
+            else w_nxt = w_in[dnext.x + lane];
+        }
         if (dsc.z != cur_key) {
             if (SPREAD && cur_key >= 0) flush();
             cur_key = dsc.z;
-            org = (int64_t)(cur_key / ng - kM + 1) * ng + (cur_key % ng - kM + 1);
+            org = origin(cur_key);
             if (GATHER) {
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
@@ -128,9 +179,12 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
         }
-        if (GATHER && lane < cnt) epi.prefetch(p0 + lane);
-        mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
-        const double* X = swin + buf * kW2;
+        if (GATHER && k + 1 < nck && dnext.z != cur_key && lane < 16) {
+            // warm L1 with the next group's footprint rows
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(grid_in + origin(dnext.z) + (int64_t)lane * ng));
+        }
+        mbar_wait(&bar[slot], (uint32_t)((k / kRing2) & 1));
+        const double* X = swin + slot * kW2;
         const double* Y = X + kChunk * kChunkT;
 
         double wn = 0.0;  // spread weight of slot `lane`
@@ -161,12 +215,9 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             }
             __syncwarp();
             const double t = sm.red[warp][lane];
-            if (lane < cnt) {
-                ddmax = fmax(ddmax, epi(p0 + lane, t));
-                if (SPREAD) wn = epi.w_next[p0 + lane];
-            }
+            if (lane < cnt) ddmax = fmax(ddmax, epi.apply(p0 + lane, t, in_cur, wn));
         } else {
-            wn = lane < cnt ? w_in[p0 + lane] : 0.0;
+            wn = w_cur;
         }
 
         if (SPREAD) {
@@ -186,12 +237,15 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 dmma(S[1][1][0], S[1][1][1], xa1, yb1);
             }
         }
-        __syncwarp();  // the warp is done with window slot `buf` and red
+        __syncwarp();  // the warp is done with window slot `slot` and red
         if (lane == 0 && k + kRing2 < nck) {
             fence_proxy_async();
-            mbar_expect_tx(&bar[buf], kW2Bytes);
-            bulk_g2s(swin + buf * kW2, win + (c + kRing2) * kW2, kW2Bytes, &bar[buf]);
+            mbar_expect_tx(&bar[slot], kW2Bytes);
+            bulk_g2s(swin + slot * kW2, win + (c + kRing2) * kW2, kW2Bytes, &bar[slot]);
         }
+        if (k + 1 < nck) dsc = db.get(k + 1, lane);
+        in_cur = in_next;
+        w_cur = w_nxt;
     }
     if (SPREAD && cur_key >= 0) flush();
     if (GATHER) warp_max_atomic(dmax, ddmax);

@@ -193,6 +193,7 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
     double h[2 * kMaxD + 2];
     UOTK_CUDA(cudaMemcpyAsync(h, fin.p, (2 * d + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
     UOTK_CUDA(cudaStreamSynchronize(s));
+    trace_mark("geometry: reductions + sync");
     if (h[2 * d] != 0) fail(UOTK_EDOMAIN, "non-finite point coordinate");
     if (n1 + n2 == 0) return g;
     for (int t = 0; t < d; ++t) g.center[t] = 0.5 * (h[t] + h[d + t]);
@@ -228,6 +229,7 @@ void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams&
     UOTK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key0.p, ps.key.p, idx0.p, ps.perm.p, (int)n, 0,
                                               end_bit, s));
     add_launches(1 + (end_bit + 7) / 8);  // CUB onesweep: histogram + one pass per 8 key bits
+    trace_mark("pointset: sort");
     if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
     else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
     else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);

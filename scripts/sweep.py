@@ -28,19 +28,37 @@ def cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
+def spin_up(seconds=0.3):
+    """Keep the GPU busy briefly so that the SM clock has left its idle state (the
+    library's host synchronisations between short calls otherwise let it drop)."""
+    a = torch.randn(2048, 2048, device="cuda")
+    t0 = time.time()
+    while time.time() - t0 < seconds:
+        a = (a @ a).clamp_(-1, 1)
+    torch.cuda.synchronize()
+
+
 def timed(fn, reps=3):
+    """Median device time per call over `reps` calls (each bracketed by CUDA events), the
+    library's per-tag kernel times and launch count averaged over the same calls."""
     fn()
+    spin_up()
     torch.cuda.synchronize()
     uk.profile_enable(True)
     uk.profile_reset()
     uk.reset_launch_counter()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
+    times, walls = [], []
     for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        s.record()
         out = fn()
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / reps
+        e.record()
+        torch.cuda.synchronize()
+        walls.append((time.perf_counter() - w0) * 1e3)
+        times.append(s.elapsed_time(e))
+    timed.wall_ms = float(np.median(walls))
+    ms = float(np.median(times))
     prof = {k: round(v[0] / reps, 4) for k, v in uk.profile_read().items() if v[1]}
     launches = uk.launch_counter() / reps
     uk.profile_enable(False)
@@ -48,6 +66,7 @@ def timed(fn, reps=3):
 
 
 def emit(**kw):
+    kw["wall_ms"] = round(getattr(timed, "wall_ms", 0.0), 3)
     print(json.dumps(kw), flush=True)
 
 
@@ -83,10 +102,10 @@ def case_c4(iters):
          iters_per_s=1e3 / per_it, prof=prof, launches=nl, info=out[2].info, gen_s=gen)
 
 
-def case_c5(max_n):
-    for d in (1, 2, 3):
+def case_c5(max_n, dims=(1, 2, 3), min_n=10_000):
+    for d in dims:
         for kind in (W.GAUSS, W.IMQ):
-            n = 10_000
+            n = min_n
             while n <= max_n:
                 pr = W.c5_sum(d, n, kind=kind)
                 s, al, t = cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt)
@@ -107,6 +126,8 @@ def main():
     p.add_argument("--cases", default="c1,c2,c4,c5")
     p.add_argument("--c5-max", type=float, default=1e7)
     p.add_argument("--c4-iters", type=int, default=5)
+    p.add_argument("--c5-dims", default="1,2,3")
+    p.add_argument("--c5-min", type=float, default=1e4)
     a = p.parse_args()
     cases = a.cases.split(",")
     if "c1" in cases:
@@ -114,7 +135,7 @@ def main():
     if "c2" in cases:
         case_c2()
     if "c5" in cases:
-        case_c5(int(a.c5_max))
+        case_c5(int(a.c5_max), tuple(int(x) for x in a.c5_dims.split(",")), int(a.c5_min))
     if "c4" in cases:
         case_c4(a.c4_iters)
 
