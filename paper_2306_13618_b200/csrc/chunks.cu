@@ -32,12 +32,12 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
         desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r], 0);
 }
 
-// window block of every chunk (layout per d: chunks.cuh)
+// window block of every chunk (layout per d: chunks.cuh), d <= 2
 template <int D>
 __global__ void chunk_window_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
                                KBWindow w, double* __restrict__ out) {
     constexpr int kW = chunk_win_doubles(D);
-    constexpr int kRow = D == 3 ? kStride3 : kChunkT;
+    constexpr int kRow = kChunkT;
     const int64_t c = blockIdx.x;
     const int4 dsc = desc[c];
     double* o = out + c * kW;
@@ -49,11 +49,54 @@ __global__ void chunk_window_k(const int4* __restrict__ desc, const double* __re
         // tap stored at this column
         const int a = D == 2 ? ((col - 4 * p) & 15) : col;
         double val = 0.0;
-        if (p < dsc.y && a < kChunkT) {
+        if (p < dsc.y) {
             const double ut = u[ax * n + dsc.x + p];
             val = kb_phi(ut - floor(ut) + (double)(kChunkM - 1 - a), w);
         }
         o[e] = val;
+    }
+}
+
+// d = 3: X and Y rows of 16 taps (stride 20); Z rows of KZ columns (stride ZS) holding the
+// 16 z-taps at the point's cell offset within the group's z-segment (0 for KZ = 16)
+template <int KZ>
+__global__ void chunk_window3_k(const int4* __restrict__ desc, const double* __restrict__ u,
+                                const int32_t* __restrict__ key, int64_t n, KBWindow w, double* __restrict__ out) {
+    constexpr int ZS = chunk_zstride3(KZ);
+    constexpr int kW = chunk_win3_doubles(KZ);
+    constexpr int kXY = 2 * kChunk * kStride3;
+    const int64_t c = blockIdx.x;
+    const int4 dsc = desc[c];
+    double* o = out + c * kW;
+    for (int e = threadIdx.x; e < kW; e += blockDim.x) {
+        int ax, p, a;
+        if (e < kXY) {
+            ax = e / (kChunk * kStride3);
+            const int r = e - ax * kChunk * kStride3;
+            p = r / kStride3;
+            a = r - p * kStride3;
+        } else {
+            ax = 2;
+            const int r = e - kXY;
+            p = r / ZS;
+            a = r - p * ZS;  // column of the placed row
+            if (KZ != 16 && p < dsc.y) a -= key[dsc.x + p] - dsc.z;  // minus the cell's z offset
+        }
+        double val = 0.0;
+        if (p < dsc.y && a >= 0 && a < kChunkT) {
+            const double ut = u[ax * n + dsc.x + p];
+            val = kb_phi(ut - floor(ut) + (double)(kChunkM - 1 - a), w);
+        }
+        o[e] = val;
+    }
+}
+
+// group key of a z-segment: the cell key with its z index rounded down to a multiple of kSegZ
+__global__ void segment_key_k(const int32_t* __restrict__ key, int64_t n, int ng, int32_t* __restrict__ gk) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        const int32_t k = key[i];
+        gk[i] = k - (k % ng) % kSegZ;
     }
 }
 
@@ -100,36 +143,62 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     const int d = fp.d;
     const int n = (int)ps.n;
     DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(2, s);
-    size_t tmp_bytes = 0, t2 = 0, t3 = 0;
+    size_t tmp_bytes = 0, t2 = 0;
     UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
     UOTK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_len.p, run_start.p, n, s));
     tmp_bytes = std::max(tmp_bytes, t2);
     DevBuf<uint8_t> tmp(tmp_bytes, s);
-    UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
-    add_launches(2);
     int32_t nruns = 0;
-    UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    UOTK_CUDA(cudaStreamSynchronize(s));
-    trace_mark("chunks: rle + sync");
-    t3 = tmp_bytes;
-    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, run_len.p, run_start.p, nruns, s));
-    chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
-    UOTK_LAUNCHED();
-    UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t3, nchunk.p, chunk_off.p, nruns, s));
-    add_launches(2);
-    int32_t last[2];
-    UOTK_CUDA(cudaMemcpyAsync(&last[0], chunk_off.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    UOTK_CUDA(cudaMemcpyAsync(&last[1], nchunk.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    UOTK_CUDA(cudaStreamSynchronize(s));
-    const int64_t nchunks = (int64_t)last[0] + last[1];
-    trace_mark("chunks: count + sync");
-    // minimum mean fill of the 32-slot chunks: below it the padded GEMM work and the
-    // per-group footprint flush cost more than the generic kernels' per-tap atomics
-    // (d = 3: ~3 points per chunk, measured on C5/C2 clouds; d = 2: ~2; d = 1: any)
-    const double min_fill = d == 3 ? 0.09 : (d == 2 ? 1.0 / 16 : 0.0);
+    // runs of equal group keys -> chunks of <= 32 points; returns the number of chunks
+    auto encode = [&](const int32_t* keys) -> int64_t {
+        size_t t = tmp_bytes;
+        UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, t, keys, run_key.p, run_len.p, cnt.p, n, s));
+        add_launches(2);
+        UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        UOTK_CUDA(cudaStreamSynchronize(s));
+        t = tmp_bytes;
+        UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, run_len.p, run_start.p, nruns, s));
+        chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
+        UOTK_LAUNCHED();
+        t = tmp_bytes;
+        UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, nchunk.p, chunk_off.p, nruns, s));
+        add_launches(2);
+        int32_t last[2];
+        UOTK_CUDA(cudaMemcpyAsync(&last[0], chunk_off.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        UOTK_CUDA(cudaMemcpyAsync(&last[1], nchunk.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        UOTK_CUDA(cudaStreamSynchronize(s));
+        return (int64_t)last[0] + last[1];
+    };
+    int64_t nchunks = encode(ps.key.p);
+    trace_mark("chunks: encode");
     const bool forced = fp.flags & UOTK_FLAG_CHUNKED;
-    if (!forced && (double)n < min_fill * kChunk * (double)nchunks) return;  // too sparse for the chunked kernels
-    const size_t win_bytes = (size_t)nchunks * chunk_win_doubles(d) * sizeof(double);
+    // d = 3 sparse clouds: group z-segments of kSegZ cells when that needs sufficiently
+    // fewer chunks (each costs 1.5x a one-cell chunk: 24 instead of 16 z-columns)
+    int kz = 16;
+    double chunk_cost = 1.0;
+    DevBuf<int32_t> gk;
+    if (d == 3 && (double)n < 0.5 * kChunk * (double)nchunks) {
+        gk.alloc(n, s);
+        segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, gk.p);
+        UOTK_LAUNCHED();
+        const int64_t nseg = encode(gk.p);
+        if (1.5 * (double)nseg < (double)nchunks) {
+            kz = 24;
+            chunk_cost = 1.5;
+            nchunks = nseg;
+        } else {
+            nchunks = encode(ps.key.p);  // back to one-cell groups
+        }
+        trace_mark("chunks: z-segments");
+    }
+    // minimum mean fill of the 32-slot chunks (per unit of chunk cost): below it the padded
+    // GEMM work and the per-group footprint flush cost more than the generic kernels'
+    // per-tap atomics (d = 3: ~3 points per chunk, measured on C5/C2 clouds; d = 2: ~2;
+    // d = 1: any)
+    const double min_fill = d == 3 ? 0.09 : (d == 2 ? 1.0 / 16 : 0.0);
+    if (!forced && (double)n < min_fill * chunk_cost * kChunk * (double)nchunks) return;
+    const int wd = d == 3 ? chunk_win3_doubles(kz) : chunk_win_doubles(d);
+    const size_t win_bytes = (size_t)nchunks * wd * sizeof(double);
     size_t free_b = 0, total_b = 0;
     UOTK_CUDA(cudaMemGetInfo(&free_b, &total_b));
     trace_mark("chunks: memgetinfo");
@@ -138,14 +207,19 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
         return;
     }
     ps.chunk_desc.alloc(nchunks, s);
-    ps.chunk_win.alloc((size_t)nchunks * chunk_win_doubles(d), s);
+    ps.chunk_win.alloc((size_t)nchunks * wd, s);
     chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
                                                         ps.chunk_desc.p);
     UOTK_LAUNCHED();
     const KBWindow win = make_window(fp.b, kChunkM);
     {
         ProfScope prof(kProfSetup, s);
-        if (d == 3) chunk_window_k<3><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
+        if (d == 3 && kz == 24)
+            chunk_window3_k<24><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, win,
+                                                                   ps.chunk_win.p);
+        else if (d == 3)
+            chunk_window3_k<16><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, win,
+                                                                   ps.chunk_win.p);
         else if (d == 2) chunk_window_k<2><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
         else chunk_window_k<1><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
         UOTK_LAUNCHED();
@@ -171,6 +245,8 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     UOTK_LAUNCHED();
     trace_mark("chunks: windows + bounds");
     ps.chunk_blocks = nb;
+    ps.chunk_kz = kz;
+    ps.chunk_fill = (double)n / ((double)kChunk * (double)nchunks);
     ps.nchunks = nchunks;
     ps.chunked = true;
 }

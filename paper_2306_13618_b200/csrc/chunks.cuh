@@ -5,7 +5,8 @@
 // window footprint.  Runs are cut into chunks of <= 32 points and the window values of
 // every chunk are precomputed once per point set (points do not move between Sinkhorn
 // iterations) into a fixed-size block per chunk, zero for empty slots:
-//   d = 3: [axis 3][slot 32][tap, row stride 20]      (padded: conflict-free fragments)
+//   d = 3: [axis 3][slot 32][tap, row stride 20]      (padded: conflict-free fragments);
+//          z-segment groups: X, Y as above, Z [slot 32][24 placed taps, row stride 28]
 //   d = 2: [axis 2][slot 32][16 taps, swizzled]       (tap a of slot p at (a + 4p) & 15)
 //   d = 1: [slot 32][16 taps]                          (each lane reads its own row)
 #pragma once
@@ -26,8 +27,15 @@ __host__ __device__ constexpr int chunk_units_per_sm(int d) {
     return d == 3 ? kCtas3 : (d == 2 ? kWarps2 * kCtas2 : kWarps1 * kCtas1);
 }
 
+// d = 3 z-column segments (sparse clouds): a group spans kSegZ cells along z, the
+// footprint is 16 x 16 x KZ with KZ = 24 >= 15 + kSegZ, and each point's 16 z-taps are
+// placed at its cell's offset in a KZ-wide row (stride 28: conflict-free fragments)
+constexpr int kSegZ = 9;
+__host__ __device__ constexpr int chunk_zstride3(int kz) { return kz == 16 ? kStride3 : 28; }
+__host__ __device__ constexpr int chunk_win3_doubles(int kz) { return kChunk * (2 * kStride3 + chunk_zstride3(kz)); }
+
 __host__ __device__ constexpr int chunk_win_doubles(int d) {
-    return d == 3 ? 3 * kChunk * kStride3 : d * kChunk * kChunkT;
+    return d == 3 ? chunk_win3_doubles(16) : d * kChunk * kChunkT;
 }
 
 // d = 2 swizzle: column of tap a in slot row p

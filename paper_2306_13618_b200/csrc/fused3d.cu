@@ -42,21 +42,31 @@ constexpr int kWinDoubles = chunk_win_doubles(3);
 constexpr uint32_t kWinBytes = kWinDoubles * sizeof(double);  // 15 KB
 constexpr int kBlocksPerSM = kCtas3;
 
-struct __align__(128) Smem {
-    double win[2][3][kChunk][kStride];  // double-buffered window blocks (TMA destination)
-    double red[kThreads / 32][kChunk];  // per-warp partial gathers
-    unsigned long long bar[2];          // mbarriers of the two buffers
+// Shared-memory copy of one chunk's window block with a z-row width KZ (chunks.cuh:
+// 16 for one-cell groups, 24 for z-column segments of sparse clouds).
+template <int KZ>
+struct __align__(128) SmemK {
+    double win[2][chunk_win3_doubles(KZ)];  // double-buffered window blocks (TMA destination)
+    double red[kThreads / 32][kChunk];      // per-warp partial gathers
+    unsigned long long bar[2];              // mbarriers of the two buffers
 };
 
-// MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
-template <int MODE, class Epi>
+// MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only.
+// KZ: footprint extent along z (16: the group is one cell; 24: a segment of kSegZ cells
+// along z, each point's z-window placed at its cell's offset in the segment).
+template <int MODE, class Epi, int KZ>
 __global__ void __launch_bounds__(kThreads, kBlocksPerSM)
 chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
             int64_t nchunks, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
             const double* __restrict__ w_in, Epi epi, unsigned long long* dmax) {
     constexpr bool GATHER = MODE != 1;
     constexpr bool SPREAD = MODE != 2;
-    __shared__ Smem sm;
+    constexpr int KS = KZ / 4;  // k-steps of the gather GEMM (contraction over z)
+    constexpr int NZ = KZ / 8;  // n-tiles of the spread GEMM (output columns along z)
+    constexpr int ZS = chunk_zstride3(KZ);
+    constexpr int kWD = chunk_win3_doubles(KZ);
+    constexpr uint32_t kWB = kWD * sizeof(double);
+    __shared__ SmemK<KZ> sm;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -73,20 +83,20 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     if (tid == 0) {
         mbar_init(&sm.bar[0], 1);
         mbar_init(&sm.bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_init_fence();
     }
     __syncthreads();
     if (tid == 0) {
         for (int k = 0; k < 2 && cbeg + k < cend; ++k) {
-            mbar_expect_tx(&sm.bar[k], kWinBytes);
-            bulk_g2s(&sm.win[k][0][0][0], win + (cbeg + k) * kWinDoubles, kWinBytes, &sm.bar[k]);
+            mbar_expect_tx(&sm.bar[k], kWB);
+            bulk_g2s(&sm.win[k][0], win + (cbeg + k) * kWD, kWB, &sm.bar[k]);
         }
     }
 
     // gather B operand: Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
-    double Fb[4][4];
-    // spread accumulators: S[mt][nt2] = {S[a0 + (mt>>1)][8(mt&1) + gq][8nt2 + 2tq + i]}
-    double S[4][2][2];
+    double Fb[4][KS];
+    // spread accumulators: S[mt][nz] = {S[a0 + (mt>>1)][8(mt&1) + gq][8nz + 2tq + i]}
+    double S[4][NZ][2];
     int32_t cur_key = -1;
     int64_t gorg = 0;  // grid index of footprint (0,0,0) for the current group
     double ddmax = 0.0;
@@ -100,10 +110,10 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         for (int mt = 0; mt < 4; ++mt) {
             const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
+            for (int nz = 0; nz < NZ; ++nz)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
-                    if (S[mt][nt][i] != 0.0) atomicAdd(grid_out + row + 8 * nt + 2 * tq + i, S[mt][nt][i]);
+                    if (S[mt][nz][i] != 0.0) atomicAdd(grid_out + row + 8 * nz + 2 * tq + i, S[mt][nz][i]);
         }
     };
 
@@ -111,7 +121,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     for (int64_t c = cbeg; c < cend; ++c) {
         const int k = (int)(c - cbeg);
         const int buf = k & 1;
-        const int4 dsc = dsc_next;  // {first point, count, key, 0}
+        const int4 dsc = dsc_next;  // {first point, count, group key, 0}
         if (c + 1 < cend) dsc_next = desc[c + 1];  // loaded one chunk ahead
         const int64_t p0 = dsc.x;
         const int cnt = dsc.y;
@@ -125,14 +135,14 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             for (int nt = 0; nt < 4; ++nt) {
                 const int64_t row = gorg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks)
+                for (int ks = 0; ks < KS; ++ks)
                     if (GATHER) Fb[nt][ks] = __ldg(grid_in + row + 4 * ks + tq);
             }
             if (SPREAD) {
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
+                    for (int nz = 0; nz < NZ; ++nz) S[mt][nz][0] = S[mt][nz][1] = 0.0;
             }
         }
         if (GATHER) {
@@ -153,9 +163,9 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             }
         }
         mbar_wait(&sm.bar[buf], (k >> 1) & 1);
-        const double(*wx)[kStride] = sm.win[buf][0];
-        const double(*wy)[kStride] = sm.win[buf][1];
-        const double(*wz)[kStride] = sm.win[buf][2];
+        const double(*wx)[kStride] = reinterpret_cast<const double(*)[kStride]>(&sm.win[buf][0]);
+        const double(*wy)[kStride] = wx + kChunk;
+        const double(*wz)[ZS] = reinterpret_cast<const double(*)[ZS]>(&sm.win[buf][2 * kChunk * kStride]);
 
         double wn = 0.0;  // spread weight of slot `lane`
         if (GATHER) {
@@ -166,7 +176,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {
+                for (int ks = 0; ks < KS; ++ks) {
                     const double az = wz[p][4 * ks + tq];  // A[p][c] = Z_p[c]
 #pragma unroll
                     for (int nt = 0; nt < 4; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
@@ -199,7 +209,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 if (warp == 0) {
                     const double dd = epi(p0 + lane, t);
                     ddmax = fmax(ddmax, dd);
-                    if (SPREAD) wn = epi.w_next[p0 + lane];
+                    if (SPREAD) wn = epi.weight(p0 + lane, t);
                 } else if (SPREAD) {
                     wn = epi.weight(p0 + lane, t);
                 }
@@ -213,9 +223,10 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             for (int ks = 0; ks < 8; ++ks) {  // 4 points per k-step
                 const int p = 4 * ks + tq;
                 const double wp = __shfl_sync(0xffffffffu, wn, p);
-                // B[p][c] = w_p Z_p[c] for c = 8 nt2 + gq
-                const double b0 = wp * wz[p][gq];
-                const double b1 = wp * wz[p][8 + gq];
+                // B[p][c] = w_p Z_p[c] for c = 8 nz + gq
+                double bz[NZ];
+#pragma unroll
+                for (int nz = 0; nz < NZ; ++nz) bz[nz] = wp * wz[p][8 * nz + gq];
                 const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
                 const double xv[2] = {xa.x, xa.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
@@ -223,16 +234,16 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 for (int mt = 0; mt < 4; ++mt) {
                     // A[(a,b)][p] = X_p[a] Y_p[b], a = a0 + (mt>>1), b = 8(mt&1) + gq
                     const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
-                    dmma(S[mt][0][0], S[mt][0][1], am, b0);
-                    dmma(S[mt][1][0], S[mt][1][1], am, b1);
+#pragma unroll
+                    for (int nz = 0; nz < NZ; ++nz) dmma(S[mt][nz][0], S[mt][nz][1], am, bz[nz]);
                 }
             }
         }
         __syncthreads();  // every thread is done with win[buf] and red
         if (tid == 0 && c + 2 < cend) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&sm.bar[buf], kWinBytes);
-            bulk_g2s(&sm.win[buf][0][0][0], win + (c + 2) * kWinDoubles, kWinBytes, &sm.bar[buf]);
+            fence_proxy_async();
+            mbar_expect_tx(&sm.bar[buf], kWB);
+            bulk_g2s(&sm.win[buf][0], win + (c + 2) * kWD, kWB, &sm.bar[buf]);
         }
     }
     if (SPREAD && cur_key >= 0) flush();
@@ -461,9 +472,14 @@ void launch(const PointSet& ps, const double* gin, double* gout, const double* w
             const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
     if (ps.n == 0 || ps.nchunks == 0) return;
     ProfScope prof(tag, s);
-    chunked3d_k<MODE, Epi><<<ps.chunk_blocks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p,
-                                                                ps.chunk_bounds.p, ps.nchunks, fp.ng, gin, gout,
-                                                                w, epi, dmax);
+    if (ps.chunk_kz == 24)
+        chunked3d_k<MODE, Epi, 24><<<ps.chunk_blocks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                        ps.chunk_bounds.p, ps.nchunks, fp.ng, gin,
+                                                                        gout, w, epi, dmax);
+    else
+        chunked3d_k<MODE, Epi, 16><<<ps.chunk_blocks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                        ps.chunk_bounds.p, ps.nchunks, fp.ng, gin,
+                                                                        gout, w, epi, dmax);
     UOTK_LAUNCHED();
 }
 
@@ -476,7 +492,7 @@ void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* gr
         const char* e = getenv("UOTK_FUSED_WS");
         return !(e && e[0] == '0');
     }();
-    if (!ws) {
+    if (!ws || ps.chunk_kz != 16) {  // z-segment groups (sparse clouds) use the phase-locked kernel
         launch<0, EpiSinkhorn>(ps, grid_in, grid_out, nullptr, fp, epi, dmax, s, kProfFused);
         return;
     }

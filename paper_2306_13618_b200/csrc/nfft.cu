@@ -199,18 +199,24 @@ void spread(const PointSet& ps, const double* w_sorted, double* grid, const Fast
     UOTK_DISPATCH_DM(fp.d, fp.m, (spread_dm<DD, MM>(ps, w_sorted, grid, fp, s)));
 }
 
+// Stand-alone gathers (kernel sums, marginals) on sparse d = 3 clouds stay on the generic
+// kernel: with few points per chunk its per-point loads beat the padded DMMA GEMMs (the
+// spread still profits from the cell groups: footprint flushes instead of per-tap atomics).
+constexpr double kGatherMinFill3 = 0.3;
+
 template <class Epi>
 void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,
                 unsigned long long* dmax, cudaStream_t s) {
     if (ps.n == 0) return;
+    const bool sparse3 = fp.d == 3 && ps.chunk_fill < kGatherMinFill3 && !(fp.flags & UOTK_FLAG_CHUNKED);
     if constexpr (std::is_same<Epi, EpiStore>::value) {
-        if (chunked_available(fp) && ps.chunked) {
+        if (chunked_available(fp) && ps.chunked && !sparse3) {
             chunked_gather_store(ps, grid, fp, epi, s);
             return;
         }
     }
     if constexpr (std::is_same<Epi, EpiDot>::value) {
-        if (chunked_available(fp) && ps.chunked) {
+        if (chunked_available(fp) && ps.chunked && !sparse3) {
             chunked_gather_dot(ps, grid, fp, epi, s);
             return;
         }
