@@ -47,10 +47,11 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="C3", choices=["C3", "C1"])
+    p.add_argument("--workload", default="C3", choices=["C3", "C1", "C4"])
     p.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-mmd", action="store_true")
+    p.add_argument("--no-c4", action="store_true", help="skip the C4 (d=2, 16M points) side leg")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ncu", action="store_true", help="short run for ncu launch lists (no side legs)")
     return p.parse_args()
@@ -66,6 +67,8 @@ def dist_env():
 def make_problem(name, iters):
     if name == "C3":
         pr = W.c3_uot()
+    elif name == "C4":
+        pr = W.c4_uot()
     else:
         pr = W.c1_uot()
     if iters is not None:
@@ -245,6 +248,8 @@ def main_ours(args):
             out["e2e"] = e2e_leg(uk, pr, x, a, y, b, comm, barrier, world, dev)
         if not args.no_mmd:
             out["mmd2"] = mmd_leg(uk, world, rank, comm, dev, barrier)
+        if not args.no_c4 and args.workload == "C3":
+            out["c4"] = c4_leg(uk, world, rank, comm, dev, barrier)
     if rank == 0:
         line = {
             "metric": "UOT Sinkhorn iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
@@ -312,6 +317,13 @@ def roofline_leg(uk, step, pr, res, world):
             traffic = json.load(f).get(kern)
     except (OSError, ValueError):
         pass
+    if pr.d <= 2:  # d <= 2 cell-group kernels stream precomputed windows: HBM-bound
+        nb = n_local * (pr.d * 2 * res.info["m"] * 8 + 32)
+        gbs = nb / (avg_ms / 1e3) / 1e9
+        return {"bound": "hbm", "kernel": kern, "achieved": gbs, "peak": hbm_peak(), "unit": "GB/s",
+                "frac": gbs / hbm_peak(), "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "avg_launch_ms": avg_ms, "launches_per_step": cnt, "share_of_step": ms / total if total else None,
+                "per_tag_ms": {k: round(v[0], 3) for k, v in prof.items()}}
     return {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src + " (FP64 FMA pipe)",
             "avg_launch_ms": avg_ms, "launches_per_step": cnt, "share_of_step": ms / total if total else None,
@@ -354,8 +366,9 @@ def mmd_leg(uk, world, rank, comm, dev, barrier):
     x, a, y, b = (torch.from_numpy(shard(v, world, rank)).to(dev) for v in (pr.x, pr.a, pr.y, pr.b))
     kind, param = pr.kernels[0]
     opts = {"method": "nfft"}
-    v = uk.mmd2(x, a, y, b, kind, param, opts=opts, comm=comm)
-    steps = 3
+    for _ in range(3):
+        v = uk.mmd2(x, a, y, b, kind, param, opts=opts, comm=comm)
+    steps = 10
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -364,6 +377,69 @@ def mmd_leg(uk, world, rank, comm, dev, barrier):
     dt = time.perf_counter() - t0
     return {"metric": "MMD^2 evals/s", "value": steps / dt, "unit": "evals/s", "mmd2": v,
             "config": "C2 distributions at n=m=1M, d=3, Gaussian exp(-r^2/0.0025), full call incl. setup"}
+
+
+def c4_leg(uk, world, rank, comm, dev, barrier):
+    """C4 (BASELINE.json configs[3]): UOT d=2, n=m=16M uniform in the ball of radius 0.2,
+    eps=0.002, lam=2, 50 iterations — whole solves (setup included), device-timed, inputs
+    resident in HBM; and the d=2 fused half-step kernel against the HBM roofline
+    (algorithmic bytes per point: 2 x 16 window values + mass + potential read, potential
+    and next weight written = 288 B)."""
+    import torch
+    pr = W.c4_uot()
+    x, a, y, b = (torch.from_numpy(shard(v, world, rank)).to(dev) for v in (pr.x, pr.a, pr.y, pr.b))
+    opts = {"method": "nfft"}
+    stream = torch.cuda.current_stream()
+
+    def solve():
+        return uk.uot_sinkhorn(x, a, y, b, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm)
+
+    solve()
+    steps = 2
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        _, _, res = solve()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    uk.profile_reset()
+    uk.profile_enable(True)
+    solve()
+    torch.cuda.synchronize()
+    prof = uk.profile_read()
+    uk.profile_enable(False)
+    uk.profile_reset()
+    fms, fcnt = prof["fused"]
+    roof = None
+    if fcnt:
+        avg = fms / fcnt
+        per_launch_bytes = (len(x) + len(y)) / 2 * 288  # one half-step visits one point set
+        achieved = per_launch_bytes / (avg / 1e3) / 1e9
+        peak = hbm_peak()
+        roof = {"bound": "hbm", "kernel": "chunked2d_k<0> (fused d=2 half-step)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "avg_launch_ms": avg,
+                "launches_per_solve": fcnt, "share_of_solve": fms / sum(v[0] for v in prof.values())}
+    return {"metric": "UOT Sinkhorn iterations/s", "value": pr.iters * steps / (ms / 1e3), "unit": "iterations/s",
+            "ms_per_solve": ms / steps, "config": f"C4: UOT d=2 n=m={len(pr.x)} eps={pr.eps} lam={pr.lam} "
+            f"iters={pr.iters} (whole solves incl. setup, inputs in HBM)",
+            "n_grid": res.info["n_grid"], "N": res.info["N"], "plan_mass": res.plan_mass, "roofline": roof}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6550.7
 
 
 def main():

@@ -36,6 +36,10 @@ KEYS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% of peak)"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
     ("lts__t_bytes.sum", "L2 bytes"),
+    ("dram__bytes.sum.per_second", "DRAM bandwidth achieved"),
+    ("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "DFMA thread instructions"),
+    ("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "DADD thread instructions"),
+    ("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", "DMUL thread instructions"),
 ]
 
 
@@ -73,6 +77,16 @@ def full(rep, pat, out, tag=None):
                     pass
         lines.append("\nwarp stalls per issued instruction: " +
                      ", ".join(f"{n} {v:.2f}" for v, n in sorted(st, reverse=True)[:8]) + "\n")
+        try:
+            fl = sum(float(row[hdr.index(k)].replace(",", "")) * w for k, w in (
+                ("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", 2),
+                ("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", 1),
+                ("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", 1)))
+            dur = float(row[hdr.index("gpu__time_duration.sum")].replace(",", ""))
+            dur *= {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}[units[hdr.index("gpu__time_duration.sum")]]
+            lines.append(f"scalar FP64 (2 DFMA + DADD + DMUL, DMMA excluded): {fl / dur / 1e12:.2f} TFLOP/s\n")
+        except (ValueError, KeyError, IndexError):
+            pass
         rd = to_bytes(row[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_read.sum")])
         wr = to_bytes(row[hdr.index("dram__bytes_write.sum")], units[hdr.index("dram__bytes_write.sum")])
         traffic.append(rd + wr)

@@ -1,0 +1,63 @@
+"""One invocation of each hot kernel family, for ncu captures (profiles/r01/ncu_*.md).
+
+    ncu --set full --clock-control none --import-source on -k regex:'<kernel>' -c 1 \\
+        -o gpurun_out/<name> python scripts/profile_targets.py <target>
+
+targets:
+  sum3d    kernel sum d=3 (C5 recipe, n = m = 4e6, Gaussian l = 0.05): chunked3d_k spread
+           (mode 1) and gather (mode 2), cuFFT D2Z / scale_spectrum_k / Z2D on 140^3
+  c4       two C4 iterations (d = 2, n = m = 16M): chunked2d_k fused half-steps, 160^2 FFTs
+  c3       two C3 iterations (d = 3, n = m = 1M): sinkhorn3d_ws_k, 96^3 FFTs
+  direct   direct kernel sum d = 3, n = m = 2e5 (direct_k, FP64 exp)
+  sum1d    kernel sum d = 1, n = m = 1e7 (chunked1d_k)
+Each target runs its call twice (the first call warms plans and caches); the second runs
+inside the NVTX range "prof" (ncu --nvtx --nvtx-include "prof/").
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2306_13618_b200 as uk  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def main(target):
+    if target == "sum3d":
+        pr = W.c5_sum(3, 4_000_000, kind=W.GAUSS)
+        args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param)
+        call = lambda: uk.kernel_sum(*args, opts={"method": "nfft"})  # noqa: E731
+    elif target == "sum1d":
+        pr = W.c5_sum(1, 10_000_000, kind=W.GAUSS)
+        args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param)
+        call = lambda: uk.kernel_sum(*args, opts={"method": "nfft"})  # noqa: E731
+    elif target == "direct":
+        pr = W.c5_sum(3, 200_000, kind=W.GAUSS)
+        args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param)
+        call = lambda: uk.kernel_sum(*args, opts={"method": "direct"})  # noqa: E731
+    elif target in ("c3", "c4"):
+        pr = W.c3_uot(iters=2) if target == "c3" else W.c4_uot(iters=2)
+        args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
+        call = lambda: uk.uot_sinkhorn(*args, iters=2, opts={"method": "nfft"})  # noqa: E731
+    else:
+        raise SystemExit(f"unknown target {target}")
+    call()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("prof")  # ncu --nvtx --nvtx-include "prof/" captures this call only
+    call()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
+    print(f"{target}: ok")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "sum3d")
