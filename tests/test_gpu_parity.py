@@ -299,15 +299,25 @@ def test_kernel_sum_dense_cloud_auto(uk, d):
     assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9
 
 
-@pytest.mark.parametrize("flags", ["chunked", "generic"])
-def test_uot_c4_like_reduced(uk, flags):
-    """C4's parameters (d = 2, eps = 0.002, lam = 2) at reduced n: the fused d = 2
-    half-step (gather -> update -> spread in one launch) and the generic path."""
+@pytest.fixture(scope="module")
+def c4_reduced():
     pr = W.c4_uot(n=5003, m=4001, iters=12)
     ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    return pr, ref
+
+
+@pytest.mark.parametrize("flags", ["chunked", "generic"])
+@pytest.mark.parametrize("N", [0, 2048])
+def test_uot_c4_like_reduced(uk, c4_reduced, flags, N):
+    """C4's parameters (d = 2, eps = 0.002, lam = 2) at reduced n: the fused d = 2
+    half-step (gather -> update -> spread in one launch) and the generic path, with the
+    automatic bandwidth (N = 80, grid 160^2) and with the literal reading of the config's
+    "oversampled grid 4096^2" (N = 2048; reading R19)."""
+    pr, ref = c4_reduced
     f = uk.FLAG_CHUNKED if flags == "chunked" else uk.FLAG_GENERIC
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
-                                       iters=pr.iters, opts={"method": "nfft", "flags": f})
+                                       iters=pr.iters, opts={"method": "nfft", "flags": f, "N": N})
+    assert res.info["n_grid"] == (4096 if N else 160)
     _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
 
 
