@@ -261,6 +261,7 @@ def main_ours(args):
                                            "h": res.info["h"], "parallelism": f"points sharded x{world}",
                                            "l2": "flushed between steps (256 MB write outside the events)"}),
             "gpu_launches": launches,
+            "step_ms": [round(v, 3) for v in step_ms],
             "clocks": clk.summary(),
             "result": {"primal": res.primal, "dual": res.dual, "plan_mass": res.plan_mass,
                        "max_dbeta": res.max_dbeta, "max_dgamma": res.max_dgamma},

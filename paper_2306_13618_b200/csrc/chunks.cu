@@ -199,9 +199,19 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     if (!forced && (double)n < min_fill * chunk_cost * kChunk * (double)nchunks) return;
     const int wd = d == 3 ? chunk_win3_doubles(kz) : chunk_win_doubles(d);
     const size_t win_bytes = (size_t)nchunks * wd * sizeof(double);
-    size_t free_b = 0, total_b = 0;
-    UOTK_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    trace_mark("chunks: memgetinfo");
+    // cudaMemGetInfo can stall the host for milliseconds: query it only when the blocks
+    // are a noticeable fraction of the device memory (total cached per device)
+    static size_t total_b = 0;
+    if (total_b == 0) {
+        size_t f0 = 0;
+        UOTK_CUDA(cudaMemGetInfo(&f0, &total_b));
+    }
+    size_t free_b = total_b;
+    if (win_bytes > total_b / 16) {
+        size_t t0 = 0;
+        UOTK_CUDA(cudaMemGetInfo(&free_b, &t0));
+        trace_mark("chunks: memgetinfo");
+    }
     if (win_bytes > free_b / 2) {  // keep the generic path rather than exhaust HBM
         if (forced) fail(UOTK_ENOMEM, "UOTK_FLAG_CHUNKED: window blocks do not fit in device memory");
         return;

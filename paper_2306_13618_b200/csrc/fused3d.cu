@@ -384,9 +384,8 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             double wp = 0.0;
             if (lane < cnt) {
                 const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
-                if (gw == 0) {
-                    ddmax = fmax(ddmax, epi(p0 + lane, t));
-                    wp = epi.w_next[p0 + lane];
+                if (gw == 0) {  // one update evaluation returning both the change and the weight
+                    ddmax = fmax(ddmax, epi.apply(p0 + lane, t, epi.load(p0 + lane), wp));
                 } else {
                     wp = epi.weight(p0 + lane, t);
                 }
