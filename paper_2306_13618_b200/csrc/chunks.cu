@@ -199,8 +199,9 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     if (!forced && (double)n < min_fill * chunk_cost * kChunk * (double)nchunks) return;
     const int wd = d == 3 ? chunk_win3_doubles(kz) : chunk_win_doubles(d);
     const size_t win_bytes = (size_t)nchunks * wd * sizeof(double);
-    // cudaMemGetInfo can stall the host for milliseconds: query it only when the blocks
-    // are a noticeable fraction of the device memory (total cached per device)
+    // cudaMemGetInfo can stall the host (milliseconds, and seconds when the stream-ordered
+    // pool caches tens of GB): ask it only for blocks that are a noticeable fraction of the
+    // device and that the pool's cached (reserved but unused) memory cannot hold already
     static size_t total_b = 0;
     if (total_b == 0) {
         size_t f0 = 0;
@@ -208,9 +209,24 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     }
     size_t free_b = total_b;
     if (win_bytes > total_b / 16) {
-        size_t t0 = 0;
-        UOTK_CUDA(cudaMemGetInfo(&free_b, &t0));
-        trace_mark("chunks: memgetinfo");
+        size_t cached = 0;
+        int dev = 0;
+        cudaMemPool_t pool;
+        UOTK_CUDA(cudaGetDevice(&dev));
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long reserved = 0, used = 0;
+            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+                cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+                reserved > used)
+                cached = (size_t)(reserved - used);
+        }
+        cudaGetLastError();
+        if (cached < win_bytes) {
+            size_t t0 = 0;
+            UOTK_CUDA(cudaMemGetInfo(&free_b, &t0));
+            free_b += cached;
+        }
+        trace_mark("chunks: memory check");
     }
     if (win_bytes > free_b / 2) {  // keep the generic path rather than exhaust HBM
         if (forced) fail(UOTK_ENOMEM, "UOTK_FLAG_CHUNKED: window blocks do not fit in device memory");
