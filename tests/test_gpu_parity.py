@@ -393,3 +393,30 @@ def test_mmd2_c2_imq_chunked_vs_generic(uk):
     denom = max(abs(vd), 1e-3 * (abs(xx) + abs(yy)))
     assert abs(v1 - vd) / denom <= 1e-8, (v1, vd)
     assert abs(v2 - vd) / denom <= 1e-8, (v2, vd)
+
+
+@pytest.mark.parametrize("d,kind", [(3, W.GAUSS), (3, W.IMQ), (2, W.IMQ), (1, W.IMQ)])
+def test_kernel_sum_c5_1e7_sampled(uk, d, kind):
+    """C5 at n = m = 1e7 (signed N(0,1) weights): dense d = 3 cell groups (Gauss, 140^3),
+    z-segment groups (IMQ, 384^3), d = 2 / d = 1 cell groups — 32 sampled targets against
+    the oracle."""
+    pr = W.c5_sum(d, 10_000_000, kind=kind)
+    got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), kind, pr.param, opts={"method": "nfft"})
+    idx = np.random.default_rng(6).choice(len(pr.tgt), 32, replace=False)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt[idx], pr.kind, pr.param)
+    g = got.cpu().numpy()[idx]
+    assert np.max(np.abs(g - ref)) / np.max(np.abs(ref)) <= 1e-9
+
+
+def test_kernel_sum_c5_1e8_d3_sampled(uk):
+    """C5's largest size, n = m = 1e8 in d = 3 (Gaussian l = 0.05): 2 x 48 GB of window
+    blocks on the cell-group kernels; 8 sampled targets against the oracle."""
+    pr = W.c5_sum(3, 100_000_000, kind=W.GAUSS)
+    src, alpha, tgt = cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt)
+    got = uk.kernel_sum(src, alpha, tgt, "gauss", pr.param, opts={"method": "nfft"})
+    g_all = got.cpu().numpy()
+    del src, alpha, tgt, got
+    torch.cuda.empty_cache()
+    idx = np.random.default_rng(7).choice(len(pr.tgt), 8, replace=False)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt[idx], pr.kind, pr.param, block_bytes=1 << 31)
+    assert np.max(np.abs(g_all[idx] - ref)) / np.max(np.abs(ref)) <= 1e-9
