@@ -169,8 +169,8 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         permute_values(w.p, A.d, PS.perm.p, n_src, s);
         grid.zero();
         spread(PS, w.p, grid.p, ns.fp, s);
-        fft_chain(ns.sp, grid.p, spec.p, s, comm);
-        gather_epi(PT, grid.p, ns.fp, EpiStore{O.d, PT.perm.p}, nullptr, s);
+        const double* gp = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+        gather_epi(PT, gp, ns.fp, EpiStore{O.d, PT.perm.p}, nullptr, s);
         trace_mark("passes enqueued");
     }
     O.flush();
@@ -274,32 +274,32 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
             if (last) e2.t_store = ty.p;
             if (fused) {
                 // beta-step at x: gather t from g', update, spread mu (.) u into the other grid
-                fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
                 grid2.zero();
-                chunked_gather_spread(PX, grid.p, grid2.p, fp, ex, last ? dmax.p : nullptr, s);
-                fft_chain(ns.sp, grid2.p, spec.p, s, comm);
+                chunked_gather_spread(PX, g1, grid2.p, fp, ex, last ? dmax.p : nullptr, s);
+                const double* g2 = fft_chain(ns.sp, grid2.p, spec.p, s, comm);
                 grid.zero();
-                chunked_gather_spread(PY, grid2.p, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
+                chunked_gather_spread(PY, g2, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
             } else {
-                fft_chain(ns.sp, grid.p, spec.p, s, comm);
-                gather_epi(PX, grid.p, fp, ex, last ? dmax.p : nullptr, s);  // (3.3)
+                const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                gather_epi(PX, g1, fp, ex, last ? dmax.p : nullptr, s);  // (3.3)
                 grid.zero();
                 spread(PX, wx.p, grid.p, fp, s);
-                fft_chain(ns.sp, grid.p, spec.p, s, comm);
-                gather_epi(PY, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
+                const double* g2 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                gather_epi(PY, g2, fp, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
                 grid.zero();
                 spread(PY, wy.p, grid.p, fp, s);
             }
         }
         // grid holds the spread of nu (.) v with the final v: t at x for the marginals
-        fft_chain(ns.sp, grid.p, spec.p, s, comm);
-        gather_epi(PX, grid.p, fp, EpiStore{tx.p, nullptr}, nullptr, s);
+        const double* gx = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+        gather_epi(PX, gx, fp, EpiStore{tx.p, nullptr}, nullptr, s);
         if (iters == 0) {
             scaled_mass(mass_x.p, pot_x.p, n, lam, wx.p, s);
             grid.zero();
             spread(PX, wx.p, grid.p, fp, s);
-            fft_chain(ns.sp, grid.p, spec.p, s, comm);
-            gather_epi(PY, grid.p, fp, EpiStore{ty.p, nullptr}, nullptr, s);
+            const double* gy = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+            gather_epi(PY, gy, fp, EpiStore{ty.p, nullptr}, nullptr, s);
         }
     }
 

@@ -125,6 +125,10 @@ struct SpectralPlan {
     cufftHandle r2c = 0, c2r = 0;  // owned by the context cache
     size_t grid_elems = 0;   // ng^d
     size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
+    // Gaussian kernel: D_k = prod_t d1(k_t) is separable, so F^-1 D F is the tensor power
+    // of one real symmetric circulant n_g x n_g matrix Csep (DESIGN.md §7 "separable")
+    bool separable = false;
+    DevBuf<double> Csep;
 };
 
 // ------------------------------------------------------------------ library context
@@ -148,7 +152,10 @@ void unpermute_values(double* dst, const double* src, const int32_t* perm, int64
 
 // NFFT passes
 void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s);
-void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
+// g' = F^-1 (D .* F g): returns the buffer holding g' (grid itself, or spec's storage
+// reinterpreted as n_g^d doubles on the separable path)
+double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
+void get_cublas(void** handle);  // per-device cuBLAS handle (context.cu)
 void gather(const PointSet& ps, const double* grid, double* out_sorted, const FastParams& fp, cudaStream_t s);
 template <class Epi>
 void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,

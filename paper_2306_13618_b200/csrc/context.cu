@@ -5,6 +5,8 @@
 #include <mutex>
 #include <tuple>
 
+#include <cublas_v2.h>
+
 #include "common.cuh"
 
 namespace uotk {
@@ -126,6 +128,7 @@ struct Context {
     // (device, d, n) -> (r2c, c2r)
     std::map<std::tuple<int, int, int>, std::pair<cufftHandle, cufftHandle>> fft;
     bool pool_configured[64] = {};
+    std::map<int, cublasHandle_t> blas;
 };
 
 Context& ctx() {
@@ -172,6 +175,20 @@ void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r) {
     c.fft[key] = {a, b};
     *r2c = a;
     *c2r = b;
+}
+
+void get_cublas(void** handle) {
+    int dev = 0;
+    UOTK_CUDA(cudaGetDevice(&dev));
+    Context& c = ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.blas.find(dev);
+    if (it == c.blas.end()) {
+        cublasHandle_t h;
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cublasCreate failed");
+        it = c.blas.emplace(dev, h).first;
+    }
+    *handle = it->second;
 }
 
 void ensure_pool() {

@@ -2,6 +2,11 @@
 // (4.6)), the FFT chain with the fused D_k multiplication, and interpolation
 // (forward NFFT, outer sum of (4.6)) — P:590-592.  These are the simple
 // thread-per-point kernels; the tuned cell-group kernels live in fused3d.cu / fused12d.cu.
+#include <cublas_v2.h>
+
+#include <string>
+#include <utility>
+
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "profile.cuh"
@@ -235,8 +240,50 @@ void gather(const PointSet& ps, const double* grid, double* out_sorted, const Fa
     gather_epi(ps, grid, fp, EpiStore{out_sorted, nullptr}, nullptr, s);
 }
 
-void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
+int comm_nranks(void* comm);  // comm.cu
+
+// Separable chain (Gaussian kernel, one rank): one GEMM per axis with the circulant Csep
+// on the FP64 tensor cores (cuBLAS DGEMM).  Row-major grid g[x][y][z]; cuBLAS is
+// column-major, so a row-major R x n block is an n x R column-major matrix.  Csep is
+// symmetric.  Returns the buffer holding the result (grid or tmp).
+static double* separable_chain(SpectralPlan& sp, double* grid, double* tmp, cudaStream_t s) {
     const FastParams& fp = sp.fp;
+    const int n = fp.ng;
+    void* hv = nullptr;
+    get_cublas(&hv);
+    cublasHandle_t h = (cublasHandle_t)hv;
+    if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cublasSetStream failed");
+    const double one = 1.0, zero = 0.0;
+    const double* C = sp.Csep.p;
+    auto ok = [](cublasStatus_t st) {
+        if (st != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cuBLAS DGEMM failed (" + std::to_string((int)st) + ")");
+    };
+    int64_t rows = 1;  // number of length-n lines along the last axis
+    for (int t = 0; t < fp.d - 1; ++t) rows *= n;
+    // last axis: out(:, r) = C in(:, r)
+    ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, (int)rows, n, &one, C, n, grid, n, &zero, tmp, n));
+    add_launches(1);
+    if (fp.d == 1) return tmp;
+    if (fp.d == 3) {
+        // middle axis, per x-slab S (row-major [y][z]): out^T = S^T C
+        ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, tmp, n, (long long)n * n, C, n, 0,
+                                     &zero, grid, n, (long long)n * n, n));
+        add_launches(1);
+        std::swap(grid, tmp);  // result of two passes now in `tmp` (the original grid)
+    }
+    // first axis, row-major G (n x P): out^T = G^T C  (P = n^(d-1))
+    const int64_t P = rows;
+    ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)P, n, n, &one, tmp, (int)P, C, n, &zero, grid, (int)P));
+    add_launches(1);
+    return grid;
+}
+
+double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
+    const FastParams& fp = sp.fp;
+    if (sp.separable && (comm == nullptr || comm_nranks(comm) == 1)) {
+        ProfScope ps_(kProfFft, s);
+        return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s);
+    }
     ProfScope ps_(kProfFft, s);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftSetStream(sp.c2r, s));
@@ -248,6 +295,7 @@ void fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, vo
     UOTK_LAUNCHED();
     if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
     UOTK_CUFFT(cufftExecZ2D(sp.c2r, (cufftDoubleComplex*)spec, grid));
+    return grid;
 }
 
 namespace {

@@ -5,6 +5,7 @@
 //     D_k = w_k b_k / (n_g^{2d} prod_t phihat(k_t)^2),   k in I_N,
 // which turns "spread -> FFT -> *D_k -> inverse FFT -> interpolate" into the
 // factorisation (4.5)-(4.6).  See DESIGN.md "Fast summation".
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -297,6 +298,41 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     else dk_kernel<3><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
     UOTK_LAUNCHED();
     // psi_d / samp / bspec are freed stream-ordered after the kernels that use them
+
+    // 4) Gaussian: the samples exp(-h^2 |j/N|^2 / eps) factor over the axes, hence so do b_k
+    //    and D_k = prod_t d1(k_t), d1(k) = psi(k) w(k) b1(k) / N (the same factors dk_kernel
+    //    multiplies).  The chain F^-1 (D .* F g) is then (Csep x ... x Csep) g with the real
+    //    symmetric circulant Csep[l][l'] = c(l - l'),  c(D) = d1(0) + 2 sum_{k=1}^{N/2} d1(k)
+    //    cos(2 pi k D / n_g)  (k = +-N/2 carry weight 1/2 each, as in the FFT path).
+    sp.separable = false;
+    static const bool sep_env = [] {
+        const char* e = getenv("UOTK_SEPARABLE");
+        return !(e && e[0] == '0');
+    }();
+    if (fp.kind == UOTK_GAUSS && sep_env) {
+        std::vector<long double> d1(N / 2 + 1);
+        const long double h2e = (long double)fp.h * fp.h / fp.param;
+        for (int k = 0; k <= N / 2; ++k) {
+            long double b1 = 0;
+            for (int j = -N / 2; j < N / 2; ++j) {
+                const long double y = (long double)j / N;
+                b1 += expl(-h2e * y * y) * cosl(2.0L * M_PI * k * j / N);
+            }
+            d1[k] = (long double)psi[k] * (k == N / 2 ? 0.5L : 1.0L) * b1 / N;
+        }
+        std::vector<double> cvec(ng), C((size_t)ng * ng);
+        for (int D = 0; D < ng; ++D) {
+            long double c = d1[0];
+            for (int k = 1; k <= N / 2; ++k) c += 2.0L * d1[k] * cosl(2.0L * M_PI * k * D / ng);
+            cvec[D] = (double)c;
+        }
+        for (int l = 0; l < ng; ++l)
+            for (int lp = 0; lp < ng; ++lp) C[(size_t)l * ng + lp] = cvec[((l - lp) % ng + ng) % ng];
+        sp.Csep.alloc(C.size(), s);
+        UOTK_CUDA(cudaMemcpyAsync(sp.Csep.p, C.data(), C.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        UOTK_CUDA(cudaStreamSynchronize(s));  // C lives on the host stack frame
+        sp.separable = true;
+    }
 
     get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
     sp.grid_elems = 1;
