@@ -97,6 +97,9 @@ struct FastParams {
     int p = 0;             // IMQ boundary order
     std::vector<double> poly;  // IMQ boundary polynomial in t = (r - r0)/eps_B (torus units), ascending
     int flags = 0;         // uotk_opts.flags (kernel family policy)
+    // grid box [box_lo, box_lo + box_w)^d holding every window footprint of the points
+    // (both sets): the spread writes only inside it and the gathers read only inside it
+    int box_lo = 0, box_w = 0;
 };
 
 // Sorted, scaled point set on device.

@@ -168,6 +168,14 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
     if (grid > 2.0e9) fail(UOTK_EUNSUPPORTED, "oversampled grid too large");
     fp.ng = ng;
     fp.b = M_PI * (2.0 - (double)N / ng);  // b = pi (2 - 1/sigma_eff)
+    {
+        // grid coordinates u in [-Rc, Rc] around index n_g/2; taps floor(u) - m + 1 .. floor(u) + m
+        const int Rc = (int)std::ceil(Rbar * ng) + 1;
+        const int lo = std::max(0, ng / 2 - Rc - fp.m);
+        const int hi = std::min(ng, ng / 2 + Rc + fp.m + 1);
+        fp.box_lo = lo;
+        fp.box_w = hi - lo;
+    }
     if (kind == UOTK_IMQ) fp.poly = imq_boundary_poly(h, param, fp.eps_B, fp.p);
     return fp;
 }
