@@ -5,6 +5,7 @@
 #include <cufft.h>
 
 #include <cstdint>
+#include <memory>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -121,17 +122,29 @@ struct PointSet {
     double chunk_fill = 0;    // mean occupied fraction of the 32 chunk slots
 };
 
-// Fourier-side plan: the D_k table and the cuFFT handles.
-struct SpectralPlan {
-    FastParams fp;
+// Kernel-dependent Fourier-side tables, cached across calls (nfft_plan.cu) by the
+// parameters they depend on; `ready` marks the end of their construction on the stream
+// that built them (other streams wait on it).
+struct PlanData {
     DevBuf<double> Dk;       // (N+1)^(d-1) * (N/2+1)
-    cufftHandle r2c = 0, c2r = 0;  // owned by the context cache
-    size_t grid_elems = 0;   // ng^d
-    size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
     // Gaussian kernel: D_k = prod_t d1(k_t) is separable, so F^-1 D F is the tensor power
     // of one real symmetric circulant n_g x n_g matrix Csep (DESIGN.md §7 "separable")
     bool separable = false;
     DevBuf<double> Csep;
+    cudaEvent_t ready = nullptr;
+    PlanData() = default;
+    PlanData(const PlanData&) = delete;
+    PlanData& operator=(const PlanData&) = delete;
+    ~PlanData();
+};
+
+// Fourier-side plan: the D_k table and the cuFFT handles.
+struct SpectralPlan {
+    FastParams fp;
+    std::shared_ptr<PlanData> pd;
+    cufftHandle r2c = 0, c2r = 0;  // owned by the context cache
+    size_t grid_elems = 0;   // ng^d
+    size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
 };
 
 // ------------------------------------------------------------------ library context

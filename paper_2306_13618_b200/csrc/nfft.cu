@@ -260,7 +260,7 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
     cublasHandle_t h = (cublasHandle_t)hv;
     if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cublasSetStream failed");
     const double one = 1.0, zero = 0.0;
-    const double* Cb = sp.Csep.p + (size_t)o * n + o;  // the box block of Csep
+    const double* Cb = sp.pd->Csep.p + (size_t)o * n + o;  // the box block of Csep
     auto ok = [](cublasStatus_t st) {
         if (st != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cuBLAS DGEMM failed (" + std::to_string((int)st) + ")");
     };
@@ -294,7 +294,7 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
 
 double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
-    if (sp.separable && (comm == nullptr || comm_nranks(comm) == 1)) {
+    if (sp.pd->separable && (comm == nullptr || comm_nranks(comm) == 1)) {
         ProfScope ps_(kProfFft, s);
         return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s);
     }
@@ -303,9 +303,9 @@ double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s,
     UOTK_CUFFT(cufftSetStream(sp.c2r, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
     const int64_t total = (int64_t)sp.spec_elems;
-    if (fp.d == 1) scale_spectrum_k<1><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total);
-    else if (fp.d == 2) scale_spectrum_k<2><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total);
-    else scale_spectrum_k<3><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total);
+    if (fp.d == 1) scale_spectrum_k<1><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
+    else if (fp.d == 2) scale_spectrum_k<2><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
+    else scale_spectrum_k<3><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
     UOTK_LAUNCHED();
     if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
     UOTK_CUFFT(cufftExecZ2D(sp.c2r, (cufftDoubleComplex*)spec, grid));
@@ -365,9 +365,9 @@ void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
     if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
     const int64_t total = (int64_t)sp.spec_elems;
-    if (fp.d == 1) spectrum_energy_k<1><<<nparts, 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total, part);
-    else if (fp.d == 2) spectrum_energy_k<2><<<nparts, 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total, part);
-    else spectrum_energy_k<3><<<nparts, 256, 0, s>>>(spec, sp.Dk.p, fp.ng, fp.N, total, part);
+    if (fp.d == 1) spectrum_energy_k<1><<<nparts, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total, part);
+    else if (fp.d == 2) spectrum_energy_k<2><<<nparts, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total, part);
+    else spectrum_energy_k<3><<<nparts, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total, part);
     UOTK_LAUNCHED();
 }
 

@@ -5,6 +5,9 @@
 //     D_k = w_k b_k / (n_g^{2d} prod_t phihat(k_t)^2),   k in I_N,
 // which turns "spread -> FFT -> *D_k -> inverse FFT -> interpolate" into the
 // factorisation (4.5)-(4.6).  See DESIGN.md "Fast summation".
+#include <tuple>
+#include <mutex>
+#include <list>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -252,8 +255,72 @@ __global__ void dk_kernel(double* Dk, const double2* bspec, const double* psi, i
     Dk[i] = fac * bspec[bidx].x * invN;
 }
 
+PlanData::~PlanData() {
+    // evicted tables may still be read by kernels queued on other streams
+    cudaDeviceSynchronize();
+    cudaGetLastError();
+    if (ready) cudaEventDestroy(ready);
+}
+
+namespace {
+
+// the tables depend on (device, d, kind, N, n_g, m, b, h, kernel parameter, IMQ boundary)
+using PlanKey = std::tuple<int, int, int, int, int, int, uint64_t, uint64_t, uint64_t, uint64_t, int, int>;
+uint64_t bits(double v) {
+    uint64_t u;
+    memcpy(&u, &v, sizeof u);
+    return u;
+}
+std::mutex g_plan_mu;
+std::list<std::pair<PlanKey, std::shared_ptr<PlanData>>> g_plans;  // most recent first
+constexpr size_t kPlanCacheSize = 8;
+
+void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s);
+
+}  // namespace
+
 void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     const FastParams& fp = sp.fp;
+    const int d = fp.d, ng = fp.ng;
+    int dev = 0;
+    UOTK_CUDA(cudaGetDevice(&dev));
+    static const bool sep_env = [] {
+        const char* e = getenv("UOTK_SEPARABLE");
+        return !(e && e[0] == '0');
+    }();
+    const PlanKey key{dev, d, fp.kind, fp.N, ng, fp.m, bits(fp.b), bits(fp.h), bits(fp.param), bits(fp.eps_B), fp.p,
+                      sep_env ? 1 : 0};
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        for (auto it = g_plans.begin(); it != g_plans.end(); ++it) {
+            if (it->first == key) {
+                sp.pd = it->second;
+                g_plans.splice(g_plans.begin(), g_plans, it);
+                break;
+            }
+        }
+    }
+    if (sp.pd) {
+        UOTK_CUDA(cudaStreamWaitEvent(s, sp.pd->ready, 0));
+    } else {
+        auto pd = std::make_shared<PlanData>();
+        build_plan_data(*pd, fp, s);
+        UOTK_CUDA(cudaEventCreateWithFlags(&pd->ready, cudaEventDisableTiming));
+        UOTK_CUDA(cudaEventRecord(pd->ready, s));
+        sp.pd = pd;
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        g_plans.emplace_front(key, pd);
+        if (g_plans.size() > kPlanCacheSize) g_plans.pop_back();
+    }
+    get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
+    sp.grid_elems = 1;
+    for (int t = 0; t < d; ++t) sp.grid_elems *= ng;
+    sp.spec_elems = sp.grid_elems / ng * (ng / 2 + 1);
+}
+
+namespace {
+
+void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s) {
     const int d = fp.d, N = fp.N, ng = fp.ng;
     // 1) samples of K_R and their DFT -> b_k (real: K_R is real and even)
     size_t nsamp = 1;
@@ -299,11 +366,11 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     // 3) D_k table
     size_t ndk = (size_t)(N / 2 + 1);
     for (int t = 0; t < d - 1; ++t) ndk *= (N + 1);
-    sp.Dk.alloc(ndk, s);
+    pd.Dk.alloc(ndk, s);
     gb = (int)((ndk + tb - 1) / tb);
-    if (d == 1) dk_kernel<1><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
-    else if (d == 2) dk_kernel<2><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
-    else dk_kernel<3><<<gb, tb, 0, s>>>(sp.Dk.p, bspec.p, psi_d.p, N);
+    if (d == 1) dk_kernel<1><<<gb, tb, 0, s>>>(pd.Dk.p, bspec.p, psi_d.p, N);
+    else if (d == 2) dk_kernel<2><<<gb, tb, 0, s>>>(pd.Dk.p, bspec.p, psi_d.p, N);
+    else dk_kernel<3><<<gb, tb, 0, s>>>(pd.Dk.p, bspec.p, psi_d.p, N);
     UOTK_LAUNCHED();
     // psi_d / samp / bspec are freed stream-ordered after the kernels that use them
 
@@ -312,7 +379,7 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     //    multiplies).  The chain F^-1 (D .* F g) is then (Csep x ... x Csep) g with the real
     //    symmetric circulant Csep[l][l'] = c(l - l'),  c(D) = d1(0) + 2 sum_{k=1}^{N/2} d1(k)
     //    cos(2 pi k D / n_g)  (k = +-N/2 carry weight 1/2 each, as in the FFT path).
-    sp.separable = false;
+    pd.separable = false;
     static const bool sep_env = [] {
         const char* e = getenv("UOTK_SEPARABLE");
         return !(e && e[0] == '0');
@@ -336,16 +403,13 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
         }
         for (int l = 0; l < ng; ++l)
             for (int lp = 0; lp < ng; ++lp) C[(size_t)l * ng + lp] = cvec[((l - lp) % ng + ng) % ng];
-        sp.Csep.alloc(C.size(), s);
-        UOTK_CUDA(cudaMemcpyAsync(sp.Csep.p, C.data(), C.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        pd.Csep.alloc(C.size(), s);
+        UOTK_CUDA(cudaMemcpyAsync(pd.Csep.p, C.data(), C.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         UOTK_CUDA(cudaStreamSynchronize(s));  // C lives on the host stack frame
-        sp.separable = true;
+        pd.separable = true;
     }
-
-    get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
-    sp.grid_elems = 1;
-    for (int t = 0; t < d; ++t) sp.grid_elems *= ng;
-    sp.spec_elems = sp.grid_elems / ng * (ng / 2 + 1);
 }
+
+}  // namespace
 
 }  // namespace uotk
