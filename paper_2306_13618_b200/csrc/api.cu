@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "epilogue.cuh"
+#include "profile.cuh"
 #include "reduce.cuh"
 
 namespace uotk {
@@ -18,6 +19,7 @@ void comm_destroy(void* comm);
 void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);
 int comm_nranks(void* comm);
 void ensure_pool();
+cudaStream_t private_stream();  // context.cu
 
 void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
                      void* comm);  // nfft.cu
@@ -116,6 +118,47 @@ size_t grid_elems(const FastParams& fp) {
     size_t g = 1;
     for (int t = 0; t < fp.d; ++t) g *= fp.ng;
     return g;
+}
+
+// Sinkhorn iterations below this many points (n + m) are replayed from CUDA graphs.
+constexpr int64_t kGraphMaxPoints = 1 << 18;
+constexpr int kGraphIters = 16;  // iterations per captured graph
+
+// Runs iterate(0) .. iterate(iters - 1) in order on stream s.  With use_graph the first
+// iteration runs eagerly (first-use initialisation: kernel attributes, cuBLAS), then
+// blocks of kGraphIters identical middle iterations are captured once and replayed, and
+// the remaining iterations (including the last, whose epilogue differs) run eagerly.
+template <class F>
+void run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s) {
+    int it = 0;
+    if (use_graph && iters >= 4) {
+        iterate(it++);
+        const int per = std::min(kGraphIters, iters - 2);
+        const int reps = (iters - 1 - it) / per;
+        if (reps >= 1) {
+            cudaGraph_t g = nullptr;
+            const int64_t l0 = g_launches;
+            UOTK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (int k = 0; k < per; ++k) iterate(it + k);  // none of them is the last
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            UOTK_CUDA(cudaStreamEndCapture(s, &g));
+            const int64_t per_launches = g_launches - l0;
+            cudaGraphExec_t ge = nullptr;
+            const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            UOTK_CUDA(ie);
+            for (int r = 0; r < reps; ++r) UOTK_CUDA(cudaGraphLaunch(ge, s));
+            UOTK_CUDA(cudaGraphExecDestroy(ge));  // safe: destruction waits for nothing, launches hold refs
+            g_launches += per_launches * (reps - 1);
+            it += reps * per;
+        }
+    }
+    for (; it < iters; ++it) iterate(it);
 }
 
 int read_flag(const DevBuf<int>& flag, cudaStream_t s) {
@@ -245,14 +288,17 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     EpiSinkhorn ex{pot_x.p, mass_x.p, wx.p, nullptr, c1, lam, flag.p};
     EpiSinkhorn ey{pot_y.p, mass_y.p, wy.p, nullptr, c2, lam, flag.p};
 
+    // small problems are launch-bound: replay the iteration from a CUDA graph
+    const bool use_graph = comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints && !profiling_enabled();
     if (method == UOTK_DIRECT) {
-        for (int it = 0; it < iters; ++it) {
+        auto iterate = [&](int it) {
             const bool last = it == iters - 1;
             direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, ex, last ? dmax.p : nullptr, s);  // (3.3)
             EpiSinkhorn e2 = ey;
             if (last) e2.t_store = ty.p;
             direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
-        }
+        };
+        run_iterations(iters, iterate, use_graph, s);
         // marginals of the recovered plan: t at x from the final gamma
         direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, EpiStore{tx.p, nullptr}, nullptr, s);
         if (iters == 0) {
@@ -268,7 +314,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         if (fused) grid2.alloc(ge, s);
         grid.zero();
         spread(PY, wy.p, grid.p, fp, s);  // adjoint NFFT of nu (.) v at y
-        for (int it = 0; it < iters; ++it) {
+        auto iterate = [&](int it) {
             const bool last = it == iters - 1;
             EpiSinkhorn e2 = ey;
             if (last) e2.t_store = ty.p;
@@ -290,7 +336,8 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                 grid.zero();
                 spread(PY, wy.p, grid.p, fp, s);
             }
-        }
+        };
+        run_iterations(iters, iterate, use_graph, s);
         // grid holds the spread of nu (.) v with the final v: t at x for the marginals
         const double* gx = fft_chain(ns.sp, grid.p, spec.p, s, comm);
         gather_epi(PX, gx, fp, EpiStore{tx.p, nullptr}, nullptr, s);
@@ -430,8 +477,34 @@ int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a, int64_
                       double eps, double lam1, double lam2, int iters, const double* gamma_init, double* beta,
                       double* gamma, uotk_uot_result* res, const uotk_opts* opts, void* comm, void* cuda_stream) {
     return guarded([&] {
-        uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm,
-                 (cudaStream_t)cuda_stream);
+        cudaStream_t cs = (cudaStream_t)cuda_stream;
+        // graph capture is impossible on the legacy / per-thread default streams: small
+        // problems (the ones replayed from CUDA graphs) run on the library's own
+        // non-blocking stream, ordered after and before the caller's stream by events
+        const bool default_stream = (uintptr_t)cs <= 2;
+        if (default_stream && comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints && n >= 0 && m >= 0) {
+            cudaStream_t ps = private_stream();
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            UOTK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+            UOTK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+            UOTK_CUDA(cudaEventRecord(e0, cs));
+            UOTK_CUDA(cudaStreamWaitEvent(ps, e0, 0));
+            try {
+                uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, ps);
+            } catch (...) {
+                cudaEventRecord(e1, ps);
+                cudaStreamWaitEvent(cs, e1, 0);
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                throw;
+            }
+            UOTK_CUDA(cudaEventRecord(e1, ps));
+            UOTK_CUDA(cudaStreamWaitEvent(cs, e1, 0));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            return;
+        }
+        uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, cs);
     });
 }
 

@@ -129,6 +129,7 @@ struct Context {
     std::map<std::tuple<int, int, int>, std::pair<cufftHandle, cufftHandle>> fft;
     bool pool_configured[64] = {};
     std::map<int, cublasHandle_t> blas;
+    std::map<int, cudaStream_t> streams;
 };
 
 Context& ctx() {
@@ -189,6 +190,20 @@ void get_cublas(void** handle) {
         it = c.blas.emplace(dev, h).first;
     }
     *handle = it->second;
+}
+
+cudaStream_t private_stream() {
+    int dev = 0;
+    UOTK_CUDA(cudaGetDevice(&dev));
+    Context& c = ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.streams.find(dev);
+    if (it == c.streams.end()) {
+        cudaStream_t st;
+        UOTK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        it = c.streams.emplace(dev, st).first;
+    }
+    return it->second;
 }
 
 void ensure_pool() {

@@ -37,6 +37,12 @@ cudaEvent_t take_event(Prof& p) {
 const char* kTagNames[kProfTags] = {"spread", "gather", "fused", "fft", "direct", "setup"};
 }  // namespace
 
+bool profiling_enabled() {
+    Prof& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    return p.on;
+}
+
 ProfScope::ProfScope(int tag, cudaStream_t s) : tag_(tag), s_(s) {
     Prof& p = prof();
     if (!p.on) return;

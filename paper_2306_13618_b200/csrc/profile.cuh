@@ -7,6 +7,8 @@ namespace uotk {
 enum ProfTag { kProfSpread = 0, kProfGather = 1, kProfFused = 2, kProfFft = 3, kProfDirect = 4, kProfSetup = 5 };
 constexpr int kProfTags = 6;
 
+bool profiling_enabled();
+
 class ProfScope {
    public:
     ProfScope(int tag, cudaStream_t s);

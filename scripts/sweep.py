@@ -39,13 +39,12 @@ def spin_up(seconds=0.3):
 
 
 def timed(fn, reps=3):
-    """Median device time per call over `reps` calls (each bracketed by CUDA events), the
-    library's per-tag kernel times and launch count averaged over the same calls."""
+    """Median device time per call over `reps` unprofiled calls (each bracketed by CUDA
+    events on the current stream); then one profiled call for the per-tag kernel times
+    (profiling brackets every launch with events and disables the CUDA-graph replay)."""
     fn()
     spin_up()
     torch.cuda.synchronize()
-    uk.profile_enable(True)
-    uk.profile_reset()
     uk.reset_launch_counter()
     times, walls = [], []
     for _ in range(reps):
@@ -57,10 +56,14 @@ def timed(fn, reps=3):
         torch.cuda.synchronize()
         walls.append((time.perf_counter() - w0) * 1e3)
         times.append(s.elapsed_time(e))
+    launches = uk.launch_counter() / reps
     timed.wall_ms = float(np.median(walls))
     ms = float(np.median(times))
-    prof = {k: round(v[0] / reps, 4) for k, v in uk.profile_read().items() if v[1]}
-    launches = uk.launch_counter() / reps
+    uk.profile_enable(True)
+    uk.profile_reset()
+    fn()
+    torch.cuda.synchronize()
+    prof = {k: round(v[0], 4) for k, v in uk.profile_read().items() if v[1]}
     uk.profile_enable(False)
     return ms, prof, launches, out
 
