@@ -420,3 +420,22 @@ def test_kernel_sum_c5_1e8_d3_sampled(uk):
     idx = np.random.default_rng(7).choice(len(pr.tgt), 8, replace=False)
     ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt[idx], pr.kind, pr.param, block_bytes=1 << 31)
     assert np.max(np.abs(g_all[idx] - ref)) / np.max(np.abs(ref)) <= 1e-9
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_small_graph_replay_on_user_stream(uk, method):
+    """Small problems replay captured iterations from CUDA graphs: on a caller-created
+    stream (captured directly) and on the default stream (the library's own stream),
+    both equal to the oracle; iteration counts that leave eager remainders."""
+    pr = W.c1_uot(n=700, m=650)
+    for iters in (4, 37):
+        ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, iters)
+        st = torch.cuda.Stream()
+        args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            beta, gamma, res = uk.uot_sinkhorn(*args, iters=iters, opts={"method": method}, stream=st)
+        st.synchronize()
+        _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+        beta2, gamma2, res2 = uk.uot_sinkhorn(*args, iters=iters, opts={"method": method})
+        _uot_check(res2, beta2.cpu().numpy(), gamma2.cpu().numpy(), ref)
