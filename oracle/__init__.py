@@ -16,6 +16,9 @@ What is computed, and where it comes from (``P:n`` = line n of the paper text
 * ``sinkhorn``    — Algorithm 1 step by step: updates (3.3)/(3.4)
                     with dense direct sums, the plan recovery of P:488, the dual
                     (3.1) and the discrete primal.
+                    Also the constant c* of Prop. 2.9 / Eq. (2.10), the
+                    Sinkhorn divergence of Eq. (2.12), and a tolerance stopping
+                    rule (reading R20).
 * ``mmd``         — the discrete MMD^2 of Eq. (3.5), V-statistic form.
 
 Every function is pinned by ``tests/test_oracle_pins.py`` against closed forms,
@@ -31,5 +34,7 @@ from .sinkhorn import (  # noqa: F401
     primal_objective_dense,
     primal_objective_marginals,
     SinkhornResult,
+    cstar,
+    sinkhorn_divergence_direct,
 )
 from .mmd import mmd2_direct, mmd2_combined  # noqa: F401

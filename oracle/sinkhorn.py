@@ -149,12 +149,18 @@ def primal_objective_marginals(mu, nu, beta, gamma, p, q, eps, eta1, eta2):
     )
 
 
-def uot_sinkhorn_direct(x, mu, y, nu, eps, eta1, eta2=None, iters=100, gamma0=None):
+def uot_sinkhorn_direct(x, mu, y, nu, eps, eta1, eta2=None, iters=100, gamma0=None, stop_tol=0.0,
+                        check_every=10):
     """Algorithm 1 for `iters` iterations from gamma^0 (default 0).
 
     Returns beta^{2*iters-1}, gamma^{2*iters} and the objective values of the
     recovered plan: primal, dual (3.1), plan mass pi(X x X), and the
     sup-norm changes of the potentials in the last iteration.
+
+    Stopping rule (reading R20 of DESIGN.md; the paper's "while stopping criteria",
+    P:502/P:618): with stop_tol > 0, after every `check_every`-th iteration the loop
+    ends once max_i |beta_i - beta_i^prev| <= stop_tol and max_j |gamma_j -
+    gamma_j^prev| <= stop_tol (changes within that iteration); `iters` is then the cap.
     """
     if eta2 is None:
         eta2 = eta1
@@ -166,13 +172,17 @@ def uot_sinkhorn_direct(x, mu, y, nu, eps, eta1, eta2=None, iters=100, gamma0=No
     gamma = np.zeros(m) if gamma0 is None else np.array(gamma0, dtype=np.float64)
     beta = np.zeros(n)
     dbeta = dgamma = 0.0
-    for _ in range(iters):
+    done = 0
+    for it in range(iters):
         beta_new = beta_step(x, y, nu, gamma, eps, eta1)  # Delta odd  (3.3)
         dbeta = float(np.max(np.abs(beta_new - beta))) if n else 0.0
         beta = beta_new
         gamma_new = gamma_step(x, y, mu, beta, eps, eta2)  # Delta even (3.4)
         dgamma = float(np.max(np.abs(gamma_new - gamma))) if m else 0.0
         gamma = gamma_new
+        done = it + 1
+        if stop_tol > 0 and done % check_every == 0 and dbeta <= stop_tol and dgamma <= stop_tol:
+            break
     p, q = plan_marginals(x, mu, y, nu, beta, gamma, eps)
     primal = primal_objective_marginals(mu, nu, beta, gamma, p, q, eps, eta1, eta2)
     dual = dual_objective(x, mu, y, nu, beta, gamma, eps, eta1, eta2)
@@ -186,5 +196,47 @@ def uot_sinkhorn_direct(x, mu, y, nu, eps, eta1, eta2=None, iters=100, gamma0=No
         mass_b=float(np.sum(nu)),
         max_dbeta=dbeta,
         max_dgamma=dgamma,
-        iters=iters,
+        iters=done,
     )
+
+
+def cstar(x, mu, y, nu, eps, eta1, eta2=None):
+    """Prop. 2.9, Eq. (2.10) (P:229-233) with r = 2 and lambda = 1/eps:
+
+        c* = exp(-<mu (x) nu | d^2> / (mu(X) nu(X) (eta1 + eta2 + 1/lambda)))
+             * mu(X)^(-eta2 / (eta1 + eta2 + 1/lambda)) * nu(X)^(-eta1 / (...)),
+
+    with <mu (x) nu | d^2> = sum_ij mu_i nu_j ||x_i - x~_j||^2 summed by its definition
+    (all pairwise differences, numpy pairwise summation)."""
+    if eta2 is None:
+        eta2 = eta1
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    x = x.reshape(len(mu), -1)
+    y = y.reshape(len(nu), -1)
+    mu = np.asarray(mu, dtype=np.float64)
+    nu = np.asarray(nu, dtype=np.float64)
+    total = 0.0
+    for i0 in range(0, len(mu), 256):  # blocks of rows only to bound memory
+        d2 = np.sum((x[i0:i0 + 256, None, :] - y[None, :, :]) ** 2, axis=2)
+        total += float(np.sum(mu[i0:i0 + 256, None] * d2 * nu[None, :]))
+    ma, mb = float(np.sum(mu)), float(np.sum(nu))
+    S = eta1 + eta2 + eps
+    return float(np.exp(-total / (ma * mb * S)) * ma ** (-eta2 / S) * mb ** (-eta1 / S))
+
+
+def sinkhorn_divergence_direct(x, mu, y, nu, eps, eta1, eta2=None, iters=100):
+    """The debiased UOT of Eq. (2.12) (Rem. 2.11), lambda = 1/eps:
+
+        sd = UOT(mu, nu) - UOT(mu, mu)/2 - UOT(nu, nu)/2 + (eps/2) (mu(X) - nu(X))^2,
+
+    each UOT the primal value (reading R3) after `iters` iterations of Algorithm 1.
+    Returns (sd, (uot_xy, uot_xx, uot_yy))."""
+    if eta2 is None:
+        eta2 = eta1
+    rxy = uot_sinkhorn_direct(x, mu, y, nu, eps, eta1, eta2, iters)
+    rxx = uot_sinkhorn_direct(x, mu, x, mu, eps, eta1, eta2, iters)
+    ryy = uot_sinkhorn_direct(y, nu, y, nu, eps, eta1, eta2, iters)
+    ma, mb = float(np.sum(mu)), float(np.sum(nu))
+    sd = rxy.primal - 0.5 * rxx.primal - 0.5 * ryy.primal + 0.5 * eps * (ma - mb) ** 2
+    return sd, (rxy.primal, rxx.primal, ryy.primal)

@@ -58,6 +58,7 @@ def timed(fn, reps=3):
         times.append(s.elapsed_time(e))
     launches = uk.launch_counter() / reps
     timed.wall_ms = float(np.median(walls))
+    timed.all_ms = [round(t, 3) for t in times]
     ms = float(np.median(times))
     uk.profile_enable(True)
     uk.profile_reset()
@@ -70,6 +71,7 @@ def timed(fn, reps=3):
 
 def emit(**kw):
     kw["wall_ms"] = round(getattr(timed, "wall_ms", 0.0), 3)
+    kw["all_ms"] = getattr(timed, "all_ms", None)
     print(json.dumps(kw), flush=True)
 
 

@@ -323,3 +323,82 @@ def test_mmd_gaussian_mixture_closed_form(d, q, rtol):
     v = oracle.mmd2_direct(px, wx, py, wy, GAUSS, ell2)
     ref = cf.gm_population_mmd2(mx, my, sigma, ell2, 1.3, 0.8)
     np.testing.assert_allclose(v, ref, rtol=rtol)
+
+
+# ------------------------------------------------------------------ c*, Sinkhorn divergence, stopping
+def test_cstar_oracle_golden_coincident():
+    """Eq. (2.10) with a zero transport term (all points at one location): the SPEC
+    worked example mu(X)=2, nu(X)=3, eta=1, lambda=1 gives 6^(-1/3) (golden file)."""
+    g = golden("cstar_example.json")
+    x = np.zeros((3, 2))
+    y = np.zeros((2, 2))
+    mu = np.array([0.5, 1.0, 0.5]) * g["mass_a"] / 2.0
+    nu = np.array([1.0, 2.0]) * g["mass_b"] / 3.0
+    c = oracle.cstar(x, mu, y, nu, 1.0 / g["lambda"], g["eta1"], g["eta2"])
+    np.testing.assert_allclose(c, g["c_star"], rtol=1e-14)
+
+
+@pytest.mark.parametrize("eta1,eta2", [(1.0, 1.0), (0.3, 2.0)])
+def test_cstar_oracle_minimises_restricted_primal(eta1, eta2):
+    """c* (with the transport moment summed by the oracle) minimises the independently
+    written primal of P:462 along the ray c * mu (x) nu (Prop. 2.9)."""
+    rng = np.random.default_rng(12)
+    x = uniform_ball(rng, 17, 3, 0.2)
+    y = uniform_ball(rng, 11, 3, 0.2)
+    mu = rng.uniform(0.5, 1.5, 17)
+    nu = rng.uniform(0.2, 2.0, 11)
+    eps = 0.05
+    d2 = np.sum((x[:, None] - y[None]) ** 2, 2)
+    c = oracle.cstar(x, mu, y, nu, eps, eta1, eta2)
+    f = lambda cc: cf.primal_of_plan(cc * np.outer(mu, nu), d2, mu, nu, 1 / eps, eta1, eta2)  # noqa: E731
+    for fac in (0.999, 1.001, 0.9, 1.1):
+        assert f(fac * c) > f(c)
+
+
+def test_sinkhorn_divergence_single_atoms_closed_form():
+    """Eq. (2.12) for single atoms at one location: every UOT term has the closed-form
+    plan mass of the coincident single-atom problem, so sd is explicit; pins the signs
+    and the (eps/2)(mu(X) - nu(X))^2 term."""
+    a, b, eps, eta = 2.0, 0.7, 0.3, 0.8
+    lam = 1.0 / eps
+
+    def uot_closed(m1, m2):
+        pi = cf.single_atom_plan_mass(m1, m2, lam, eta, eta)
+        return cf.primal_of_plan(np.array([[pi]]), np.zeros((1, 1)), np.array([m1]), np.array([m2]), lam, eta, eta)
+
+    want = uot_closed(a, b) - 0.5 * uot_closed(a, a) - 0.5 * uot_closed(b, b) + 0.5 * eps * (a - b) ** 2
+    p = np.array([[0.05, -0.1]])
+    sd, _ = oracle.sinkhorn_divergence_direct(p, np.array([a]), p, np.array([b]), eps, eta, eta, iters=400)
+    np.testing.assert_allclose(sd, want, rtol=1e-12, atol=1e-14)
+
+
+def test_sinkhorn_divergence_identities():
+    """sd(mu, mu) = 0 and sd(mu, nu) = sd(nu, mu) for eta1 = eta2 (UOT is then symmetric)."""
+    rng = np.random.default_rng(13)
+    x = uniform_ball(rng, 9, 2, 0.2)
+    y = uniform_ball(rng, 7, 2, 0.2)
+    mu = rng.uniform(0.5, 1.5, 9)
+    nu = rng.uniform(0.2, 2.0, 7)
+    s0, _ = oracle.sinkhorn_divergence_direct(x, mu, x, mu, 0.05, 1.0, iters=60)
+    assert abs(s0) <= 1e-12 * mu.sum() ** 2
+    s1, _ = oracle.sinkhorn_divergence_direct(x, mu, y, nu, 0.05, 1.0, iters=300)
+    s2, _ = oracle.sinkhorn_divergence_direct(y, nu, x, mu, 0.05, 1.0, iters=300)
+    np.testing.assert_allclose(s1, s2, rtol=1e-9)
+
+
+def test_stopping_rule():
+    """With stop_tol the oracle stops at the first multiple of check_every whose
+    iteration changed both potentials by <= stop_tol, and the result equals the
+    fixed-iteration run of that length."""
+    rng = np.random.default_rng(14)
+    x = uniform_ball(rng, 25, 2, 0.2)
+    y = uniform_ball(rng, 20, 2, 0.2)
+    mu = rng.uniform(0.5, 1.5, 25)
+    nu = rng.uniform(0.2, 2.0, 20)
+    r = oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, 1.0, iters=500, stop_tol=1e-9, check_every=7)
+    assert r.iters % 7 == 0 and r.iters < 500
+    assert r.max_dbeta <= 1e-9 and r.max_dgamma <= 1e-9
+    prev = oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, 1.0, iters=r.iters - 7)
+    assert prev.max_dbeta > 1e-9 or prev.max_dgamma > 1e-9
+    fixed = oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, 1.0, iters=r.iters)
+    np.testing.assert_array_equal(fixed.beta, r.beta)
