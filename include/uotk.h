@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define UOTK_ABI_VERSION 1
+#define UOTK_ABI_VERSION 2
 
 /* Status codes (mirroring SPEC's split of input vs numeric errors). */
 enum {
@@ -85,6 +85,13 @@ typedef struct {
     double tol;       /* target truncation tolerance of the auto rules; 0 = 1e-16        */
     int32_t flags;    /* UOTK_FLAG_* bits below; 0 = automatic                           */
     int32_t reserved; /* must be 0                                                       */
+    /* Sinkhorn stopping rule (reading R20 of DESIGN.md; the paper's "while stopping
+     * criteria"): with stop_tol > 0, after every check_every-th iteration the
+     * loop ends once the sup-norm changes of beta and gamma within that iteration are
+     * both <= stop_tol; `iters` is then the cap and uotk_uot_result.iters the count. */
+    double stop_tol;     /* 0 = run exactly `iters` iterations                            */
+    int32_t check_every; /* 0 = 10                                                        */
+    int32_t reserved2;   /* must be 0                                                     */
 } uotk_opts;
 
 /* opts.flags: which spread/gather kernels the NFFT path may use (results agree to
@@ -172,6 +179,33 @@ int uotk_mmd2(int d, int64_t n, const double* x, const double* a,
               int64_t m, const double* y, const double* b, int kind, double param,
               double* mmd2, const uotk_opts* opts, uotk_info* info,
               void* comm, void* cuda_stream);
+
+/*
+ * The constant c* of Prop. 2.9, Eq. (2.10), r = 2, lambda = 1/eps:
+ *   c* = exp(-<mu x nu | d^2> / (mu(X) nu(X) (lam1 + lam2 + eps))) mu(X)^(-lam2/(..)) nu(X)^(-lam1/(..))
+ * with the transport moment <mu x nu | d^2> = sum_ij a_i b_j ||x_i - y_j||^2 evaluated
+ * from first and second moments in O((n + m) d) (centred, two passes).  Remark 5.2
+ * uses it to initialise Algorithm 2 with gamma^0 = c* 1.  *cstar: host double.
+ * Masses must be positive (UOTK_EDOMAIN otherwise).  With `comm`, the moments are
+ * summed over ranks.
+ */
+int uotk_uot_cstar(int d, int64_t n, const double* x, const double* a,
+                   int64_t m, const double* y, const double* b,
+                   double eps, double lam1, double lam2, double* cstar,
+                   void* comm, void* cuda_stream);
+
+/*
+ * Sinkhorn divergence of Eq. (2.12) (Rem. 2.11), the debiased UOT:
+ *   sd = UOT(mu, nu) - UOT(mu, mu)/2 - UOT(nu, nu)/2 + (eps/2) (mu(X) - nu(X))^2
+ * each UOT the primal value (uotk_uot_result.primal) of uotk_uot_sinkhorn with the
+ * same arguments and `iters`.  *sd: host double; terms (may be NULL): host double[3] =
+ * {UOT(mu,nu), UOT(mu,mu), UOT(nu,nu)}.
+ */
+int uotk_sinkhorn_divergence(int d, int64_t n, const double* x, const double* a,
+                             int64_t m, const double* y, const double* b,
+                             double eps, double lam1, double lam2, int iters,
+                             double* sd, double* terms, const uotk_opts* opts,
+                             void* comm, void* cuda_stream);
 
 /* Multi-GPU communicator (one process per GPU).  uotk_comm_unique_id fills 128
  * bytes on one rank; broadcast them (e.g. with torch.distributed) and call

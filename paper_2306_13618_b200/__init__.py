@@ -27,7 +27,8 @@ FLAG_GENERIC, FLAG_CHUNKED = 1, 2  # opts["flags"]: kernel family of the NFFT pa
 _KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, GAUSS: GAUSS, IMQ: IMQ}
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 
-__all__ = ["kernel_sum", "uot_sinkhorn", "mmd2", "Comm", "UOTResult", "GAUSS", "IMQ", "UotkError",
+__all__ = ["kernel_sum", "uot_sinkhorn", "mmd2", "uot_cstar", "sinkhorn_divergence", "Comm", "UOTResult", "GAUSS",
+           "IMQ", "UotkError",
            "launch_counter", "reset_launch_counter", "library_path"]
 
 
@@ -174,6 +175,13 @@ def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, op
     X, A, Y, B = _Arr(x, "x", d), _Arr(a, "a"), _Arr(y, "y", d), _Arr(b, "b")
     if A.shape != (X.n,) or B.shape != (Y.n,):
         raise ValueError("masses must match the point counts")
+    if isinstance(gamma_init, str):
+        if gamma_init != "cstar":
+            raise ValueError("gamma_init: an array, None or 'cstar'")
+        # Remark 5.2: gamma^0 = c* 1 with c* of Eq. (2.10)
+        c = uot_cstar(x, a, y, b, eps, lam, lam2, comm=comm, stream=stream)
+        gamma_init = _like(Y, Y.n)
+        gamma_init[:] = c
     G0 = _Arr(gamma_init, "gamma_init") if gamma_init is not None else None
     beta = _like(X, X.n)
     gamma = _like(Y, Y.n)
@@ -188,6 +196,40 @@ def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, op
     r = UOTResult(res.primal, res.dual, res.plan_mass, res.mass_a, res.mass_b, res.max_dbeta, res.max_dgamma,
                   res.iters, _info_dict(res.info))
     return BO.obj, GO.obj, r
+
+
+def uot_cstar(x, a, y, b, eps, lam, lam2=None, comm=None, stream=None):
+    """The constant c* of Prop. 2.9 / Eq. (2.10) for r = 2 (host float)."""
+    lib = _native.load()
+    d = _dim(x, "x")
+    X, A, Y, B = _Arr(x, "x", d), _Arr(a, "a"), _Arr(y, "y", d), _Arr(b, "b")
+    if A.shape != (X.n,) or B.shape != (Y.n,):
+        raise ValueError("masses must match the point counts")
+    out = ctypes.c_double(0.0)
+    lam2 = lam if lam2 is None else lam2
+    code = lib.uotk_uot_cstar(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam), float(lam2),
+                              ctypes.byref(out), _comm_ptr(comm), _stream(stream, [X, A, Y, B]))
+    _native.check(code)
+    return out.value
+
+
+def sinkhorn_divergence(x, a, y, b, eps, lam, lam2=None, iters=100, opts=None, comm=None, stream=None,
+                        return_terms=False):
+    """Debiased UOT of Eq. (2.12): UOT(mu,nu) - UOT(mu,mu)/2 - UOT(nu,nu)/2 + eps/2 (mu(X)-nu(X))^2."""
+    lib = _native.load()
+    d = _dim(x, "x")
+    X, A, Y, B = _Arr(x, "x", d), _Arr(a, "a"), _Arr(y, "y", d), _Arr(b, "b")
+    if A.shape != (X.n,) or B.shape != (Y.n,):
+        raise ValueError("masses must match the point counts")
+    sd = ctypes.c_double(0.0)
+    terms = (ctypes.c_double * 3)()
+    o = _opts(opts)
+    lam2 = lam if lam2 is None else lam2
+    code = lib.uotk_sinkhorn_divergence(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam),
+                                        float(lam2), int(iters), ctypes.byref(sd), terms, ctypes.byref(o),
+                                        _comm_ptr(comm), _stream(stream, [X, A, Y, B]))
+    _native.check(code)
+    return (sd.value, tuple(terms)) if return_terms else sd.value
 
 
 def mmd2(x, a, y, b, kind="gauss", param=None, opts=None, comm=None, stream=None, return_info=False):

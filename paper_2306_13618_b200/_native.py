@@ -20,6 +20,7 @@ STATUS = {
 # every symbol include/uotk.h declares (tests check the library exports all of them)
 EXPORTED = (
     "uotk_opts_init", "uotk_kernel_sum", "uotk_uot_sinkhorn", "uotk_mmd2",
+    "uotk_uot_cstar", "uotk_sinkhorn_divergence",
     "uotk_comm_unique_id", "uotk_comm_create", "uotk_comm_destroy",
     "uotk_last_error", "uotk_abi_version", "uotk_launch_counter", "uotk_launch_counter_reset",
     "uotk_profile_enable", "uotk_profile_reset", "uotk_profile_read",
@@ -31,7 +32,8 @@ class UotkOpts(ctypes.Structure):
         ("method", ctypes.c_int32), ("N", ctypes.c_int32), ("sigma", ctypes.c_double),
         ("m", ctypes.c_int32), ("p", ctypes.c_int32), ("eps_B", ctypes.c_double),
         ("h", ctypes.c_double), ("tol", ctypes.c_double), ("flags", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("reserved", ctypes.c_int32), ("stop_tol", ctypes.c_double), ("check_every", ctypes.c_int32),
+        ("reserved2", ctypes.c_int32),
     ]
 
 
@@ -86,6 +88,11 @@ def load():
     lib.uotk_mmd2.argtypes = [INT, I64, P, P, I64, P, P, INT, D, ctypes.POINTER(D),
                               ctypes.POINTER(UotkOpts), ctypes.POINTER(UotkInfo), P, P]
     lib.uotk_mmd2.restype = INT
+    lib.uotk_uot_cstar.argtypes = [INT, I64, P, P, I64, P, P, D, D, D, ctypes.POINTER(D), P, P]
+    lib.uotk_uot_cstar.restype = INT
+    lib.uotk_sinkhorn_divergence.argtypes = [INT, I64, P, P, I64, P, P, D, D, D, INT, ctypes.POINTER(D), P,
+                                             ctypes.POINTER(UotkOpts), P, P]
+    lib.uotk_sinkhorn_divergence.restype = INT
     lib.uotk_comm_unique_id.argtypes = [P]
     lib.uotk_comm_unique_id.restype = INT
     lib.uotk_comm_create.argtypes = [P, INT, INT, ctypes.POINTER(P)]

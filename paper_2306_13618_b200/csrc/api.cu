@@ -62,6 +62,9 @@ uotk_opts resolve(const uotk_opts* o) {
     if (r.method < 0 || r.method > 2) fail(UOTK_EINVAL, "opts.method must be AUTO, NFFT or DIRECT");
     if (r.N < 0 || r.m < 0 || r.p < 0 || r.sigma < 0 || r.eps_B < 0 || r.h < 0 || r.tol < 0 || r.tol >= 1)
         fail(UOTK_EINVAL, "negative option value");
+    if (!(r.stop_tol >= 0) || r.check_every < 0 || r.reserved2 != 0)
+        fail(UOTK_EINVAL, "opts.stop_tol / check_every must be >= 0 and reserved2 = 0");
+    if (r.check_every == 0) r.check_every = 10;
     return r;
 }
 
@@ -129,7 +132,25 @@ constexpr int kGraphIters = 16;  // iterations per captured graph
 // blocks of kGraphIters identical middle iterations are captured once and replayed, and
 // the remaining iterations (including the last, whose epilogue differs) run eagerly.
 template <class F>
-void run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s) {
+int run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s, int check_every = 0,
+                   double stop_tol = 0.0, const unsigned long long* dmax = nullptr) {
+    if (check_every > 0) {
+        // stopping rule: after every check_every-th iteration read the two sup-norm
+        // changes (non-negative doubles stored as their bit patterns) and stop if both
+        // are <= stop_tol
+        for (int it = 0; it < iters; ++it) {
+            iterate(it);
+            if ((it + 1) % check_every == 0 && it + 1 < iters) {
+                unsigned long long h[2];
+                UOTK_CUDA(cudaMemcpyAsync(h, dmax, sizeof h, cudaMemcpyDeviceToHost, s));
+                UOTK_CUDA(cudaStreamSynchronize(s));
+                double v[2];
+                memcpy(v, h, sizeof v);
+                if (v[0] <= stop_tol && v[1] <= stop_tol) return it + 1;
+            }
+        }
+        return iters;
+    }
     int it = 0;
     if (use_graph && iters >= 4) {
         iterate(it++);
@@ -159,6 +180,7 @@ void run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s) {
         }
     }
     for (; it < iters; ++it) iterate(it);
+    return iters;
 }
 
 int read_flag(const DevBuf<int>& flag, cudaStream_t s) {
@@ -289,16 +311,23 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     EpiSinkhorn ey{pot_y.p, mass_y.p, wy.p, nullptr, c2, lam, flag.p};
 
     // small problems are launch-bound: replay the iteration from a CUDA graph
-    const bool use_graph = comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints && !profiling_enabled();
+    const bool stop_rule = o.stop_tol > 0;
+    const bool use_graph =
+        comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints && !profiling_enabled() && !stop_rule;
+    // iterations whose sup-norm changes are recorded: the last one, and with the stopping
+    // rule every check_every-th one (dmax is reset before each of them)
+    auto records = [&](int it) { return it == iters - 1 || (stop_rule && (it + 1) % o.check_every == 0); };
+    int done = iters;
     if (method == UOTK_DIRECT) {
         auto iterate = [&](int it) {
-            const bool last = it == iters - 1;
+            const bool last = records(it);
+            if (last) dmax.zero();
             direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, ex, last ? dmax.p : nullptr, s);  // (3.3)
             EpiSinkhorn e2 = ey;
             if (last) e2.t_store = ty.p;
             direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
         };
-        run_iterations(iters, iterate, use_graph, s);
+        done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p);
         // marginals of the recovered plan: t at x from the final gamma
         direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, EpiStore{tx.p, nullptr}, nullptr, s);
         if (iters == 0) {
@@ -315,7 +344,8 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         grid.zero();
         spread(PY, wy.p, grid.p, fp, s);  // adjoint NFFT of nu (.) v at y
         auto iterate = [&](int it) {
-            const bool last = it == iters - 1;
+            const bool last = records(it);
+            if (last) dmax.zero();
             EpiSinkhorn e2 = ey;
             if (last) e2.t_store = ty.p;
             if (fused) {
@@ -337,7 +367,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                 spread(PY, wy.p, grid.p, fp, s);
             }
         };
-        run_iterations(iters, iterate, use_graph, s);
+        done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p);
         // grid holds the spread of nu (.) v with the final v: t at x for the marginals
         const double* gx = fft_chain(ns.sp, grid.p, spec.p, s, comm);
         gather_epi(PX, gx, fp, EpiStore{tx.p, nullptr}, nullptr, s);
@@ -391,9 +421,112 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         res->mass_b = my;
         res->max_dbeta = hs[10];
         res->max_dgamma = hs[11];
-        res->iters = iters;
+        res->iters = done;
         fill_info(&res->info, method, fpp);
     }
+}
+
+// ============================================================== Sinkhorn divergence (2.12)
+static void sd_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
+                    const double* b, double eps, double lam1, double lam2, int iters, double* sd, double* terms,
+                    const uotk_opts* opts, void* comm, cudaStream_t s) {
+    need(sd != nullptr, "sd output pointer is null");
+    need(n >= 1 && m >= 1, "n and m must be >= 1");
+    ensure_pool();
+    DevBuf<double> p1(n, s), q1(m, s), p2(n, s), q2(n, s), p3(m, s), q3(m, s);  // potentials (unused)
+    uotk_uot_result r1, r2, r3;
+    uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, nullptr, p1.p, q1.p, &r1, opts, comm, s);
+    uot_impl(d, n, x, a, n, x, a, eps, lam1, lam2, iters, nullptr, p2.p, q2.p, &r2, opts, comm, s);
+    uot_impl(d, m, y, b, m, y, b, eps, lam1, lam2, iters, nullptr, p3.p, q3.p, &r3, opts, comm, s);
+    const double dmass = r1.mass_a - r1.mass_b;
+    *sd = r1.primal - 0.5 * r2.primal - 0.5 * r3.primal + 0.5 * eps * dmass * dmass;
+    if (terms) {
+        terms[0] = r1.primal;
+        terms[1] = r2.primal;
+        terms[2] = r3.primal;
+    }
+}
+
+// Graph capture is impossible on the legacy / per-thread default streams: work that
+// may be replayed from CUDA graphs (small Sinkhorn problems) runs on the library's own
+// non-blocking stream, ordered after and before the caller's stream by events.
+template <class F>
+void on_capturable_stream(cudaStream_t cs, bool graphable, F&& f) {
+    const bool default_stream = (uintptr_t)cs <= 2;
+    if (!(graphable && default_stream)) {
+        f(cs);
+        return;
+    }
+    cudaStream_t ps = private_stream();
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    UOTK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    UOTK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    UOTK_CUDA(cudaEventRecord(e0, cs));
+    UOTK_CUDA(cudaStreamWaitEvent(ps, e0, 0));
+    auto finish = [&] {
+        cudaEventRecord(e1, ps);
+        cudaStreamWaitEvent(cs, e1, 0);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    };
+    try {
+        f(ps);
+    } catch (...) {
+        finish();
+        throw;
+    }
+    finish();
+}
+
+// ============================================================== c* (Prop. 2.9)
+static void cstar_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
+                       const double* b, double eps, double lam1, double lam2, double* cstar, void* comm,
+                       cudaStream_t s) {
+    need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
+    need(n >= 1 && m >= 1, "n and m must be >= 1");
+    need(x && a && y && b && cstar, "null pointer argument");
+    need(eps > 0 && std::isfinite(eps), "eps must be positive and finite");
+    need(lam1 > 0 && lam2 > 0 && std::isfinite(lam1) && std::isfinite(lam2), "lam1, lam2 must be positive");
+    ensure_pool();
+    InArr X, A, Y, B;
+    X.bind(x, (size_t)n * d, s);
+    A.bind(a, (size_t)n, s);
+    Y.bind(y, (size_t)m * d, s);
+    B.bind(b, (size_t)m, s);
+    DevBuf<int> flag(1, s);
+    flag.zero();
+    check_mass(A.d, n, flag.p, s);
+    check_mass(B.d, m, flag.p, s);
+    if (read_flag(flag, s) & 4) fail(UOTK_EDOMAIN, "masses must be positive and finite");
+    const int nc = 2 + d;
+    DevBuf<double> cols((size_t)nc * std::max(n, m), s), sums(2 * nc, s), cen(2 * d, s);
+    // <mu x nu | d^2> = A B |mx - my|^2 + B sum a |x - mx|^2 + A sum b |y - my|^2 with the
+    // weighted means mx, my: pass 1 the masses and first moments, pass 2 the centred
+    // second moments (no cancellation between large raw moments)
+    double h[2 * 5];
+    auto moments = [&](const double* cx, const double* cy) {
+        moment_cols(X.d, A.d, n, d, cx, cols.p, s);
+        sum_columns(cols.p, n, nc, sums.p, s);
+        moment_cols(Y.d, B.d, m, d, cy, cols.p, s);
+        sum_columns(cols.p, m, nc, sums.p + nc, s);
+        if (comm) comm_allreduce(sums.p, 2 * nc, 0, comm, s);
+        UOTK_CUDA(cudaMemcpyAsync(h, sums.p, 2 * nc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        UOTK_CUDA(cudaStreamSynchronize(s));
+    };
+    moments(nullptr, nullptr);
+    const double Am = h[0], Bm = h[nc];
+    double mean[2 * kMaxD];
+    for (int t = 0; t < d; ++t) {
+        mean[t] = h[2 + t] / Am;
+        mean[d + t] = h[nc + 2 + t] / Bm;
+    }
+    UOTK_CUDA(cudaMemcpyAsync(cen.p, mean, 2 * d * sizeof(double), cudaMemcpyHostToDevice, s));
+    moments(cen.p, cen.p + d);
+    double dm2 = 0.0;
+    for (int t = 0; t < d; ++t) dm2 += (mean[t] - mean[d + t]) * (mean[t] - mean[d + t]);
+    const double T = Am * Bm * dm2 + Bm * h[1] + Am * h[nc + 1];
+    const double S = lam1 + lam2 + eps;
+    *cstar = std::exp(-T / (Am * Bm * S)) * std::pow(Am, -lam2 / S) * std::pow(Bm, -lam1 / S);
 }
 
 // ============================================================== MMD^2
@@ -478,32 +611,11 @@ int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a, int64_
                       double* gamma, uotk_uot_result* res, const uotk_opts* opts, void* comm, void* cuda_stream) {
     return guarded([&] {
         cudaStream_t cs = (cudaStream_t)cuda_stream;
-        // graph capture is impossible on the legacy / per-thread default streams: small
-        // problems (the ones replayed from CUDA graphs) run on the library's own
-        // non-blocking stream, ordered after and before the caller's stream by events
-        const bool default_stream = (uintptr_t)cs <= 2;
-        if (default_stream && comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints && n >= 0 && m >= 0) {
-            cudaStream_t ps = private_stream();
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            UOTK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
-            UOTK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
-            UOTK_CUDA(cudaEventRecord(e0, cs));
-            UOTK_CUDA(cudaStreamWaitEvent(ps, e0, 0));
-            try {
-                uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, ps);
-            } catch (...) {
-                cudaEventRecord(e1, ps);
-                cudaStreamWaitEvent(cs, e1, 0);
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
-                throw;
-            }
-            UOTK_CUDA(cudaEventRecord(e1, ps));
-            UOTK_CUDA(cudaStreamWaitEvent(cs, e1, 0));
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-            return;
-        }
+        const bool graphable = comm == nullptr && iters >= 4 && n >= 0 && m >= 0 && n + m <= kGraphMaxPoints;
+        on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
+            uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, st);
+        });
+        return;
         uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, cs);
     });
 }
@@ -513,6 +625,25 @@ int uotk_mmd2(int d, int64_t n, const double* x, const double* a, int64_t m, con
               void* cuda_stream) {
     return guarded([&] {
         mmd2_impl(d, n, x, a, m, y, b, kind, param, mmd2, opts, info, comm, (cudaStream_t)cuda_stream);
+    });
+}
+
+int uotk_uot_cstar(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
+                   double eps, double lam1, double lam2, double* cstar, void* comm, void* cuda_stream) {
+    return guarded([&] { cstar_impl(d, n, x, a, m, y, b, eps, lam1, lam2, cstar, comm, (cudaStream_t)cuda_stream); });
+}
+
+int uotk_sinkhorn_divergence(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
+                             const double* b, double eps, double lam1, double lam2, int iters, double* sd,
+                             double* terms, const uotk_opts* opts, void* comm, void* cuda_stream) {
+    return guarded([&] {
+        need(n >= 1 && m >= 1, "n and m must be >= 1");
+        need(iters >= 0, "iters must be >= 0");
+        cudaStream_t cs = (cudaStream_t)cuda_stream;
+        const bool graphable = comm == nullptr && iters >= 4 && 2 * std::max(n, m) <= kGraphMaxPoints;
+        on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
+            sd_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, sd, terms, opts, comm, st);
+        });
     });
 }
 

@@ -85,9 +85,32 @@ __global__ void signed_concat_k(const double* __restrict__ a, int64_t n, const d
     else if (i < n + m) w[i] = -b[i - n];
 }
 
+// moment columns of one weighted point set (row-major n x d), around a centre c:
+//   col 0: a_i   col 1: a_i ||x_i - c||^2   col 2 + t: a_i (x_it - c_t)
+__global__ void moment_cols_k(const double* __restrict__ x, const double* __restrict__ a, int64_t n, int d,
+                              const double* __restrict__ c, double* __restrict__ cols) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double ai = a[i];
+    double r2 = 0.0;
+    for (int t = 0; t < d; ++t) {
+        const double v = x[i * d + t] - (c ? c[t] : 0.0);
+        r2 = fma(v, v, r2);
+        cols[(2 + t) * n + i] = ai * v;
+    }
+    cols[i] = ai;
+    cols[n + i] = ai * r2;
+}
+
 inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
 
 }  // namespace
+
+void moment_cols(const double* x, const double* a, int64_t n, int d, const double* c, double* cols, cudaStream_t s) {
+    if (n == 0) return;
+    moment_cols_k<<<blocks_for(n, 256), 256, 0, s>>>(x, a, n, d, c, cols);
+    UOTK_LAUNCHED();
+}
 
 void sum_columns(const double* vals, int64_t n, int ncols, double* out_dev, cudaStream_t s) {
     DevBuf<double> part((size_t)ncols * kRBlocks, s);

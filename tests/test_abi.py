@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.uotk_abi_version() == 1
+    assert lib.uotk_abi_version() == 2
 
 
 def test_struct_layout_matches_c(tmp_path):
@@ -97,3 +97,17 @@ def test_dtype_and_shape_checks():
         uk.kernel_sum(np.zeros((3, 2), np.float32), np.ones(3), np.zeros((3, 2)), "gauss", 0.1)
     with pytest.raises(ValueError):
         uk.kernel_sum(np.zeros((3, 2)), np.ones(4), np.zeros((3, 2)), "gauss", 0.1)
+
+
+def test_solver_variant_argument_errors():
+    import paper_2306_13618_b200 as uk
+    x = np.zeros((4, 2))
+    with pytest.raises(uk.UotkError) as e:
+        uk.uot_cstar(x, np.ones(4), x, np.ones(4), 0.0, 1.0)
+    assert e.value.code == -1
+    with pytest.raises(uk.UotkError) as e:
+        uk.uot_sinkhorn(x, np.ones(4), x, np.ones(4), 0.1, 1.0, iters=3, opts={"stop_tol": -1.0})
+    assert e.value.code == -1
+    with pytest.raises(uk.UotkError) as e:
+        uk.sinkhorn_divergence(x[:0], np.ones(0), x, np.ones(4), 0.1, 1.0)
+    assert e.value.code == -1

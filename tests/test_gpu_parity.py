@@ -439,3 +439,61 @@ def test_uot_small_graph_replay_on_user_stream(uk, method):
         _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
         beta2, gamma2, res2 = uk.uot_sinkhorn(*args, iters=iters, opts={"method": method})
         _uot_check(res2, beta2.cpu().numpy(), gamma2.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ solver variants
+@pytest.mark.parametrize("d", [2, 3])
+def test_uot_cstar_matches_oracle(uk, d):
+    """c* of Eq. (2.10): the library's centred moment formula against the oracle's
+    pairwise definition of <mu x nu | d^2>; points far from the origin (shifted by 5)
+    to exercise the centring."""
+    rng = np.random.default_rng(50 + d)
+    x = W.uniform_ball(rng, 3001, d, 0.2) + 5.0
+    y = W.uniform_ball(rng, 2003, d, 0.2) + 5.05
+    a = rng.uniform(0.5, 1.5, 3001)
+    b = rng.uniform(0.2, 2.0, 2003)
+    for (e1, e2) in ((1.0, 1.0), (0.3, 2.5)):
+        ref = oracle.cstar(x, a, y, b, 0.05, e1, e2)
+        got = uk.uot_cstar(cuda(x), cuda(a), cuda(y), cuda(b), 0.05, e1, e2)
+        assert abs(got - ref) <= 1e-12 * ref, (got, ref)
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_gamma_init_cstar(uk, method):
+    """Remark 5.2: gamma^0 = c* 1, against the oracle started from the same gamma^0."""
+    pr = W.c1_uot(n=600, m=500)
+    c = oracle.cstar(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, 20, gamma0=np.full(500, c))
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=20,
+                                       gamma_init="cstar", opts={"method": method})
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_stopping_rule(uk, method):
+    """Tolerance stopping (reading R20): same stopping iteration as the oracle (the
+    tolerance sits 12-45% away from the sup-norm changes at the neighbouring checks,
+    far beyond rounding), same result."""
+    pr = W.c1_uot(n=300, m=250)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, iters=400, stop_tol=1e-9,
+                                     check_every=5)
+    assert ref.iters == 175
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=400,
+                                       opts={"method": method, "stop_tol": 1e-9, "check_every": 5})
+    assert res.iters == ref.iters
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    assert res.max_dbeta <= 1e-9 and res.max_dgamma <= 1e-9
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_sinkhorn_divergence_matches_oracle(uk, method):
+    """Eq. (2.12) from three UOT solves, against the oracle; the tolerance is relative
+    to the largest UOT term (sd itself is a cancellation of the three)."""
+    pr = W.c1_uot(n=400, m=300)
+    ref, terms = oracle.sinkhorn_divergence_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, iters=30)
+    sd, got_terms = uk.sinkhorn_divergence(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=30,
+                                           opts={"method": method}, return_terms=True)
+    scale = max(abs(t) for t in terms)
+    assert abs(sd - ref) <= 1e-8 * scale, (sd, ref)
+    for g_, r_ in zip(got_terms, terms):
+        assert abs(g_ - r_) <= 1e-8 * abs(r_)
