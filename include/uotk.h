@@ -207,6 +207,21 @@ int uotk_sinkhorn_divergence(int d, int64_t n, const double* x, const double* a,
                              double* sd, double* terms, const uotk_opts* opts,
                              void* comm, void* cuda_stream);
 
+/*
+ * lambda-scaling (Sec. 5.1.3): uotk_uot_sinkhorn solved for each entropy
+ * parameter eps_list[0..n_eps-1] in turn (decreasing eps = increasing lambda = 1/eps),
+ * each stage warm-started from the previous stage's gamma (the first from gamma_init,
+ * or 0).  Every stage runs `iters` iterations (or fewer with opts->stop_tol).  Outputs
+ * and res are those of the last stage, except res->iters = the total over all stages.
+ * eps_list: host array of n_eps >= 1 positive values.
+ */
+int uotk_uot_sinkhorn_scaling(int d, int64_t n, const double* x, const double* a,
+                              int64_t m, const double* y, const double* b,
+                              const double* eps_list, int n_eps, double lam1, double lam2,
+                              int iters, const double* gamma_init, double* beta, double* gamma,
+                              uotk_uot_result* res, const uotk_opts* opts,
+                              void* comm, void* cuda_stream);
+
 /* Multi-GPU communicator (one process per GPU).  uotk_comm_unique_id fills 128
  * bytes on one rank; broadcast them (e.g. with torch.distributed) and call
  * uotk_comm_create on every rank with the current CUDA device set.  NCCL is

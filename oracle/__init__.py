@@ -17,8 +17,8 @@ What is computed, and where it comes from (``P:n`` = line n of the paper text
                     with dense direct sums, the plan recovery of P:488, the dual
                     (3.1) and the discrete primal.
                     Also the constant c* of Prop. 2.9 / Eq. (2.10), the
-                    Sinkhorn divergence of Eq. (2.12), and a tolerance stopping
-                    rule (reading R20).
+                    Sinkhorn divergence of Eq. (2.12), a tolerance stopping
+                    rule (reading R20) and lambda-scaling (Sec. 5.1.3).
 * ``mmd``         — the discrete MMD^2 of Eq. (3.5), V-statistic form.
 
 Every function is pinned by ``tests/test_oracle_pins.py`` against closed forms,
@@ -36,5 +36,6 @@ from .sinkhorn import (  # noqa: F401
     SinkhornResult,
     cstar,
     sinkhorn_divergence_direct,
+    uot_sinkhorn_scaling_direct,
 )
 from .mmd import mmd2_direct, mmd2_combined  # noqa: F401

@@ -240,3 +240,20 @@ def sinkhorn_divergence_direct(x, mu, y, nu, eps, eta1, eta2=None, iters=100):
     ma, mb = float(np.sum(mu)), float(np.sum(nu))
     sd = rxy.primal - 0.5 * rxx.primal - 0.5 * ryy.primal + 0.5 * eps * (ma - mb) ** 2
     return sd, (rxy.primal, rxx.primal, ryy.primal)
+
+
+def uot_sinkhorn_scaling_direct(x, mu, y, nu, eps_list, eta1, eta2=None, iters=100, stop_tol=0.0, check_every=10):
+    """lambda-scaling (Sec. 5.1.3): Algorithm 1 solved for the entropy
+    parameters lambda = 1/eps in the order given (eps decreasing = lambda increasing),
+    each stage started from the previous stage's gamma (stage 1 from gamma^0 = 0).
+    Returns the last stage's SinkhornResult with `iters` = the total iteration count."""
+    gamma0 = None
+    total = 0
+    r = None
+    for eps in eps_list:
+        r = uot_sinkhorn_direct(x, mu, y, nu, eps, eta1, eta2, iters, gamma0=gamma0, stop_tol=stop_tol,
+                                check_every=check_every)
+        total += r.iters
+        gamma0 = r.gamma
+    r.iters = total
+    return r

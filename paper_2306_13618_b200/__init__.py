@@ -27,7 +27,7 @@ FLAG_GENERIC, FLAG_CHUNKED = 1, 2  # opts["flags"]: kernel family of the NFFT pa
 _KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, GAUSS: GAUSS, IMQ: IMQ}
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 
-__all__ = ["kernel_sum", "uot_sinkhorn", "mmd2", "uot_cstar", "sinkhorn_divergence", "Comm", "UOTResult", "GAUSS",
+__all__ = ["kernel_sum", "uot_sinkhorn", "uot_sinkhorn_scaling", "mmd2", "uot_cstar", "sinkhorn_divergence", "Comm", "UOTResult", "GAUSS",
            "IMQ", "UotkError",
            "launch_counter", "reset_launch_counter", "library_path"]
 
@@ -192,6 +192,34 @@ def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, op
     code = lib.uotk_uot_sinkhorn(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam), float(lam2),
                                  int(iters), G0.ptr if G0 else None, BO.ptr, GO.ptr, ctypes.byref(res),
                                  ctypes.byref(o), _comm_ptr(comm), _stream(stream, [X, A, Y, B, BO, GO]))
+    _native.check(code)
+    r = UOTResult(res.primal, res.dual, res.plan_mass, res.mass_a, res.mass_b, res.max_dbeta, res.max_dgamma,
+                  res.iters, _info_dict(res.info))
+    return BO.obj, GO.obj, r
+
+
+def uot_sinkhorn_scaling(x, a, y, b, eps_list, lam, lam2=None, iters=100, gamma_init=None, opts=None, comm=None,
+                         stream=None):
+    """lambda-scaling (Sec. 5.1.3): uot_sinkhorn for each eps in eps_list (decreasing),
+    each stage warm-started from the previous gamma.  Returns (beta, gamma, UOTResult) of
+    the last stage; UOTResult.iters is the total over the stages."""
+    lib = _native.load()
+    d = _dim(x, "x")
+    X, A, Y, B = _Arr(x, "x", d), _Arr(a, "a"), _Arr(y, "y", d), _Arr(b, "b")
+    if A.shape != (X.n,) or B.shape != (Y.n,):
+        raise ValueError("masses must match the point counts")
+    G0 = _Arr(gamma_init, "gamma_init") if gamma_init is not None else None
+    eps_arr = np.ascontiguousarray(np.asarray(eps_list, dtype=np.float64))
+    beta = _like(X, X.n)
+    gamma = _like(Y, Y.n)
+    BO, GO = _Arr(beta, "beta"), _Arr(gamma, "gamma")
+    res = UotkUotResult()
+    o = _opts(opts)
+    lam2 = lam if lam2 is None else lam2
+    code = lib.uotk_uot_sinkhorn_scaling(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, eps_arr.ctypes.data, len(eps_arr),
+                                         float(lam), float(lam2), int(iters), G0.ptr if G0 else None, BO.ptr, GO.ptr,
+                                         ctypes.byref(res), ctypes.byref(o), _comm_ptr(comm),
+                                         _stream(stream, [X, A, Y, B, BO, GO]))
     _native.check(code)
     r = UOTResult(res.primal, res.dual, res.plan_mass, res.mass_a, res.mass_b, res.max_dbeta, res.max_dgamma,
                   res.iters, _info_dict(res.info))

@@ -647,6 +647,44 @@ int uotk_sinkhorn_divergence(int d, int64_t n, const double* x, const double* a,
     });
 }
 
+int uotk_uot_sinkhorn_scaling(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
+                              const double* b, const double* eps_list, int n_eps, double lam1, double lam2, int iters,
+                              const double* gamma_init, double* beta, double* gamma, uotk_uot_result* res,
+                              const uotk_opts* opts, void* comm, void* cuda_stream) {
+    return guarded([&] {
+        need(eps_list != nullptr && n_eps >= 1, "eps_list must hold n_eps >= 1 values");
+        for (int k = 0; k < n_eps; ++k) need(eps_list[k] > 0 && std::isfinite(eps_list[k]), "eps_list: eps > 0");
+        need(n >= 1 && m >= 1 && beta && gamma, "n, m >= 1 and beta, gamma required");
+        cudaStream_t cs = (cudaStream_t)cuda_stream;
+        const bool graphable = comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints;
+        on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
+            // the previous stage's gamma (device, caller order) warm-starts the next stage
+            DevBuf<double> g0(m, st), bt(n, st);
+            const double* init = gamma_init;
+            int total = 0;
+            uotk_uot_result r;
+            for (int k = 0; k < n_eps; ++k) {
+                const bool last = k == n_eps - 1;
+                double* gout = last ? gamma : g0.p;
+                double* bout = last ? beta : bt.p;
+                if (!last && init == g0.p) {  // gamma_in and gamma_out must not alias
+                    DevBuf<double> tmp(m, st);
+                    UOTK_CUDA(cudaMemcpyAsync(tmp.p, g0.p, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                    uot_impl(d, n, x, a, m, y, b, eps_list[k], lam1, lam2, iters, tmp.p, bout, gout, &r, opts, comm,
+                             st);
+                } else {
+                    uot_impl(d, n, x, a, m, y, b, eps_list[k], lam1, lam2, iters, init, bout, gout, &r, opts, comm,
+                             st);
+                }
+                total += r.iters;
+                init = g0.p;
+            }
+            r.iters = total;
+            if (res) *res = r;
+        });
+    });
+}
+
 int uotk_comm_unique_id(void* id128) {
     return guarded([&] {
         if (!id128) fail(UOTK_EINVAL, "null id buffer");

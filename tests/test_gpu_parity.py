@@ -497,3 +497,16 @@ def test_sinkhorn_divergence_matches_oracle(uk, method):
     assert abs(sd - ref) <= 1e-8 * scale, (sd, ref)
     for g_, r_ in zip(got_terms, terms):
         assert abs(g_ - r_) <= 1e-8 * abs(r_)
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_lambda_scaling(uk, method):
+    """lambda-scaling (Sec. 5.1.3): three stages eps = 0.2, 0.1, 0.05, each warm-started
+    from the previous gamma, against the oracle's stage loop."""
+    pr = W.c1_uot(n=500, m=450)
+    eps_list = [0.2, 0.1, 0.05]
+    ref = oracle.uot_sinkhorn_scaling_direct(pr.x, pr.a, pr.y, pr.b, eps_list, pr.lam, iters=15)
+    beta, gamma, res = uk.uot_sinkhorn_scaling(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), eps_list, pr.lam,
+                                               iters=15, opts={"method": method})
+    assert res.iters == 45 == ref.iters
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)

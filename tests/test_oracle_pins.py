@@ -402,3 +402,21 @@ def test_stopping_rule():
     assert prev.max_dbeta > 1e-9 or prev.max_dgamma > 1e-9
     fixed = oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, 1.0, iters=r.iters)
     np.testing.assert_array_equal(fixed.beta, r.beta)
+
+
+def test_lambda_scaling_converges_to_the_unique_dual_maximiser():
+    """lambda-scaling (Sec. 5.1.3) warm-starts each stage; run to convergence, the last
+    stage reaches the same (unique, Thm. 3.1) potentials as a cold start at the
+    final eps — pins the stage ordering and the warm-start plumbing."""
+    rng = np.random.default_rng(15)
+    x = uniform_ball(rng, 14, 2, 0.2)
+    y = uniform_ball(rng, 12, 2, 0.2)
+    mu = rng.uniform(0.5, 1.5, 14)
+    nu = rng.uniform(0.2, 2.0, 12)
+    r = oracle.uot_sinkhorn_scaling_direct(x, mu, y, nu, [0.2, 0.1, 0.05], 1.0, iters=2000, stop_tol=1e-13,
+                                           check_every=10)
+    cold = oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, iters=2000, stop_tol=1e-13, check_every=10)
+    np.testing.assert_allclose(r.gamma, cold.gamma, atol=1e-11)
+    np.testing.assert_allclose(r.primal, cold.primal, rtol=1e-11)
+    single = oracle.uot_sinkhorn_scaling_direct(x, mu, y, nu, [0.05], 1.0, iters=30)
+    np.testing.assert_array_equal(single.gamma, oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, iters=30).gamma)
