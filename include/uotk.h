@@ -65,7 +65,9 @@ enum {
 /* Radial kernels of Eq. (4.2), P:560 (Table 1), as functions of r = ||x - y||:
  *   UOTK_GAUSS: k(r) = exp(-r^2 / param)          (param = l^2 = eps in the configs' form)
  *   UOTK_IMQ:   k(r) = 1 / sqrt(r^2 + param^2)    (param = c)                            */
-typedef enum { UOTK_GAUSS = 0, UOTK_IMQ = 1 } uotk_kernel_kind;
+typedef enum { UOTK_GAUSS = 0, UOTK_IMQ = 1, UOTK_GAUSS_R2 = 2 } uotk_kernel_kind;
+/*   UOTK_GAUSS_R2: k(r) = r^2 exp(-r^2 / param)  (kernel sums only: the transport-cost
+ *                  kernel of the Gibbs plan, d^2 k_ij, giving <pi, d^2> of P:462)    */
 
 /* Evaluation method.  AUTO picks DIRECT when n_src * n_tgt is below a measured
  * crossover and NFFT otherwise. */
@@ -101,6 +103,7 @@ typedef struct {
  * generic thread-per-point kernels.  At most one of the two bits may be set. */
 #define UOTK_FLAG_GENERIC 1  /* always the generic thread-per-point kernels          */
 #define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m must be 8)     */
+#define UOTK_FLAG_TRANSPORT 4 /* uot: also evaluate the transport term <pi, d^2>    */
 
 /* What a call actually used (any pointer to it may be NULL). */
 typedef struct {
@@ -130,6 +133,8 @@ typedef struct {
     int32_t iters;
     int32_t reserved;
     uotk_info info;
+    double transport;   /* <pi, d^2> = sum_ij pi_ij ||x_i - y_j||^2 with
+                           UOTK_FLAG_TRANSPORT, else NaN */
 } uotk_uot_result;
 
 /* Fill *opts with the defaults (all automatic). */
@@ -179,6 +184,19 @@ int uotk_mmd2(int d, int64_t n, const double* x, const double* a,
               int64_t m, const double* y, const double* b, int kind, double param,
               double* mmd2, const uotk_opts* opts, uotk_info* info,
               void* comm, void* cuda_stream);
+
+/*
+ * uotk_uot_sinkhorn plus the marginals of the recovered plan pi, in caller order:
+ *   p_i = sum_j pi_ij (n values),  q_j = sum_i pi_ij (m values)  (device or host; either
+ *   may be NULL).  With opts->flags & UOTK_FLAG_TRANSPORT, res->transport = <pi, d^2>,
+ *   one extra kernel sum with k(r) = r^2 exp(-r^2/eps) (UOTK_GAUSS_R2).
+ */
+int uotk_uot_sinkhorn_ex(int d, int64_t n, const double* x, const double* a,
+                         int64_t m, const double* y, const double* b,
+                         double eps, double lam1, double lam2, int iters,
+                         const double* gamma_init, double* beta, double* gamma,
+                         double* p, double* q, uotk_uot_result* res, const uotk_opts* opts,
+                         void* comm, void* cuda_stream);
 
 /*
  * The constant c* of Prop. 2.9, Eq. (2.10), r = 2, lambda = 1/eps:

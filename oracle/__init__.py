@@ -10,7 +10,8 @@ What is computed, and where it comes from (``P:n`` = line n of the paper text
 ``PAPER.md``; ``S:n`` = line n of ``SPEC.md``):
 
 * ``kernels``     — radial kernels K^Gauss, K^IMQ of Eq. (4.2) in the
-                    config form exp(-r^2/eps) and (r^2+c^2)^(-1/2).
+                    config form exp(-r^2/eps) and (r^2+c^2)^(-1/2); r^2 exp(-r^2/eps)
+                    (the transport-cost kernel d^2 k).
 * ``direct``      — the kernel sum (4.3) by its plain definition, an
                     O(n m) double loop vectorised over blocks of targets.
 * ``sinkhorn``    — Algorithm 1 step by step: updates (3.3)/(3.4)
@@ -18,7 +19,8 @@ What is computed, and where it comes from (``P:n`` = line n of the paper text
                     (3.1) and the discrete primal.
                     Also the constant c* of Prop. 2.9 / Eq. (2.10), the
                     Sinkhorn divergence of Eq. (2.12), a tolerance stopping
-                    rule (reading R20) and lambda-scaling (Sec. 5.1.3).
+                    rule (reading R20), lambda-scaling (Sec. 5.1.3), and the
+                    transport term <pi, d^2> of the recovered plan.
 * ``mmd``         — the discrete MMD^2 of Eq. (3.5), V-statistic form.
 
 Every function is pinned by ``tests/test_oracle_pins.py`` against closed forms,
@@ -26,7 +28,7 @@ brute force and invariants that do not reuse the oracle's own formulas (see
 DESIGN.md "Oracle pins").  No function here is "parity unpinned".
 """
 
-from .kernels import gauss, imq, kernel_fn  # noqa: F401
+from .kernels import gauss, gauss_r2, imq, kernel_fn  # noqa: F401
 from .direct import kernel_sum_direct  # noqa: F401
 from .sinkhorn import (  # noqa: F401
     uot_sinkhorn_direct,
@@ -37,5 +39,7 @@ from .sinkhorn import (  # noqa: F401
     cstar,
     sinkhorn_divergence_direct,
     uot_sinkhorn_scaling_direct,
+    plan_marginals,
+    transport_cost,
 )
 from .mmd import mmd2_direct, mmd2_combined  # noqa: F401

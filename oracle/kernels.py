@@ -9,6 +9,7 @@ import numpy as np
 
 GAUSS = 0
 IMQ = 1
+GAUSS_R2 = 2
 
 
 def gauss(r2, eps):
@@ -21,10 +22,18 @@ def imq(r2, c):
     return 1.0 / np.sqrt(np.asarray(r2, dtype=np.float64) + c * c)
 
 
+def gauss_r2(r2, eps):
+    """r^2 exp(-r^2/eps): the transport-cost kernel d^2 k of the Gibbs plan."""
+    r2 = np.asarray(r2, dtype=np.float64)
+    return r2 * np.exp(-r2 / eps)
+
+
 def kernel_fn(kind, param):
     """Return K as a function of the squared distance."""
     if kind == GAUSS:
         return lambda r2: gauss(r2, param)
     if kind == IMQ:
         return lambda r2: imq(r2, param)
+    if kind == GAUSS_R2:
+        return lambda r2: gauss_r2(r2, param)
     raise ValueError(f"unknown kernel kind {kind!r}")

@@ -257,3 +257,20 @@ def uot_sinkhorn_scaling_direct(x, mu, y, nu, eps_list, eta1, eta2=None, iters=1
         gamma0 = r.gamma
     r.iters = total
     return r
+
+
+def transport_cost(x, mu, y, nu, beta, gamma, eps):
+    """<pi, d^2> = sum_ij pi_ij ||x_i - x~_j||^2 for the plan of P:488,
+    pi_ij = mu_i e^{lam beta_i} k_ij e^{lam gamma_j} nu_j, summed by its definition
+    (rows of the dense plan in blocks)."""
+    lam = 1.0 / eps
+    x = np.asarray(x, dtype=np.float64).reshape(len(mu), -1)
+    y = np.asarray(y, dtype=np.float64).reshape(len(nu), -1)
+    u = np.asarray(mu) * np.exp(lam * np.asarray(beta))
+    v = np.asarray(nu) * np.exp(lam * np.asarray(gamma))
+    total = 0.0
+    for i0 in range(0, len(mu), 256):
+        d2 = np.sum((x[i0:i0 + 256, None, :] - y[None, :, :]) ** 2, axis=2)
+        pi = u[i0:i0 + 256, None] * gauss(d2, eps) * v[None, :]
+        total += float(np.sum(pi * d2))
+    return total

@@ -22,9 +22,12 @@ from ._native import UotkError, UotkOpts, UotkInfo, UotkUotResult  # noqa: F401
 
 GAUSS = 0
 IMQ = 1
+GAUSS_R2 = 2  # k(r) = r^2 exp(-r^2/param): kernel sums only (transport-cost kernel)
 AUTO, NFFT, DIRECT = 0, 1, 2
 FLAG_GENERIC, FLAG_CHUNKED = 1, 2  # opts["flags"]: kernel family of the NFFT passes (uotk.h)
-_KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, GAUSS: GAUSS, IMQ: IMQ}
+_KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, "gauss_r2": GAUSS_R2, GAUSS: GAUSS, IMQ: IMQ,
+         GAUSS_R2: GAUSS_R2}
+FLAG_TRANSPORT = 4
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 
 __all__ = ["kernel_sum", "uot_sinkhorn", "uot_sinkhorn_scaling", "mmd2", "uot_cstar", "sinkhorn_divergence", "Comm", "UOTResult", "GAUSS",
@@ -159,6 +162,9 @@ class UOTResult:
     max_dgamma: float
     iters: int
     info: dict
+    transport: float = float("nan")  # <pi, d^2> (uot_sinkhorn(..., transport=True))
+    p: object = None                 # plan marginals (uot_sinkhorn(..., marginals=True))
+    q: object = None
 
     @property
     def uot_cost(self):
@@ -166,7 +172,8 @@ class UOTResult:
         return self.primal
 
 
-def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, opts=None, comm=None, stream=None):
+def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, opts=None, comm=None, stream=None,
+                 marginals=False, transport=False):
     """Entropic UOT (Def. 2.7) by Algorithm 2: Gaussian Gibbs kernel exp(-|x-y|^2/eps),
     eps = 1/lambda_paper, marginal penalties lam (= eta_1) and lam2 (= eta_2, default lam).
     Returns (beta, gamma, UOTResult)."""
@@ -189,12 +196,23 @@ def uot_sinkhorn(x, a, y, b, eps, lam, lam2=None, iters=100, gamma_init=None, op
     res = UotkUotResult()
     o = _opts(opts)
     lam2 = lam if lam2 is None else lam2
-    code = lib.uotk_uot_sinkhorn(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam), float(lam2),
-                                 int(iters), G0.ptr if G0 else None, BO.ptr, GO.ptr, ctypes.byref(res),
-                                 ctypes.byref(o), _comm_ptr(comm), _stream(stream, [X, A, Y, B, BO, GO]))
+    if marginals or transport:
+        if transport:
+            o.flags |= FLAG_TRANSPORT
+        PO = _Arr(_like(X, X.n), "p") if marginals else None
+        QO = _Arr(_like(Y, Y.n), "q") if marginals else None
+        code = lib.uotk_uot_sinkhorn_ex(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam), float(lam2),
+                                        int(iters), G0.ptr if G0 else None, BO.ptr, GO.ptr,
+                                        PO.ptr if PO else None, QO.ptr if QO else None, ctypes.byref(res),
+                                        ctypes.byref(o), _comm_ptr(comm), _stream(stream, [X, A, Y, B, BO, GO]))
+    else:
+        PO = QO = None
+        code = lib.uotk_uot_sinkhorn(d, X.n, X.ptr, A.ptr, Y.n, Y.ptr, B.ptr, float(eps), float(lam), float(lam2),
+                                     int(iters), G0.ptr if G0 else None, BO.ptr, GO.ptr, ctypes.byref(res),
+                                     ctypes.byref(o), _comm_ptr(comm), _stream(stream, [X, A, Y, B, BO, GO]))
     _native.check(code)
     r = UOTResult(res.primal, res.dual, res.plan_mass, res.mass_a, res.mass_b, res.max_dbeta, res.max_dgamma,
-                  res.iters, _info_dict(res.info))
+                  res.iters, _info_dict(res.info), res.transport, PO.obj if PO else None, QO.obj if QO else None)
     return BO.obj, GO.obj, r
 
 
@@ -222,7 +240,7 @@ def uot_sinkhorn_scaling(x, a, y, b, eps_list, lam, lam2=None, iters=100, gamma_
                                          _stream(stream, [X, A, Y, B, BO, GO]))
     _native.check(code)
     r = UOTResult(res.primal, res.dual, res.plan_mass, res.mass_a, res.mass_b, res.max_dbeta, res.max_dgamma,
-                  res.iters, _info_dict(res.info))
+                  res.iters, _info_dict(res.info), res.transport)
     return BO.obj, GO.obj, r
 
 

@@ -20,7 +20,7 @@ STATUS = {
 # every symbol include/uotk.h declares (tests check the library exports all of them)
 EXPORTED = (
     "uotk_opts_init", "uotk_kernel_sum", "uotk_uot_sinkhorn", "uotk_mmd2",
-    "uotk_uot_cstar", "uotk_sinkhorn_divergence", "uotk_uot_sinkhorn_scaling",
+    "uotk_uot_cstar", "uotk_sinkhorn_divergence", "uotk_uot_sinkhorn_scaling", "uotk_uot_sinkhorn_ex",
     "uotk_comm_unique_id", "uotk_comm_create", "uotk_comm_destroy",
     "uotk_last_error", "uotk_abi_version", "uotk_launch_counter", "uotk_launch_counter_reset",
     "uotk_profile_enable", "uotk_profile_reset", "uotk_profile_read",
@@ -49,7 +49,7 @@ class UotkUotResult(ctypes.Structure):
         ("primal", ctypes.c_double), ("dual", ctypes.c_double), ("plan_mass", ctypes.c_double),
         ("mass_a", ctypes.c_double), ("mass_b", ctypes.c_double), ("max_dbeta", ctypes.c_double),
         ("max_dgamma", ctypes.c_double), ("iters", ctypes.c_int32), ("reserved", ctypes.c_int32),
-        ("info", UotkInfo),
+        ("info", UotkInfo), ("transport", ctypes.c_double),
     ]
 
 
@@ -93,6 +93,9 @@ def load():
     lib.uotk_sinkhorn_divergence.argtypes = [INT, I64, P, P, I64, P, P, D, D, D, INT, ctypes.POINTER(D), P,
                                              ctypes.POINTER(UotkOpts), P, P]
     lib.uotk_sinkhorn_divergence.restype = INT
+    lib.uotk_uot_sinkhorn_ex.argtypes = [INT, I64, P, P, I64, P, P, D, D, D, INT, P, P, P, P, P,
+                                         ctypes.POINTER(UotkUotResult), ctypes.POINTER(UotkOpts), P, P]
+    lib.uotk_uot_sinkhorn_ex.restype = INT
     lib.uotk_uot_sinkhorn_scaling.argtypes = [INT, I64, P, P, I64, P, P, P, INT, D, D, INT, P, P, P,
                                               ctypes.POINTER(UotkUotResult), ctypes.POINTER(UotkOpts), P, P]
     lib.uotk_uot_sinkhorn_scaling.restype = INT

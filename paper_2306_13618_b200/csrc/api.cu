@@ -55,7 +55,7 @@ uotk_opts resolve(const uotk_opts* o) {
     uotk_opts r;
     memset(&r, 0, sizeof r);
     if (o) r = *o;
-    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED)) != 0 || r.reserved != 0)
+    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED | UOTK_FLAG_TRANSPORT)) != 0 || r.reserved != 0)
         fail(UOTK_EINVAL, "unknown opts.flags bits, or opts.reserved != 0");
     if ((r.flags & UOTK_FLAG_GENERIC) && (r.flags & UOTK_FLAG_CHUNKED))
         fail(UOTK_EINVAL, "opts.flags: UOTK_FLAG_GENERIC and UOTK_FLAG_CHUNKED are exclusive");
@@ -199,7 +199,7 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
                             const double* tgt, int kind, double param, double* out, const uotk_opts* opts_in,
                             uotk_info* info, void* comm, cudaStream_t s) {
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
-    need(kind == UOTK_GAUSS || kind == UOTK_IMQ, "unknown kernel kind");
+    need(kind == UOTK_GAUSS || kind == UOTK_IMQ || kind == UOTK_GAUSS_R2, "unknown kernel kind");
     need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");
     check_points_arg(d, n_src, src, "src");
     check_points_arg(d, n_src, alpha, "alpha");
@@ -245,7 +245,8 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
 // ============================================================== UOT Sinkhorn
 static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
                      double eps, double lam1, double lam2, int iters, const double* gamma_init, double* beta_out,
-                     double* gamma_out, uotk_uot_result* res, const uotk_opts* opts_in, void* comm, cudaStream_t s) {
+                     double* gamma_out, uotk_uot_result* res, const uotk_opts* opts_in, void* comm, cudaStream_t s,
+                     double* p_out = nullptr, double* q_out = nullptr) {
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
     need(n >= 1 && m >= 1, "n and m must be >= 1");
     need(x && a && y && b && beta_out && gamma_out, "null pointer argument");
@@ -260,9 +261,12 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     Y.bind(y, (size_t)m * d, s);
     B.bind(b, (size_t)m, s);
     if (gamma_init) G0.bind(gamma_init, (size_t)m, s);
-    OutArr BO, GO;
+    OutArr BO, GO, PO, QO;
     BO.bind(beta_out, (size_t)n, s);
     GO.bind(gamma_out, (size_t)m, s);
+    if (p_out) PO.bind(p_out, (size_t)n, s);
+    if (q_out) QO.bind(q_out, (size_t)m, s);
+    const bool want_transport = (o.flags & UOTK_FLAG_TRANSPORT) != 0;
 
     const double lam = 1.0 / eps;                 // paper lambda (Def. 2.7)
     const double c1 = lam1 / (1.0 + lam1 * lam);  // (3.3): beta = -c1 log t
@@ -278,6 +282,8 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     const int method = pick_method(o, (double)n * (double)m, comm);
     // per-point state: potentials, masses, next weights, t at x (final) and t~ at y (last)
     DevBuf<double> pot_x(n, s), pot_y(m, s), mass_x(n, s), mass_y(m, s), wx(n, s), wy(m, s), tx(n, s), ty(m, s);
+    DevBuf<double> tpx;  // t' at x for the transport term
+    if (want_transport) tpx.alloc(n, s);
     pot_x.zero();
     const int32_t* perm_x = nullptr;
     const int32_t* perm_y = nullptr;
@@ -330,6 +336,9 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p);
         // marginals of the recovered plan: t at x from the final gamma
         direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, EpiStore{tx.p, nullptr}, nullptr, s);
+        // <pi, d^2>: t' at x with the kernel d^2 k (UOTK_GAUSS_R2) against the same weights
+        if (want_transport) direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS_R2, eps, EpiStore{tpx.p, nullptr},
+                                           nullptr, s);
         if (iters == 0) {
             scaled_mass(mass_x.p, pot_x.p, n, lam, wx.p, s);
             direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, EpiStore{ty.p, nullptr}, nullptr, s);
@@ -369,6 +378,17 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         };
         done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p);
         // grid holds the spread of nu (.) v with the final v: t at x for the marginals
+        if (want_transport) {
+            // the same spread grid through the D_k of the kernel d^2 k (same N, n_g, h)
+            DevBuf<double> gt(ge, s);
+            UOTK_CUDA(cudaMemcpyAsync(gt.p, grid.p, ge * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            SpectralPlan sp2;
+            sp2.fp = fp;
+            sp2.fp.kind = UOTK_GAUSS_R2;
+            build_spectral_plan(sp2, s);
+            const double* g2 = fft_chain(sp2, gt.p, spec.p, s, comm);
+            gather_epi(PX, g2, fp, EpiStore{tpx.p, nullptr}, nullptr, s);
+        }
         const double* gx = fft_chain(ns.sp, grid.p, spec.p, s, comm);
         gather_epi(PX, gx, fp, EpiStore{tx.p, nullptr}, nullptr, s);
         if (iters == 0) {
@@ -381,18 +401,34 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     }
 
     // objective terms and their global sums
-    DevBuf<double> cols(5 * (size_t)std::max(n, m), s), sums(12, s);
+    DevBuf<double> cols(5 * (size_t)std::max(n, m), s), sums(13, s);
+    sums.zero();
     uot_terms(pot_x.p, mass_x.p, tx.p, n, lam, lam1, cols.p, s);
     sum_columns(cols.p, n, 5, sums.p, s);
+    // column 0 now holds p (sorted order): export it
+    if (p_out) {
+        if (method == UOTK_DIRECT) UOTK_CUDA(cudaMemcpyAsync(PO.d, cols.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        else unpermute_values(PO.d, cols.p, perm_x, n, s);
+    }
+    if (want_transport) {
+        // <pi, d^2> = sum_i mu_i e^{lam beta_i} t'_i: reuse cols as (w_i t'_i)
+        uot_transport(pot_x.p, mass_x.p, tpx.p, n, lam, cols.p, s);
+        sum_columns(cols.p, n, 1, sums.p + 12, s);
+    }
     uot_terms(pot_y.p, mass_y.p, ty.p, m, lam, lam2, cols.p, s);
     sum_columns(cols.p, m, 5, sums.p + 5, s);
+    if (q_out) {
+        if (method == UOTK_DIRECT) UOTK_CUDA(cudaMemcpyAsync(QO.d, cols.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        else unpermute_values(QO.d, cols.p, perm_y, m, s);
+    }
     // dmax as doubles (non-negative: the bit patterns order like the values)
     UOTK_CUDA(cudaMemcpyAsync(sums.p + 10, dmax.p, 2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (comm) {
         comm_allreduce(sums.p, 10, 0, comm, s);
         comm_allreduce(sums.p + 10, 2, 1, comm, s);
+        comm_allreduce(sums.p + 12, 1, 0, comm, s);
     }
-    double hs[12];
+    double hs[13];
     UOTK_CUDA(cudaMemcpyAsync(hs, sums.p, sizeof hs, cudaMemcpyDeviceToHost, s));
     // potentials back to caller order
     if (method == UOTK_DIRECT) {
@@ -404,6 +440,8 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     }
     BO.flush();
     GO.flush();
+    if (p_out) PO.flush();
+    if (q_out) QO.flush();
     const int fl = read_flag(flag, s);  // synchronises the stream
     if (fl & 3) fail(UOTK_EOVERFLOW, "non-positive or non-finite kernel sum / scaling in the Sinkhorn loop");
 
@@ -423,6 +461,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         res->max_dgamma = hs[11];
         res->iters = done;
         fill_info(&res->info, method, fpp);
+        res->transport = want_transport ? hs[12] : std::nan("");
     }
 }
 
@@ -643,6 +682,20 @@ int uotk_sinkhorn_divergence(int d, int64_t n, const double* x, const double* a,
         const bool graphable = comm == nullptr && iters >= 4 && 2 * std::max(n, m) <= kGraphMaxPoints;
         on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
             sd_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, sd, terms, opts, comm, st);
+        });
+    });
+}
+
+int uotk_uot_sinkhorn_ex(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
+                         const double* b, double eps, double lam1, double lam2, int iters, const double* gamma_init,
+                         double* beta, double* gamma, double* p, double* q, uotk_uot_result* res,
+                         const uotk_opts* opts, void* comm, void* cuda_stream) {
+    return guarded([&] {
+        cudaStream_t cs = (cudaStream_t)cuda_stream;
+        const bool graphable = comm == nullptr && iters >= 4 && n >= 0 && m >= 0 && n + m <= kGraphMaxPoints;
+        on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
+            uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, st, p,
+                     q);
         });
     });
 }

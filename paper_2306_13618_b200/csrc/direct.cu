@@ -29,6 +29,17 @@ __device__ __forceinline__ double pair_sum_tile(const double (*sp)[kTile], const
             }
             acc = fma(exp(-r2 * inv_or_c2), sw[j], acc);
         }
+    } else if (kind == UOTK_GAUSS_R2) {
+#pragma unroll 4
+        for (int j = 0; j < cnt; ++j) {
+            double r2 = 0.0;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const double v = xi[t] - sp[t][j];
+                r2 = fma(v, v, r2);
+            }
+            acc = fma(r2 * exp(-r2 * inv_or_c2), sw[j], acc);
+        }
     } else {
 #pragma unroll 4
         for (int j = 0; j < cnt; ++j) {
@@ -110,7 +121,7 @@ void direct_sum_epi(int d, int64_t n_src, const double* src, const double* w, in
     int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(want, n_src / 64));
     if (nsplit > 65535) nsplit = 65535;
     const int64_t slice = n_src == 0 ? 1 : (n_src + nsplit - 1) / nsplit;
-    const double arg = kind == UOTK_GAUSS ? 1.0 / param : param * param;
+    const double arg = kind == UOTK_IMQ ? param * param : 1.0 / param;
     DevBuf<double> partial;
     if (nsplit > 1) partial.alloc((size_t)nsplit * n_tgt, s);
     dim3 grid((unsigned)tb, (unsigned)nsplit);

@@ -126,7 +126,7 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
 
     double Rbar_max;  // largest torus radius the points may occupy
     double h_min;
-    if (kind == UOTK_GAUSS) {
+    if (kind == UOTK_GAUSS || kind == UOTK_GAUSS_R2) {
         // pure periodisation: pair differences must stay inside the cell (|diff_t| < 1/2)
         Rbar_max = 0.24;
         const double h_decay = 2.0 * std::sqrt(param * L);  // K(h/2) <= tol K(0)
@@ -151,7 +151,7 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
 
     int N = o.N;
     if (N <= 0) {
-        if (kind == UOTK_GAUSS) {
+        if (kind == UOTK_GAUSS || kind == UOTK_GAUSS_R2) {
             const double eb = param / (h * h);  // kernel exp(-|y|^2/eb) in torus units
             N = (int)std::ceil(2.0 * std::sqrt(L / (M_PI * M_PI * eb)));
             N = nice_even(std::max(N, 8));
@@ -212,6 +212,8 @@ __global__ void sample_kernel_k(double* out, int N, KernelCoef kc) {
     double v;
     if (kc.kind == UOTK_GAUSS) {
         v = exp(-kc.h2 * r2 / kc.param);
+    } else if (kc.kind == UOTK_GAUSS_R2) {
+        v = kc.h2 * r2 * exp(-kc.h2 * r2 / kc.param);  // physical r^2 = h^2 r^2 (torus units)
     } else {
         double r = sqrt(r2);
         if (r <= kc.r0) {

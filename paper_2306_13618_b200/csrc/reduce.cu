@@ -102,9 +102,23 @@ __global__ void moment_cols_k(const double* __restrict__ x, const double* __rest
     cols[n + i] = ai * r2;
 }
 
+// w_i t'_i with w = mass e^{lam pot}: the summands of <pi, d^2> (t' = the d^2 k sum)
+__global__ void transport_k(const double* __restrict__ pot, const double* __restrict__ mass,
+                            const double* __restrict__ tp, int64_t n, double lam, double* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = mass[i] * exp(lam * pot[i]) * tp[i];
+}
+
 inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
 
 }  // namespace
+
+void uot_transport(const double* pot, const double* mass, const double* tp, int64_t n, double lam, double* out,
+                   cudaStream_t s) {
+    if (n == 0) return;
+    transport_k<<<blocks_for(n, 256), 256, 0, s>>>(pot, mass, tp, n, lam, out);
+    UOTK_LAUNCHED();
+}
 
 void moment_cols(const double* x, const double* a, int64_t n, int d, const double* c, double* cols, cudaStream_t s) {
     if (n == 0) return;

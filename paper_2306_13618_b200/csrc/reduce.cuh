@@ -8,6 +8,8 @@ namespace uotk {
 
 void uot_terms(const double* pot, const double* mass, const double* t, int64_t n, double lam, double eta,
                double* cols, cudaStream_t s);
+void uot_transport(const double* pot, const double* mass, const double* tp, int64_t n, double lam, double* out,
+                   cudaStream_t s);
 void check_mass(const double* a, int64_t n, int* flag, cudaStream_t s);
 void scaled_mass(const double* mass, const double* pot, int64_t n, double lam, double* w, cudaStream_t s);
 // cols (n x (2 + d), column-major): a, a ||x - c||^2, a (x - c)  (c: d device values or NULL)

@@ -420,3 +420,35 @@ def test_lambda_scaling_converges_to_the_unique_dual_maximiser():
     np.testing.assert_allclose(r.primal, cold.primal, rtol=1e-11)
     single = oracle.uot_sinkhorn_scaling_direct(x, mu, y, nu, [0.05], 1.0, iters=30)
     np.testing.assert_array_equal(single.gamma, oracle.uot_sinkhorn_direct(x, mu, y, nu, 0.05, 1.0, iters=30).gamma)
+
+
+# ------------------------------------------------------------------ transport term
+@pytest.mark.parametrize("eps", [0.05, 0.002])
+def test_kernel_sum_gauss_r2_line_integral(eps):
+    """Gauss-Legendre weights: sum_j (x-y_j)^2 exp(-(x-y_j)^2/eps) w_j ->
+    int y^2 exp(-y^2/eps) dy = sqrt(pi) eps^(3/2) / 2 (the Gaussian's second moment)."""
+    L = 40.0 * math.sqrt(eps)
+    t, w = np.polynomial.legendre.leggauss(400)
+    y = (L * t)[:, None]
+    s = oracle.kernel_sum_direct(y, L * w, np.array([[0.0], [0.3 * math.sqrt(eps)]]), 2, eps)
+    np.testing.assert_allclose(s, math.sqrt(math.pi) * eps ** 1.5 / 2.0, rtol=1e-12)
+
+
+def test_transport_cost_entropy_identity():
+    """For the recovered plan log(pi_ij / (mu_i nu_j)) = lam beta_i + lam gamma_j
+    - lam d_ij^2, so <pi, d^2> = sum beta p + sum gamma q - (1/lam) sum pi log(pi/(mu nu));
+    the right side is evaluated densely from an independently built plan."""
+    rng = np.random.default_rng(16)
+    x = uniform_ball(rng, 13, 2, 0.2)
+    y = uniform_ball(rng, 11, 2, 0.2)
+    mu = rng.uniform(0.5, 1.5, 13)
+    nu = rng.uniform(0.2, 2.0, 11)
+    eps = 0.05
+    r = oracle.uot_sinkhorn_direct(x, mu, y, nu, eps, 1.0, iters=40)
+    d2 = np.sum((x[:, None] - y[None]) ** 2, 2)
+    pi = np.outer(mu * np.exp(r.beta / eps), nu * np.exp(r.gamma / eps)) * np.exp(-d2 / eps)
+    ent = float(np.sum(pi * np.log(pi / np.outer(mu, nu))))
+    rhs = float(r.beta @ pi.sum(1) + r.gamma @ pi.sum(0)) - eps * ent
+    np.testing.assert_allclose(oracle.transport_cost(x, mu, y, nu, r.beta, r.gamma, eps), rhs, rtol=1e-10)
+    np.testing.assert_allclose(oracle.transport_cost(x, mu, y, nu, r.beta, r.gamma, eps), float(np.sum(pi * d2)),
+                               rtol=1e-13)

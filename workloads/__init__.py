@@ -21,6 +21,7 @@ import numpy as np
 
 GAUSS = 0
 IMQ = 1
+GAUSS_R2 = 2
 
 
 def uniform_ball(rng, n, d, radius):
