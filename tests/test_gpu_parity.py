@@ -510,3 +510,31 @@ def test_uot_lambda_scaling(uk, method):
                                                iters=15, opts={"method": method})
     assert res.iters == 45 == ref.iters
     _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ transport term and marginals (8(f) f4)
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_kernel_sum_gauss_r2(uk, method, d):
+    """The transport-cost kernel r^2 exp(-r^2/eps) (UOTK_GAUSS_R2) against the oracle."""
+    pr = W.random_sum(d, 3001, 1999, kind=W.GAUSS, param=0.02, seed=60 + d)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, 2, 0.02)
+    got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss_r2", 0.02, opts={"method": method})
+    assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+@pytest.mark.parametrize("d", [2, 3])
+def test_uot_transport_and_marginals(uk, method, d):
+    """<pi, d^2> and the plan marginals p, q (caller order) against the oracle."""
+    pr = W.c1_uot(n=800, m=700, d=d) if d == 2 else W.c3_uot(n=1200, m=1000, iters=20)
+    iters = 20
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, iters)
+    p_ref, q_ref = oracle.plan_marginals(pr.x, pr.a, pr.y, pr.b, ref.beta, ref.gamma, pr.eps)
+    t_ref = oracle.transport_cost(pr.x, pr.a, pr.y, pr.b, ref.beta, ref.gamma, pr.eps)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=iters,
+                                       opts={"method": method}, marginals=True, transport=True)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    assert rel_err(res.p.cpu().numpy(), p_ref, False) <= 1e-8
+    assert rel_err(res.q.cpu().numpy(), q_ref, False) <= 1e-8
+    assert abs(res.transport - t_ref) <= 1e-8 * abs(t_ref), (res.transport, t_ref)
