@@ -20,6 +20,8 @@
 // the chunk's block); t_p = sum_a X_p[a] F[a] in-lane, and the spread accumulates
 // w_p X_p[a] per lane, reduced across the warp by a transpose-reduction only when the
 // group is flushed.
+#include <cstdlib>
+
 #include "chunks.cuh"
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -251,6 +253,189 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     if (GATHER) warp_max_atomic(dmax, ddmax);
 }
 
+// ---------------------------------------------------------------- warp-specialised d = 2 half-step
+// One work unit = a warp pair: the G warp gathers chunk k (32 DMMAs), runs the Sinkhorn
+// update (3.3)/(3.4) and publishes the 32 new weights; the S warp spreads chunk k (32
+// DMMAs) from those weights while G already gathers chunk k+1.  The window ring (TMA,
+// refilled by S when it releases a slot) and the weight hand-off are per-unit mbarriers,
+// so the units of a CTA never synchronise with each other.
+struct __align__(128) Smem2WS {
+    double win[kWarps2][kRing2][kW2];
+    double w[kWarps2][2][kChunk];             // published weights, double-buffered
+    unsigned long long win_full[kWarps2][kRing2];
+    unsigned long long w_full[kWarps2][2];
+    unsigned long long w_empty[kWarps2][2];
+};
+
+__global__ void __launch_bounds__(2 * kWarps2 * 32, kCtas2)
+sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
+                int nunits, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
+                EpiSinkhorn epi, unsigned long long* dmax) {
+    using In = EpiSinkhorn::In;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem2WS& sm = *reinterpret_cast<Smem2WS*>(smem_raw);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const bool is_g = warp < kWarps2;
+    const int u = is_g ? warp : warp - kWarps2;  // unit within the CTA
+    const int gq = lane >> 2;
+    const int tq = lane & 3;
+    const int unit = blockIdx.x * kWarps2 + u;
+    if (unit >= nunits) return;  // both warps of the unit leave together
+    const int64_t cbeg = bounds[unit];
+    const int64_t nck = bounds[unit + 1] - cbeg;
+    if (nck <= 0) return;
+    double* swin = &sm.win[u][0][0];
+    unsigned long long* win_full = sm.win_full[u];
+    unsigned long long* w_full = sm.w_full[u];
+    unsigned long long* w_empty = sm.w_empty[u];
+    // the G warp initialises the unit's barriers; the S warp waits for it through the
+    // CTA barrier below (the only CTA-wide synchronisation, before any hand-off)
+    if (is_g && lane == 0) {
+        for (int r = 0; r < kRing2; ++r) mbar_init(&win_full[r], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&w_full[i], 32);
+            mbar_init(&w_empty[i], 1);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+    if (is_g && lane == 0) {
+        for (int k = 0; k < kRing2 && k < nck; ++k) {
+            mbar_expect_tx(&win_full[k], kW2Bytes);
+            bulk_g2s(swin + k * kW2, win + (cbeg + k) * kW2, kW2Bytes, &win_full[k]);
+        }
+    }
+    auto origin = [&](int32_t kk) -> int64_t { return (int64_t)(kk / ng - kM + 1) * ng + (kk % ng - kM + 1); };
+    DescBatch db;
+    db.init(desc, cbeg, cbeg + nck, lane);
+
+    if (is_g) {
+        double Fb[2][4];  // Fb[nt][ks] = F[4ks + tq][8nt + gq]
+        int32_t cur_key = -1;
+        double ddmax = 0.0;
+        int4 dsc = db.get(0, lane);
+        In in_cur{};
+        if (lane < dsc.y) in_cur = epi.load(dsc.x + lane);
+        for (int64_t k = 0; k < nck; ++k) {
+            const int slot = (int)(k % kRing2);
+            const int64_t p0 = dsc.x;
+            const int cnt = dsc.y;
+            const int4 dnext = db.peek_next(k);
+            In in_next{};
+            if (k + 1 < nck && lane < dnext.y) in_next = epi.load(dnext.x + lane);
+            if (dsc.z != cur_key) {
+                cur_key = dsc.z;
+                const int64_t org = origin(cur_key);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double* row = grid_in + org + (int64_t)(4 * ks + tq) * ng + gq;
+                    Fb[0][ks] = __ldg(row);
+                    Fb[1][ks] = __ldg(row + 8);
+                }
+            }
+            if (k + 1 < nck && dnext.z != cur_key && lane < 16)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(grid_in + origin(dnext.z) + (int64_t)lane * ng));
+            mbar_wait(&win_full[slot], (uint32_t)((k / kRing2) & 1));
+            const double* X = swin + slot * kW2;
+            const double* Y = X + kChunk * kChunkT;
+            double t = 0.0;  // t of slot `lane`, assembled from the 4 m-tiles
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+                const double* xr = X + p * kChunkT;
+                const double* yr = Y + p * kChunkT;
+                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double a = xr[swz2(p, 4 * ks + tq)];
+                    dmma(acc[0][0], acc[0][1], a, Fb[0][ks]);
+                    dmma(acc[1][0], acc[1][1], a, Fb[1][ks]);
+                }
+                double part = 0.0;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const double2 y = *reinterpret_cast<const double2*>(yr + swz2(p, 8 * nt + 2 * tq));
+                    part = fma(acc[nt][0], y.x, part);
+                    part = fma(acc[nt][1], y.y, part);
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                // slot p = 8 mt + gq lives on lanes 4 gq .. 4 gq + 3; move it to lane p
+                const double tp = __shfl_sync(0xffffffffu, part, 4 * (lane & 7));
+                if ((lane >> 3) == mt) t = tp;
+            }
+            double wn = 0.0;
+            if (lane < cnt) ddmax = fmax(ddmax, epi.apply(p0 + lane, t, in_cur, wn));
+            if (k >= 2) mbar_wait(&w_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
+            sm.w[u][k & 1][lane] = wn;
+            mbar_arrive(&w_full[k & 1]);
+            if (k + 1 < nck) dsc = db.get(k + 1, lane);
+            in_cur = in_next;
+        }
+        warp_max_atomic(dmax, ddmax);
+    } else {
+        double S[2][2][2];  // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]
+        int32_t cur_key = -1;
+        int64_t org = 0;
+        auto flush = [&]() {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                double* row = grid_out + org + (int64_t)(8 * mt + gq) * ng + 2 * tq;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        if (S[mt][nt][i] != 0.0) atomicAdd(row + 8 * nt + i, S[mt][nt][i]);
+            }
+        };
+        for (int64_t k = 0; k < nck; ++k) {
+            const int64_t c = cbeg + k;
+            const int slot = (int)(k % kRing2);
+            const int4 dsc = db.get(k, lane);
+            if (dsc.z != cur_key) {
+                if (cur_key >= 0) flush();
+                cur_key = dsc.z;
+                org = origin(cur_key);
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
+            }
+            mbar_wait(&w_full[k & 1], (uint32_t)((k >> 1) & 1));
+            mbar_wait(&win_full[slot], (uint32_t)((k / kRing2) & 1));
+            const double* X = swin + slot * kW2;
+            const double* Y = X + kChunk * kChunkT;
+            const double wl = sm.w[u][k & 1][lane];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int p = 4 * ks + tq;
+                const double wp = __shfl_sync(0xffffffffu, wl, p);
+                const double* xr = X + p * kChunkT;
+                const double* yr = Y + p * kChunkT;
+                const double xa0 = wp * xr[swz2(p, gq)];
+                const double xa1 = wp * xr[swz2(p, 8 + gq)];
+                const double yb0 = yr[swz2(p, gq)];
+                const double yb1 = yr[swz2(p, 8 + gq)];
+                dmma(S[0][0][0], S[0][0][1], xa0, yb0);
+                dmma(S[0][1][0], S[0][1][1], xa0, yb1);
+                dmma(S[1][0][0], S[1][0][1], xa1, yb0);
+                dmma(S[1][1][0], S[1][1][1], xa1, yb1);
+            }
+            __syncwarp();  // the S warp is done with window slot `slot` and w[k & 1]
+            if (lane == 0) {
+                mbar_arrive(&w_empty[k & 1]);
+                if (k + kRing2 < nck) {
+                    fence_proxy_async();
+                    mbar_expect_tx(&win_full[slot], kW2Bytes);
+                    bulk_g2s(swin + slot * kW2, win + (c + kRing2) * kW2, kW2Bytes, &win_full[slot]);
+                }
+            }
+        }
+        if (cur_key >= 0) flush();
+    }
+}
+
 // transpose-reduction of v[0..15] over the 32 lanes: returns sum_lanes v[lane >> 1]
 __device__ __forceinline__ double warp_transpose_reduce16(double (&v)[16], int lane) {
     double v8[8], v4[4], v2[2];
@@ -398,6 +583,26 @@ void chunked_gather_dot(const PointSet& ps, const double* grid, const FastParams
 void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
                            const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s) {
     if (fp.d == 3) return fused3d_gather_spread(ps, grid_in, grid_out, fp, epi, dmax, s);
+    static const bool ws = [] {
+        const char* e = getenv("UOTK_FUSED_WS");
+        return !(e && e[0] == '0');
+    }();
+    if (fp.d == 2 && ws) {
+        if (ps.n == 0 || ps.nchunks == 0) return;
+        static bool attr_set = false;
+        if (!attr_set) {
+            UOTK_CUDA(cudaFuncSetAttribute(sinkhorn2d_ws_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sizeof(Smem2WS)));
+            attr_set = true;
+        }
+        const int nunits = ps.chunk_blocks;
+        const int blocks = (nunits + kWarps2 - 1) / kWarps2;
+        ProfScope prof(kProfFused, s);
+        sinkhorn2d_ws_k<<<blocks, 2 * kWarps2 * 32, sizeof(Smem2WS), s>>>(
+            ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, grid_in, grid_out, epi, dmax);
+        UOTK_LAUNCHED();
+        return;
+    }
     launch12<0, EpiSinkhorn>(ps, grid_in, grid_out, nullptr, fp, epi, dmax, s, kProfFused);
 }
 
