@@ -148,6 +148,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     UOTK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_len.p, run_start.p, n, s));
     tmp_bytes = std::max(tmp_bytes, t2);
     DevBuf<uint8_t> tmp(tmp_bytes, s);
+    trace_mark("chunks: scratch allocations");
     int32_t nruns = 0;
     // runs of equal group keys -> chunks of <= 32 points; returns the number of chunks
     auto encode = [&](const int32_t* keys) -> int64_t {
@@ -156,6 +157,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
         add_launches(2);
         UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         UOTK_CUDA(cudaStreamSynchronize(s));
+        trace_mark("chunks: run-length encode");
         t = tmp_bytes;
         UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, run_len.p, run_start.p, nruns, s));
         chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
@@ -268,6 +270,13 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     add_launches(1);
     ps.chunk_bounds.alloc(nb + 1, s);
     chunk_bounds_k<<<blocks_for(nb + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nb, ps.chunk_bounds.p);
+    if (d == 2) {
+        const int nw = (int)std::min<int64_t>((int64_t)sms * kUnitsWS2 * kCtasWS2, nchunks);
+        ps.chunk_bounds_ws.alloc(nw + 1, s);
+        chunk_bounds_k<<<blocks_for(nw + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nw, ps.chunk_bounds_ws.p);
+        UOTK_LAUNCHED();
+        ps.chunk_units_ws = nw;
+    }
     UOTK_LAUNCHED();
     trace_mark("chunks: windows + bounds");
     ps.chunk_blocks = nb;

@@ -23,6 +23,9 @@ constexpr int kStride3 = 20;            // d = 3 padded row stride (doubles)
 constexpr int kCtas3 = 2;
 constexpr int kWarps2 = 3, kCtas2 = 3;
 constexpr int kWarps1 = 8, kCtas1 = 2;
+// d = 2 warp-specialised Sinkhorn half-step: units of 2 gather warps + 1 spread warp,
+// kUnitsWS2 units per CTA, kCtasWS2 CTAs per SM, its own chunk partition
+constexpr int kUnitsWS2 = 2, kCtasWS2 = 2;
 __host__ __device__ constexpr int chunk_units_per_sm(int d) {
     return d == 3 ? kCtas3 : (d == 2 ? kWarps2 * kCtas2 : kWarps1 * kCtas1);
 }

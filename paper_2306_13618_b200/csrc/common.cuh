@@ -118,6 +118,8 @@ struct PointSet {
     DevBuf<double> chunk_win; // nchunks x chunk_win_doubles(d) window values (zero for empty slots)
     DevBuf<int32_t> chunk_bounds;  // chunk_blocks + 1 cost-balanced work-unit boundaries
     int chunk_blocks = 0;     // work units: CTAs (d = 3) or warps (d <= 2)
+    DevBuf<int32_t> chunk_bounds_ws;  // d = 2: partition for the warp-specialised half-step
+    int chunk_units_ws = 0;
     int chunk_kz = 16;        // d = 3: z extent of a group footprint (16 one cell, 24 z-segment)
     double chunk_fill = 0;    // mean occupied fraction of the 32 chunk slots
 };

@@ -38,11 +38,14 @@ void note_launch(const char* file, int line) {
 void add_launches(int k) { g_launches += k; }
 
 void trace_mark(const char* what) {
-    static const bool on = [] {
+    // UOTK_TRACE=1: host time between marks; =2: the device is synchronised first, so a
+    // mark's time includes the GPU work of its phase
+    static const int level = [] {
         const char* e = getenv("UOTK_TRACE");
-        return e && e[0] == '1';
+        return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
     }();
-    if (!on) return;
+    if (!level) return;
+    if (level == 2) cudaDeviceSynchronize();
     static thread_local auto last = std::chrono::steady_clock::now();
     const auto now = std::chrono::steady_clock::now();
     fprintf(stderr, "[uotk] %-28s %9.1f us\n", what,

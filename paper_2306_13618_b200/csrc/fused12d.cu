@@ -254,20 +254,23 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 }
 
 // ---------------------------------------------------------------- warp-specialised d = 2 half-step
-// One work unit = a warp pair: the G warp gathers chunk k (32 DMMAs), runs the Sinkhorn
-// update (3.3)/(3.4) and publishes the 32 new weights; the S warp spreads chunk k (32
-// DMMAs) from those weights while G already gathers chunk k+1.  The window ring (TMA,
-// refilled by S when it releases a slot) and the weight hand-off are per-unit mbarriers,
-// so the units of a CTA never synchronise with each other.
+// One work unit = three warps: gather/update warps G0 and G1 take the even and the odd
+// chunks of the unit's range (gather = 32 DMMAs + the Sinkhorn update (3.3)/(3.4)), and
+// publish the 32 new weights; the spread warp S spreads every chunk in order (32 DMMAs)
+// from those weights.  The gather side carries about twice the instructions of the
+// spread side (the update's log/exp), hence two G warps per S warp.  The window ring
+// (TMA, refilled by S when it releases a slot) and the weight hand-offs are per-unit
+// mbarriers: the units of a CTA never synchronise after the start.
+constexpr int kRingWS2 = 5;
 struct __align__(128) Smem2WS {
-    double win[kWarps2][kRing2][kW2];
-    double w[kWarps2][2][kChunk];             // published weights, double-buffered
-    unsigned long long win_full[kWarps2][kRing2];
-    unsigned long long w_full[kWarps2][2];
-    unsigned long long w_empty[kWarps2][2];
+    double win[kUnitsWS2][kRingWS2][kW2];
+    double w[kUnitsWS2][2][kChunk];  // published weights of the even / odd chunk
+    unsigned long long win_full[kUnitsWS2][kRingWS2];
+    unsigned long long w_full[kUnitsWS2][2];
+    unsigned long long w_empty[kUnitsWS2][2];
 };
 
-__global__ void __launch_bounds__(2 * kWarps2 * 32, kCtas2)
+__global__ void __launch_bounds__(3 * kUnitsWS2 * 32, kCtasWS2)
 sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
                 int nunits, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
                 EpiSinkhorn epi, unsigned long long* dmax) {
@@ -276,54 +279,52 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     Smem2WS& sm = *reinterpret_cast<Smem2WS*>(smem_raw);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const bool is_g = warp < kWarps2;
-    const int u = is_g ? warp : warp - kWarps2;  // unit within the CTA
+    const int u = warp / 3;     // unit within the CTA
+    const int role = warp % 3;  // 0, 1: gather warps (chunk parity), 2: spread warp
     const int gq = lane >> 2;
     const int tq = lane & 3;
-    const int unit = blockIdx.x * kWarps2 + u;
-    if (unit >= nunits) return;  // both warps of the unit leave together
-    const int64_t cbeg = bounds[unit];
-    const int64_t nck = bounds[unit + 1] - cbeg;
-    if (nck <= 0) return;
+    const int unit = blockIdx.x * kUnitsWS2 + u;
+    const bool active = unit < nunits;
+    const int64_t cbeg = active ? bounds[unit] : 0;
+    const int64_t nck = active ? bounds[unit + 1] - cbeg : 0;
     double* swin = &sm.win[u][0][0];
     unsigned long long* win_full = sm.win_full[u];
     unsigned long long* w_full = sm.w_full[u];
     unsigned long long* w_empty = sm.w_empty[u];
-    // the G warp initialises the unit's barriers; the S warp waits for it through the
-    // CTA barrier below (the only CTA-wide synchronisation, before any hand-off)
-    if (is_g && lane == 0) {
-        for (int r = 0; r < kRing2; ++r) mbar_init(&win_full[r], 1);
+    if (role == 2 && lane == 0) {
+        for (int r = 0; r < kRingWS2; ++r) mbar_init(&win_full[r], 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&w_full[i], 32);
             mbar_init(&w_empty[i], 1);
         }
         mbar_init_fence();
     }
-    __syncthreads();
-    if (is_g && lane == 0) {
-        for (int k = 0; k < kRing2 && k < nck; ++k) {
+    __syncthreads();  // the only CTA-wide synchronisation (barrier initialisation)
+    if (nck <= 0) return;
+    if (role == 2 && lane == 0) {
+        for (int k = 0; k < kRingWS2 && k < nck; ++k) {
             mbar_expect_tx(&win_full[k], kW2Bytes);
             bulk_g2s(swin + k * kW2, win + (cbeg + k) * kW2, kW2Bytes, &win_full[k]);
         }
     }
     auto origin = [&](int32_t kk) -> int64_t { return (int64_t)(kk / ng - kM + 1) * ng + (kk % ng - kM + 1); };
-    DescBatch db;
-    db.init(desc, cbeg, cbeg + nck, lane);
 
-    if (is_g) {
+    if (role < 2) {
         double Fb[2][4];  // Fb[nt][ks] = F[4ks + tq][8nt + gq]
         int32_t cur_key = -1;
         double ddmax = 0.0;
-        int4 dsc = db.get(0, lane);
+        int64_t k = role;
+        int4 dsc = k < nck ? desc[cbeg + k] : make_int4(0, 0, -1, 0);
         In in_cur{};
-        if (lane < dsc.y) in_cur = epi.load(dsc.x + lane);
-        for (int64_t k = 0; k < nck; ++k) {
-            const int slot = (int)(k % kRing2);
+        if (k < nck && lane < dsc.y) in_cur = epi.load(dsc.x + lane);
+        for (; k < nck; k += 2) {
+            const int slot = (int)(k % kRingWS2);
             const int64_t p0 = dsc.x;
             const int cnt = dsc.y;
-            const int4 dnext = db.peek_next(k);
+            // this warp's next chunk (k + 2): descriptor and epilogue inputs in flight
+            const int4 dnext = k + 2 < nck ? desc[cbeg + k + 2] : make_int4(0, 0, -1, 0);
             In in_next{};
-            if (k + 1 < nck && lane < dnext.y) in_next = epi.load(dnext.x + lane);
+            if (k + 2 < nck && lane < dnext.y) in_next = epi.load(dnext.x + lane);
             if (dsc.z != cur_key) {
                 cur_key = dsc.z;
                 const int64_t org = origin(cur_key);
@@ -334,9 +335,7 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     Fb[1][ks] = __ldg(row + 8);
                 }
             }
-            if (k + 1 < nck && dnext.z != cur_key && lane < 16)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(grid_in + origin(dnext.z) + (int64_t)lane * ng));
-            mbar_wait(&win_full[slot], (uint32_t)((k / kRing2) & 1));
+            mbar_wait(&win_full[slot], (uint32_t)((k / kRingWS2) & 1));
             const double* X = swin + slot * kW2;
             const double* Y = X + kChunk * kChunkT;
             double t = 0.0;  // t of slot `lane`, assembled from the 4 m-tiles
@@ -367,10 +366,12 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             }
             double wn = 0.0;
             if (lane < cnt) ddmax = fmax(ddmax, epi.apply(p0 + lane, t, in_cur, wn));
-            if (k >= 2) mbar_wait(&w_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
-            sm.w[u][k & 1][lane] = wn;
-            mbar_arrive(&w_full[k & 1]);
-            if (k + 1 < nck) dsc = db.get(k + 1, lane);
+            // weights of chunk k go to buffer `role` (= k & 1); its previous content was
+            // chunk k - 2, released by S
+            if (k >= 2) mbar_wait(&w_empty[role], (uint32_t)(((k >> 1) - 1) & 1));
+            sm.w[u][role][lane] = wn;
+            mbar_arrive(&w_full[role]);
+            dsc = dnext;
             in_cur = in_next;
         }
         warp_max_atomic(dmax, ddmax);
@@ -389,9 +390,12 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                         if (S[mt][nt][i] != 0.0) atomicAdd(row + 8 * nt + i, S[mt][nt][i]);
             }
         };
+        DescBatch db;
+        db.init(desc, cbeg, cbeg + nck, lane);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
-            const int slot = (int)(k % kRing2);
+            const int slot = (int)(k % kRingWS2);
+            const int b = (int)(k & 1);
             const int4 dsc = db.get(k, lane);
             if (dsc.z != cur_key) {
                 if (cur_key >= 0) flush();
@@ -402,11 +406,11 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
-            mbar_wait(&w_full[k & 1], (uint32_t)((k >> 1) & 1));
-            mbar_wait(&win_full[slot], (uint32_t)((k / kRing2) & 1));
+            mbar_wait(&w_full[b], (uint32_t)((k >> 1) & 1));
+            mbar_wait(&win_full[slot], (uint32_t)((k / kRingWS2) & 1));
             const double* X = swin + slot * kW2;
             const double* Y = X + kChunk * kChunkT;
-            const double wl = sm.w[u][k & 1][lane];
+            const double wl = sm.w[u][b][lane];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 const int p = 4 * ks + tq;
@@ -422,13 +426,13 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 dmma(S[1][0][0], S[1][0][1], xa1, yb0);
                 dmma(S[1][1][0], S[1][1][1], xa1, yb1);
             }
-            __syncwarp();  // the S warp is done with window slot `slot` and w[k & 1]
+            __syncwarp();  // S is done with window slot `slot` and w[b]
             if (lane == 0) {
-                mbar_arrive(&w_empty[k & 1]);
-                if (k + kRing2 < nck) {
+                mbar_arrive(&w_empty[b]);
+                if (k + kRingWS2 < nck) {
                     fence_proxy_async();
                     mbar_expect_tx(&win_full[slot], kW2Bytes);
-                    bulk_g2s(swin + slot * kW2, win + (c + kRing2) * kW2, kW2Bytes, &win_full[slot]);
+                    bulk_g2s(swin + slot * kW2, win + (c + kRingWS2) * kW2, kW2Bytes, &win_full[slot]);
                 }
             }
         }
@@ -595,11 +599,11 @@ void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* gr
                                            (int)sizeof(Smem2WS)));
             attr_set = true;
         }
-        const int nunits = ps.chunk_blocks;
-        const int blocks = (nunits + kWarps2 - 1) / kWarps2;
+        const int nunits = ps.chunk_units_ws;
+        const int blocks = (nunits + kUnitsWS2 - 1) / kUnitsWS2;
         ProfScope prof(kProfFused, s);
-        sinkhorn2d_ws_k<<<blocks, 2 * kWarps2 * 32, sizeof(Smem2WS), s>>>(
-            ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, grid_in, grid_out, epi, dmax);
+        sinkhorn2d_ws_k<<<blocks, 3 * kUnitsWS2 * 32, sizeof(Smem2WS), s>>>(
+            ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds_ws.p, nunits, fp.ng, grid_in, grid_out, epi, dmax);
         UOTK_LAUNCHED();
         return;
     }
