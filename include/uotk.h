@@ -104,6 +104,8 @@ typedef struct {
 #define UOTK_FLAG_GENERIC 1  /* always the generic thread-per-point kernels          */
 #define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m must be 8)     */
 #define UOTK_FLAG_TRANSPORT 4 /* uot: also evaluate the transport term <pi, d^2>    */
+#define UOTK_FLAG_FFT 8       /* always the cuFFT chain (D2Z, D_k, Z2D), never the separable
+                                 circulant GEMMs of the Gaussian (which run on one rank only) */
 
 /* What a call actually used (any pointer to it may be NULL). */
 typedef struct {

@@ -28,6 +28,7 @@ FLAG_GENERIC, FLAG_CHUNKED = 1, 2  # opts["flags"]: kernel family of the NFFT pa
 _KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, "gauss_r2": GAUSS_R2, GAUSS: GAUSS, IMQ: IMQ,
          GAUSS_R2: GAUSS_R2}
 FLAG_TRANSPORT = 4
+FLAG_FFT = 8  # always the cuFFT spectral chain (the multi-rank path), never the separable GEMMs
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 
 __all__ = ["kernel_sum", "uot_sinkhorn", "uot_sinkhorn_scaling", "mmd2", "uot_cstar", "sinkhorn_divergence", "Comm", "UOTResult", "GAUSS",

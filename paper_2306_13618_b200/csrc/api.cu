@@ -55,7 +55,8 @@ uotk_opts resolve(const uotk_opts* o) {
     uotk_opts r;
     memset(&r, 0, sizeof r);
     if (o) r = *o;
-    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED | UOTK_FLAG_TRANSPORT)) != 0 || r.reserved != 0)
+    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED | UOTK_FLAG_TRANSPORT | UOTK_FLAG_FFT)) != 0 ||
+        r.reserved != 0)
         fail(UOTK_EINVAL, "unknown opts.flags bits, or opts.reserved != 0");
     if ((r.flags & UOTK_FLAG_GENERIC) && (r.flags & UOTK_FLAG_CHUNKED))
         fail(UOTK_EINVAL, "opts.flags: UOTK_FLAG_GENERIC and UOTK_FLAG_CHUNKED are exclusive");

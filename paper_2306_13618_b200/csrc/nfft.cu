@@ -294,7 +294,7 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
 
 double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
-    if (sp.pd->separable && (comm == nullptr || comm_nranks(comm) == 1)) {
+    if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT) && (comm == nullptr || comm_nranks(comm) == 1)) {
         ProfScope ps_(kProfFft, s);
         return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s);
     }

@@ -227,8 +227,11 @@ def test_one_rank_nccl_communicator_matches(uk):
         b = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts={"method": "nfft"},
                           comm=comm)
         assert close(a, b)
+        # the spectrum all-reduce of the FFT chain (the multi-rank path) on the 1-rank comm
+        nf = {"method": "nfft", "flags": uk.FLAG_FFT}
+        c = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param, opts=nf, comm=comm)
+        assert close(a, c)
         u = W.c3_uot(n=1500, m=1300, iters=5)
-        nf = {"method": "nfft"}
         r1 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf)
         r2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf, comm=comm)
         assert close(r1[0], r2[0], 1e-12) and close(r1[1], r2[1], 1e-12)
@@ -538,3 +541,21 @@ def test_uot_transport_and_marginals(uk, method, d):
     assert rel_err(res.p.cpu().numpy(), p_ref, False) <= 1e-8
     assert rel_err(res.q.cpu().numpy(), q_ref, False) <= 1e-8
     assert abs(res.transport - t_ref) <= 1e-8 * abs(t_ref), (res.transport, t_ref)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_fft_chain_vs_separable_chain(uk, d):
+    """The Gaussian's two spectral chains — cuFFT D2Z / D_k / Z2D (multi-rank path,
+    UOTK_FLAG_FFT) and the box-restricted circulant GEMMs — both against the oracle."""
+    pr = W.random_sum(d, 3001, 1999, kind=W.GAUSS, param=0.0025, seed=70 + d)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    for flags in (uk.FLAG_FFT, 0):
+        got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param,
+                            opts={"method": "nfft", "flags": flags})
+        assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9, flags
+    u = W.c3_uot(n=1100, m=900, iters=10) if d == 3 else W.c1_uot(n=800, m=700, d=d)
+    iters = 10
+    ref = oracle.uot_sinkhorn_direct(u.x, u.a, u.y, u.b, u.eps, u.lam, u.lam, iters)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=iters,
+                                       opts={"method": "nfft", "flags": uk.FLAG_FFT})
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
