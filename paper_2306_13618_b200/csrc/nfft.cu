@@ -250,7 +250,12 @@ int comm_nranks(void* comm);  // comm.cu
 // (last axis contiguous); cuBLAS is column-major.  Csep is symmetric, so any square
 // sub-block C[o.., o..] read column-major with ld n is the same sub-block.
 // Returns the buffer holding g' in grid layout (valid inside the box only).
-static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cudaStream_t s) {
+void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);  // comm.cu
+
+// With several ranks every rank spread its own sources: the chain is linear, so the
+// first pass's compact output (w^d doubles — the size of the truncated spectrum the FFT
+// path would all-reduce) is summed over ranks (NCCL) before the remaining passes.
+static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
     const int n = fp.ng;
     const int o = fp.box_lo, w = fp.box_w;
@@ -267,12 +272,14 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
     if (fp.d == 1) {  // out[z] = sum_z' C[z][z'] g[z']
         ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, w, 1, w, &one, Cb, n, grid + o, w, &zero, spare + o, w));
         add_launches(1);
+        if (comm) comm_allreduce(spare + o, (size_t)w, 0, comm, s);  // sum
         return spare;
     }
     if (fp.d == 2) {
         // y: T1(y, x) = sum_y' C[y][y'] g[x][y']                      (compact w x w in spare)
         ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, Cb, n, grid + (size_t)o * n + o, n, &zero, spare,
                        w));
+        if (comm) comm_allreduce(spare, (size_t)w2, 0, comm, s);  // sum
         // x: out[x][y] = sum_x' T1(y, x') C[x'][x]                    (into grid, box positions)
         ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, spare, w, Cb, n, &zero, grid + (size_t)o * n + o,
                        n));
@@ -282,6 +289,7 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
     // d = 3.  z, per x: T1[x][y][z] = sum_z' C[z][z'] g[x][y][z']   (compact w^3 in spare)
     ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, Cb, n, 0,
                                  grid + (size_t)o * n2 + (size_t)o * n + o, n, n2, &zero, spare, w, w2, w));
+    if (comm) comm_allreduce(spare, (size_t)w2 * w, 0, comm, s);  // sum
     // y, per x: T2[x][y][z] = sum_y' T1[x][y'][z] C[y'][y]          (compact w^3 in grid)
     ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, spare, w, w2, Cb, n, 0, &zero, grid, w,
                                  w2, w));
@@ -294,9 +302,9 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
 
 double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
-    if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT) && (comm == nullptr || comm_nranks(comm) == 1)) {
+    if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT)) {
         ProfScope ps_(kProfFft, s);
-        return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s);
+        return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s, comm);
     }
     ProfScope ps_(kProfFft, s);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));

@@ -212,9 +212,10 @@ def test_mmd2_identities(uk):
 
 # ------------------------------------------------------------------ NCCL exchange path
 def test_one_rank_nccl_communicator_matches(uk):
-    """The multi-GPU code path (bbox min/max, per-sum spectrum all-reduce, scalar sums)
-    through a real 1-rank NCCL communicator gives the single-GPU results (up to the
-    summation order of the fp64 atomics that flush the spread, ~1e-16 relative)."""
+    """The multi-GPU code path (bbox min/max, the per-sum all-reduce — of the first
+    separable pass's output by default, of the truncated spectrum with UOTK_FLAG_FFT —
+    and the scalar sums) through a real 1-rank NCCL communicator gives the single-GPU
+    results (up to the summation order of the fp64 atomics that flush the spread)."""
     comm = uk.Comm(uk.Comm.unique_id(), 1, 0)
 
     def close(p, q, tol=1e-13):
