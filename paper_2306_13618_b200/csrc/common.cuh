@@ -29,6 +29,8 @@ void check_cufft(cufftResult r, const char* what, const char* file, int line);
 #define UOTK_LAUNCHED() ::uotk::note_launch(__FILE__, __LINE__)
 
 void note_launch(const char* file, int line);  // counts launches + checks launch errors
+// cudaFuncSetAttribute(max dynamic shared memory) once per (kernel, device)
+void set_smem_attr(const void* func, int bytes);
 void add_launches(int k);                      // launches made by library code we call (CUB)
 
 // host-side phase timing for diagnosis: with UOTK_TRACE=1 in the environment every

@@ -2,6 +2,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <map>
+#include <set>
 #include <mutex>
 #include <tuple>
 
@@ -36,6 +37,17 @@ void note_launch(const char* file, int line) {
 }
 
 void add_launches(int k) { g_launches += k; }
+
+void set_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    UOTK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({func, dev})) return;
+    UOTK_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({func, dev});
+}
 
 void trace_mark(const char* what) {
     // UOTK_TRACE=1: host time between marks; =2: the device is synchronised first, so a

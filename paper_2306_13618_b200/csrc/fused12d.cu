@@ -541,12 +541,7 @@ void launch12(const PointSet& ps, const double* gin, double* gout, const double*
     const int nunits = ps.chunk_blocks;
     ProfScope prof(tag, s);
     if (fp.d == 2) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            UOTK_CUDA(cudaFuncSetAttribute(chunked2d_k<MODE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sizeof(Smem2)));
-            attr_set = true;
-        }
+        set_smem_attr((const void*)chunked2d_k<MODE, Epi>, (int)sizeof(Smem2));
         const int blocks = (nunits + kWarps2 - 1) / kWarps2;
         chunked2d_k<MODE, Epi><<<blocks, kWarps2 * 32, sizeof(Smem2), s>>>(
             ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, gin, gout, w, epi, dmax);
@@ -593,12 +588,7 @@ void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* gr
     }();
     if (fp.d == 2 && ws) {
         if (ps.n == 0 || ps.nchunks == 0) return;
-        static bool attr_set = false;
-        if (!attr_set) {
-            UOTK_CUDA(cudaFuncSetAttribute(sinkhorn2d_ws_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sizeof(Smem2WS)));
-            attr_set = true;
-        }
+        set_smem_attr((const void*)sinkhorn2d_ws_k, (int)sizeof(Smem2WS));
         const int nunits = ps.chunk_units_ws;
         const int blocks = (nunits + kUnitsWS2 - 1) / kUnitsWS2;
         ProfScope prof(kProfFused, s);

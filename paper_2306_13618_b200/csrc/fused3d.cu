@@ -496,12 +496,7 @@ void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* gr
         return;
     }
     if (ps.n == 0 || ps.nchunks == 0) return;
-    static bool attr_set = false;
-    if (!attr_set) {
-        UOTK_CUDA(cudaFuncSetAttribute(sinkhorn3d_ws_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sizeof(SmemWS)));
-        attr_set = true;
-    }
+    set_smem_attr((const void*)sinkhorn3d_ws_k, (int)sizeof(SmemWS));
     ProfScope prof(kProfFused, s);
     sinkhorn3d_ws_k<<<ps.chunk_blocks, 256, sizeof(SmemWS), s>>>(ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p,
                                                                  fp.ng, grid_in, grid_out, epi, dmax);
