@@ -237,6 +237,15 @@ def test_one_rank_nccl_communicator_matches(uk):
         r2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5, opts=nf, comm=comm)
         assert close(r1[0], r2[0], 1e-12) and close(r1[1], r2[1], 1e-12)
         assert close(r1[2].primal, r2[2].primal)
+        # c* moments and the transport term through the communicator
+        c1_ = uk.uot_cstar(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam)
+        c2_ = uk.uot_cstar(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, comm=comm)
+        assert abs(c1_ - c2_) <= 1e-14 * c1_
+        t1 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5,
+                             opts={"method": "nfft"}, transport=True)[2].transport
+        t2 = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=5,
+                             opts={"method": "nfft"}, transport=True, comm=comm)[2].transport
+        assert abs(t1 - t2) <= 1e-12 * abs(t1)
         m = W.c2_mmd(n=2000, m=1800)
         v1 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts=nf)
         v2 = uk.mmd2(cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b), "gauss", 0.0025, opts=nf, comm=comm)
