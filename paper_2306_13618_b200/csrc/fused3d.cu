@@ -117,12 +117,18 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         }
     };
 
+    // descriptors two chunks ahead; the spread-only mode's source weights one chunk ahead
     int4 dsc_next = cbeg < cend ? desc[cbeg] : make_int4(0, 0, -1, 0);
+    int4 dsc_next2 = cbeg + 1 < cend ? desc[cbeg + 1] : make_int4(0, 0, -1, 0);
+    double w_cur = (!GATHER && lane < dsc_next.y) ? w_in[dsc_next.x + lane] : 0.0;
     for (int64_t c = cbeg; c < cend; ++c) {
         const int k = (int)(c - cbeg);
         const int buf = k & 1;
         const int4 dsc = dsc_next;  // {first point, count, group key, 0}
-        if (c + 1 < cend) dsc_next = desc[c + 1];  // loaded one chunk ahead
+        dsc_next = dsc_next2;
+        if (c + 2 < cend) dsc_next2 = desc[c + 2];
+        double w_nxt = 0.0;
+        if (!GATHER && c + 1 < cend && lane < dsc_next.y) w_nxt = w_in[dsc_next.x + lane];
         const int64_t p0 = dsc.x;
         const int cnt = dsc.y;
         const int32_t key = dsc.z;
@@ -215,7 +221,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 }
             }
         } else {
-            wn = (lane < cnt) ? w_in[p0 + lane] : 0.0;
+            wn = w_cur;
         }
 
         if (SPREAD) {
@@ -245,6 +251,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             mbar_expect_tx(&sm.bar[buf], kWB);
             bulk_g2s(&sm.win[buf][0], win + (c + 2) * kWD, kWB, &sm.bar[buf]);
         }
+        w_cur = w_nxt;
     }
     if (SPREAD && cur_key >= 0) flush();
     if (GATHER && warp == 0) warp_max_atomic(dmax, ddmax);
