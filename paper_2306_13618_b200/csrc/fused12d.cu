@@ -314,17 +314,17 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
         int32_t cur_key = -1;
         double ddmax = 0.0;
         int64_t k = role;
-        int4 dsc = k < nck ? desc[cbeg + k] : make_int4(0, 0, -1, 0);
+        auto fetch = [&](int64_t kk) { return kk < nck ? desc[cbeg + kk] : make_int4(0, 0, -1, 0); };
+        // this warp's chunks k, k + 2 (descriptor ready) and k + 4 (descriptor in flight)
+        int4 dsc = fetch(k);
+        int4 dnext = fetch(k + 2);
         In in_cur{};
         if (k < nck && lane < dsc.y) in_cur = epi.load(dsc.x + lane);
         for (; k < nck; k += 2) {
             const int slot = (int)(k % kRingWS2);
             const int64_t p0 = dsc.x;
             const int cnt = dsc.y;
-            // this warp's next chunk (k + 2): descriptor and epilogue inputs in flight
-            const int4 dnext = k + 2 < nck ? desc[cbeg + k + 2] : make_int4(0, 0, -1, 0);
-            In in_next{};
-            if (k + 2 < nck && lane < dnext.y) in_next = epi.load(dnext.x + lane);
+            const int4 dnext2 = fetch(k + 4);
             if (dsc.z != cur_key) {
                 cur_key = dsc.z;
                 const int64_t org = origin(cur_key);
@@ -364,6 +364,10 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 const double tp = __shfl_sync(0xffffffffu, part, 4 * (lane & 7));
                 if ((lane >> 3) == mt) t = tp;
             }
+            // the next chunk's epilogue inputs, issued after this chunk's DMMAs (a load
+            // issued before them would share their wait on the long scoreboard)
+            In in_next{};
+            if (k + 2 < nck && lane < dnext.y) in_next = epi.load(dnext.x + lane);
             double wn = 0.0;
             if (lane < cnt) ddmax = fmax(ddmax, epi.apply(p0 + lane, t, in_cur, wn));
             // weights of chunk k go to buffer `role` (= k & 1); its previous content was
@@ -372,6 +376,7 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             sm.w[u][role][lane] = wn;
             mbar_arrive(&w_full[role]);
             dsc = dnext;
+            dnext = dnext2;
             in_cur = in_next;
         }
         warp_max_atomic(dmax, ddmax);
