@@ -142,13 +142,16 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     if (!chunked_available(fp) || ps.n == 0 || (fp.flags & UOTK_FLAG_GENERIC)) return;
     const int d = fp.d;
     const int n = (int)ps.n;
+    trace_mark("chunks: start");
     DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(2, s);
+    trace_mark("chunks: 6 scratch allocations");
     size_t tmp_bytes = 0, t2 = 0;
     UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
     UOTK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_len.p, run_start.p, n, s));
+    trace_mark("chunks: cub size queries");
     tmp_bytes = std::max(tmp_bytes, t2);
     DevBuf<uint8_t> tmp(tmp_bytes, s);
-    trace_mark("chunks: scratch allocations");
+    trace_mark("chunks: temp allocation");
     int32_t nruns = 0;
     // runs of equal group keys -> chunks of <= 32 points; returns the number of chunks
     auto encode = [&](const int32_t* keys) -> int64_t {
