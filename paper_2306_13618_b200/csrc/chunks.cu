@@ -214,18 +214,26 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     }
     size_t free_b = total_b;
     if (win_bytes > total_b / 16) {
-        size_t cached = 0;
         int dev = 0;
-        cudaMemPool_t pool;
+        cudaMemPool_t pool = nullptr;
         UOTK_CUDA(cudaGetDevice(&dev));
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            unsigned long long reserved = 0, used = 0;
-            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
-                cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
-                reserved > used)
-                cached = (size_t)(reserved - used);
-        }
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) pool = nullptr;
         cudaGetLastError();
+        // memory the pool keeps reserved but unused is reusable
+        auto pool_cached = [&]() -> size_t {
+            unsigned long long reserved = 0, used = 0;
+            if (pool && cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+                cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+                return (size_t)(reserved - used);
+            cudaGetLastError();
+            return 0;
+        };
+        size_t cached = pool_cached();
+        // the library's block cache holds freed blocks as "used": give them back first
+        if (cached < win_bytes && block_cache_bytes() > 0) {
+            block_cache_release();
+            cached = pool_cached();
+        }
         if (cached < win_bytes) {
             size_t t0 = 0;
             UOTK_CUDA(cudaMemGetInfo(&free_b, &t0));

@@ -38,13 +38,14 @@ void add_launches(int k);                      // launches made by library code 
 void trace_mark(const char* what);
 
 // ------------------------------------------------------------------ device buffers
-// Stream-ordered device allocation (cudaMallocAsync on the call's stream; the
-// device's default pool keeps memory cached between calls).
+// Device allocation through the library's block cache (context.cu), backed by the
+// stream-ordered pool (cudaMallocAsync on the call's stream).
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = nullptr;
+    bool pooled = false;  // allocated from the stream-ordered pool (inside graph capture)
     DevBuf() = default;
     DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
     void alloc(size_t count, cudaStream_t stream);
@@ -52,11 +53,13 @@ struct DevBuf {
     ~DevBuf();
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), pooled(o.pooled) { o.p = nullptr; o.n = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept;
 };
 
 bool is_device_pointer(const void* ptr);
+size_t block_cache_bytes();   // freed device blocks the library keeps for reuse (this device)
+void block_cache_release();   // return them to the stream-ordered pool
 
 // A caller array that may live on the host or the device: `d` is always a device
 // pointer valid for the duration of the call.

@@ -58,32 +58,171 @@ void trace_mark(const char* what) {
     }();
     if (!level) return;
     if (level == 2) cudaDeviceSynchronize();
+    unsigned long long reserved = 0;
+    if (level == 2) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaGetLastError();
+    }
     static thread_local auto last = std::chrono::steady_clock::now();
     const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[uotk] %-28s %9.1f us\n", what,
-            std::chrono::duration<double, std::micro>(now - last).count());
+    fprintf(stderr, "[uotk] %-28s %9.1f us  pool %.2f GB\n", what,
+            std::chrono::duration<double, std::micro>(now - last).count(), reserved / 1e9);
     last = now;
+}
+
+// ------------------------------------------------------------------ block cache
+// Device buffers of a call are recycled through a small library-level cache instead of
+// being returned to the stream-ordered pool: cudaMallocAsync occasionally blocks the
+// host for tens of milliseconds even when the pool does not grow (measured, DESIGN.md
+// §10), and a solve makes ~40 allocations.  A freed block records an event on its stream;
+// it is reused by the same stream at once, by another stream once the event completed.
+// Inside CUDA-graph capture the stream-ordered allocator is used (graph memory nodes).
+namespace {
+struct CachedBlock {
+    void* p;
+    size_t bytes;
+    int dev;
+    cudaStream_t s;
+    cudaEvent_t ev;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+size_t g_cache_bytes = 0;
+constexpr size_t kCacheMaxBytes = size_t(48) << 30;
+
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return st != cudaStreamCaptureStatusNone;
+}
+
+size_t round_bytes(size_t b) { return (b + 4095) & ~size_t(4095); }
+
+void* cache_alloc(size_t bytes, cudaStream_t s, bool* from_pool) {
+    bytes = round_bytes(bytes);
+    *from_pool = capturing(s);
+    if (*from_pool) {
+        void* p = nullptr;
+        UOTK_CUDA(cudaMallocAsync(&p, bytes, s));
+        return p;
+    }
+    int dev = 0;
+    UOTK_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        int best = -1;
+        for (int i = 0; i < (int)g_cache.size(); ++i) {
+            const CachedBlock& b = g_cache[i];
+            if (b.dev != dev || b.bytes < bytes || b.bytes > 2 * bytes + (size_t(4) << 20)) continue;
+            if (best >= 0 && g_cache[best].bytes <= b.bytes) continue;
+            if (b.s != s && cudaEventQuery(b.ev) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            best = i;
+        }
+        if (best >= 0) {
+            CachedBlock b = g_cache[best];
+            g_cache.erase(g_cache.begin() + best);
+            g_cache_bytes -= b.bytes;
+            cudaEventDestroy(b.ev);
+            return b.p;
+        }
+    }
+    void* p = nullptr;
+    UOTK_CUDA(cudaMallocAsync(&p, bytes, s));
+    return p;
+}
+
+void cache_free(void* p, size_t bytes, cudaStream_t s, bool from_pool) {
+    if (from_pool || capturing(s)) {
+        cudaFreeAsync(p, s);
+        return;
+    }
+    bytes = round_bytes(bytes);
+    int dev = 0;
+    cudaEvent_t ev = nullptr;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, s) != cudaSuccess) {
+        cudaGetLastError();
+        if (ev) cudaEventDestroy(ev);
+        cudaFreeAsync(p, s);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.push_back({p, bytes, dev, s, ev});
+    g_cache_bytes += bytes;
+    while (g_cache_bytes > kCacheMaxBytes && !g_cache.empty()) {  // evict the oldest
+        CachedBlock b = g_cache.front();
+        g_cache.erase(g_cache.begin());
+        g_cache_bytes -= b.bytes;
+        cudaStreamWaitEvent(b.s, b.ev, 0);
+        cudaFreeAsync(b.p, b.s);
+        cudaEventDestroy(b.ev);
+    }
+}
+}  // namespace
+
+// bytes held by the block cache on the current device, and releasing them to the pool
+size_t block_cache_bytes() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t b = 0;
+    for (const CachedBlock& c : g_cache)
+        if (c.dev == dev) b += c.bytes;
+    return b;
+}
+
+void block_cache_release() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (size_t i = 0; i < g_cache.size();) {
+        CachedBlock& b = g_cache[i];
+        if (b.dev != dev) {
+            ++i;
+            continue;
+        }
+        cudaStreamWaitEvent(b.s, b.ev, 0);
+        cudaFreeAsync(b.p, b.s);
+        cudaEventDestroy(b.ev);
+        g_cache_bytes -= b.bytes;
+        g_cache.erase(g_cache.begin() + i);
+    }
 }
 
 template <typename T>
 void DevBuf<T>::alloc(size_t count, cudaStream_t stream) {
-    if (p) UOTK_CUDA(cudaFreeAsync(p, s));
+    if (p) cache_free(p, n * sizeof(T), s, pooled);
     p = nullptr;
     n = count;
     s = stream;
-    if (count) UOTK_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+    if (count) p = static_cast<T*>(cache_alloc(count * sizeof(T), stream, &pooled));
 }
 
 template <typename T>
 DevBuf<T>::~DevBuf() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) cache_free(p, n * sizeof(T), s, pooled);
 }
 
 template <typename T>
 DevBuf<T>& DevBuf<T>::operator=(DevBuf&& o) noexcept {
     if (this != &o) {
-        if (p) cudaFreeAsync(p, s);
-        p = o.p; n = o.n; s = o.s;
+        if (p) cache_free(p, n * sizeof(T), s, pooled);
+        p = o.p; n = o.n; s = o.s; pooled = o.pooled;
         o.p = nullptr; o.n = 0;
     }
     return *this;
