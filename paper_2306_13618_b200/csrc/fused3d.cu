@@ -3,10 +3,12 @@
 // Points are sorted by grid cell (points.cu), so every run of equal keys shares one
 // 16^3 window footprint on the oversampled grid (m = 8, 2m taps per axis).  Runs are cut
 // into chunks of <= 32 points and the window values of every chunk (3 axes x 32 slots x
-// 16 taps, zero for empty slots) are computed ONCE per point set (fused3d_prepare) —
-// points do not move between Sinkhorn iterations.  A 128-thread CTA walks a contiguous,
-// cost-balanced range of chunks, streaming each chunk's window block into shared memory
-// with a TMA bulk copy (cp.async.bulk + mbarrier, double buffered).
+// 16 taps, zero for empty slots) are computed ONCE per point set (chunks.cu,
+// chunked_prepare) — points do not move between Sinkhorn iterations.  A 256-thread CTA
+// walks a contiguous, cost-balanced range of chunks, streaming each chunk's window block
+// into shared memory with a TMA bulk copy (cp.async.bulk + mbarrier, double buffered in
+// chunked3d_k, a ring of 3 in the warp-specialised sinkhorn3d_ws_k).  Sparse clouds use
+// z-segment groups (KZ = 24: 9 cells along z share one 16 x 16 x 24 footprint).
 //
 // Per chunk, with X_p, Y_p, Z_p the windows of point p along the three axes and F the
 // group's footprint (outer / inner sums of (4.6)):
