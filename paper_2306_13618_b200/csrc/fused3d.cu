@@ -475,6 +475,123 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     }
 }
 
+// ---------------------------------------------------------------- spread only, ring
+// The adjoint NFFT alone (kernel sums' sources, MMD^2): the same per-warp a-pair GEMMs as
+// chunked3d_k<1>, but without a CTA barrier per chunk — window blocks stream through a
+// ring of kRingS slots, each released by an mbarrier the eight warps arrive on, so the
+// warps drift apart and the TMA refill overlaps the other warps' DMMAs.
+constexpr int kRingS = 4;
+template <int KZ>
+struct __align__(128) SmemS {
+    double win[kRingS][chunk_win3_doubles(KZ)];
+    unsigned long long full[kRingS];
+    unsigned long long empty[kRingS];
+};
+
+template <int KZ>
+__global__ void __launch_bounds__(kThreads, kBlocksPerSM)
+spread3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds, int ng,
+           double* __restrict__ grid_out, const double* __restrict__ w_in) {
+    constexpr int NZ = KZ / 8;
+    constexpr int ZS = chunk_zstride3(KZ);
+    constexpr int kWD = chunk_win3_doubles(KZ);
+    constexpr uint32_t kWB = kWD * sizeof(double);
+    extern __shared__ __align__(128) unsigned char s_raw[];
+    SmemS<KZ>& sm = *reinterpret_cast<SmemS<KZ>*>(s_raw);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int gq = lane >> 2;
+    const int tq = lane & 3;
+    const int a0 = 2 * warp;
+    const int64_t cbeg = bounds[blockIdx.x];
+    const int64_t nck = bounds[blockIdx.x + 1] - cbeg;
+    const int64_t ng2 = (int64_t)ng * ng;
+    if (tid == 0) {
+        for (int r = 0; r < kRingS; ++r) {
+            mbar_init(&sm.full[r], 1);
+            mbar_init(&sm.empty[r], kThreads / 32);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 0; k < kRingS && k < nck; ++k) {
+            mbar_expect_tx(&sm.full[k], kWB);
+            bulk_g2s(&sm.win[k][0], win + (cbeg + k) * kWD, kWB, &sm.full[k]);
+        }
+    }
+    double S[4][NZ][2];
+    int32_t cur_key = -1;
+    int64_t gorg = 0;
+    auto origin = [&](int32_t kk) -> int64_t {
+        const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
+        return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
+    };
+    auto flush = [&]() {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
+#pragma unroll
+            for (int nz = 0; nz < NZ; ++nz)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (S[mt][nz][i] != 0.0) atomicAdd(grid_out + row + 8 * nz + 2 * tq + i, S[mt][nz][i]);
+        }
+    };
+    int4 d0 = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
+    int4 d1 = nck > 1 ? desc[cbeg + 1] : make_int4(0, 0, -1, 0);
+    double w_cur = lane < d0.y ? w_in[d0.x + lane] : 0.0;
+    for (int64_t k = 0; k < nck; ++k) {
+        const int slot = (int)(k % kRingS);
+        const int4 dsc = d0;
+        d0 = d1;
+        if (k + 2 < nck) d1 = desc[cbeg + k + 2];
+        const double w_nxt = (k + 1 < nck && lane < d0.y) ? w_in[d0.x + lane] : 0.0;
+        if (dsc.z != cur_key) {
+            if (cur_key >= 0) flush();
+            cur_key = dsc.z;
+            gorg = origin(cur_key);
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nz = 0; nz < NZ; ++nz) S[mt][nz][0] = S[mt][nz][1] = 0.0;
+        }
+        mbar_wait(&sm.full[slot], (uint32_t)((k / kRingS) & 1));
+        const double(*wx)[kStride] = reinterpret_cast<const double(*)[kStride]>(&sm.win[slot][0]);
+        const double(*wy)[kStride] = wx + kChunk;
+        const double(*wz)[ZS] = reinterpret_cast<const double(*)[ZS]>(&sm.win[slot][2 * kChunk * kStride]);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int p = 4 * ks + tq;
+            const double wp = __shfl_sync(0xffffffffu, w_cur, p);
+            double bz[NZ];
+#pragma unroll
+            for (int nz = 0; nz < NZ; ++nz) bz[nz] = wp * wz[p][8 * nz + gq];
+            const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+            const double xv[2] = {xa.x, xa.y};
+            const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
+#pragma unroll
+                for (int nz = 0; nz < NZ; ++nz) dmma(S[mt][nz][0], S[mt][nz][1], am, bz[nz]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[slot]);  // this warp is done with the slot
+        if (tid == 0 && k + kRingS < nck) {
+            // refill the slot once all eight warps released it
+            mbar_wait(&sm.empty[slot], (uint32_t)((k / kRingS) & 1));
+            fence_proxy_async();
+            mbar_expect_tx(&sm.full[slot], kWB);
+            bulk_g2s(&sm.win[slot][0], win + (cbeg + k + kRingS) * kWD, kWB, &sm.full[slot]);
+        }
+        w_cur = w_nxt;
+    }
+    if (cur_key >= 0) flush();
+}
+
 template <int MODE, class Epi>
 void launch(const PointSet& ps, const double* gin, double* gout, const double* w, const FastParams& fp,
             const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
@@ -513,7 +630,26 @@ void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* gr
 }
 
 void fused3d_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
-    launch<1, EpiNone>(ps, nullptr, grid, w, fp, EpiNone{}, nullptr, s, kProfSpread);
+    static const bool ring = [] {
+        const char* e = getenv("UOTK_SPREAD_RING");
+        return !(e && e[0] == '0');
+    }();
+    if (!ring) {
+        launch<1, EpiNone>(ps, nullptr, grid, w, fp, EpiNone{}, nullptr, s, kProfSpread);
+        return;
+    }
+    if (ps.n == 0 || ps.nchunks == 0) return;
+    ProfScope prof(kProfSpread, s);
+    if (ps.chunk_kz == 24) {
+        set_smem_attr((const void*)spread3d_k<24>, (int)sizeof(SmemS<24>));
+        spread3d_k<24><<<ps.chunk_blocks, kThreads, sizeof(SmemS<24>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                            ps.chunk_bounds.p, fp.ng, grid, w);
+    } else {
+        set_smem_attr((const void*)spread3d_k<16>, (int)sizeof(SmemS<16>));
+        spread3d_k<16><<<ps.chunk_blocks, kThreads, sizeof(SmemS<16>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                            ps.chunk_bounds.p, fp.ng, grid, w);
+    }
+    UOTK_LAUNCHED();
 }
 
 void fused3d_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
