@@ -32,63 +32,50 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
         desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r], 0);
 }
 
-// window block of every chunk (layout per d: chunks.cuh), d <= 2
-template <int D>
-__global__ void chunk_window_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
-                               KBWindow w, double* __restrict__ out) {
-    constexpr int kW = chunk_win_doubles(D);
-    constexpr int kRow = kChunkT;
-    const int64_t c = blockIdx.x;
-    const int4 dsc = desc[c];
-    double* o = out + c * kW;
-    for (int e = threadIdx.x; e < kW; e += blockDim.x) {
-        const int ax = e / (kChunk * kRow);
-        const int r = e - ax * kChunk * kRow;
-        const int p = r / kRow;
-        const int col = r - p * kRow;
-        // tap stored at this column
-        const int a = D == 2 ? ((col - 4 * p) & 15) : col;
-        double val = 0.0;
-        if (p < dsc.y) {
-            const double ut = u[ax * n + dsc.x + p];
-            val = kb_phi(ut - floor(ut) + (double)(kChunkM - 1 - a), w);
-        }
-        o[e] = val;
-    }
-}
+// Window blocks (layout per d: chunks.cuh).  One warp per (chunk, axis): lane p loads
+// its point's coordinate once and evaluates its row of taps phi(f + m - 1 - a); the rows
+// are staged in shared memory and written out coalesced.  KZ (d = 3 only): width of the
+// z rows (16, or 24 for z-segment groups: the 16 taps sit at the cell's offset).
+constexpr int kWinWarps = 4;
+constexpr int kMaxRow = 28;  // widest row stride (d = 3, KZ = 24)
 
-// d = 3: X and Y rows of 16 taps (stride 20); Z rows of KZ columns (stride ZS) holding the
-// 16 z-taps at the point's cell offset within the group's z-segment (0 for KZ = 16)
-template <int KZ>
-__global__ void chunk_window3_k(const int4* __restrict__ desc, const double* __restrict__ u,
-                                const int32_t* __restrict__ key, int64_t n, KBWindow w, double* __restrict__ out) {
-    constexpr int ZS = chunk_zstride3(KZ);
-    constexpr int kW = chunk_win3_doubles(KZ);
-    constexpr int kXY = 2 * kChunk * kStride3;
-    const int64_t c = blockIdx.x;
+template <int D, int KZ>
+__global__ void __launch_bounds__(kWinWarps * 32)
+chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u, const int32_t* __restrict__ key,
+                    int64_t n, int64_t nchunks, KBWindow w, double* __restrict__ out) {
+    __shared__ double stage[kWinWarps][kChunk * kMaxRow];
+    constexpr int kW = D == 3 ? chunk_win3_doubles(KZ) : chunk_win_doubles(D);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t job = blockIdx.x * (int64_t)kWinWarps + warp;  // (chunk, axis)
+    if (job >= nchunks * D) return;
+    const int64_t c = job / D;
+    const int ax = (int)(job - c * D);
     const int4 dsc = desc[c];
-    double* o = out + c * kW;
-    for (int e = threadIdx.x; e < kW; e += blockDim.x) {
-        int ax, p, a;
-        if (e < kXY) {
-            ax = e / (kChunk * kStride3);
-            const int r = e - ax * kChunk * kStride3;
-            p = r / kStride3;
-            a = r - p * kStride3;
-        } else {
-            ax = 2;
-            const int r = e - kXY;
-            p = r / ZS;
-            a = r - p * ZS;  // column of the placed row
-            if (KZ != 16 && p < dsc.y) a -= key[dsc.x + p] - dsc.z;  // minus the cell's z offset
-        }
-        double val = 0.0;
-        if (p < dsc.y && a >= 0 && a < kChunkT) {
-            const double ut = u[ax * n + dsc.x + p];
-            val = kb_phi(ut - floor(ut) + (double)(kChunkM - 1 - a), w);
-        }
-        o[e] = val;
+    // row stride and offset of this axis' matrix inside the chunk block
+    const int stride = D == 3 ? (ax == 2 ? chunk_zstride3(KZ) : kStride3) : kChunkT;
+    const int64_t base = c * kW + (int64_t)ax * kChunk * (D == 3 ? kStride3 : kChunkT);
+    double* st = stage[warp];
+    const int p = lane;
+    double f = 0.0;
+    int off = 0;  // first column of the taps in this row
+    const bool live = p < dsc.y;
+    if (live) {
+        const double ut = u[ax * n + dsc.x + p];
+        f = ut - floor(ut);
+        if (D == 3 && ax == 2 && KZ != 16) off = key[dsc.x + p] - dsc.z;
     }
+    for (int col = 0; col < stride; ++col) {
+        int a;
+        if (D == 2) a = (col - 4 * p) & 15;  // swizzled column -> tap
+        else a = col - off;
+        double v = 0.0;
+        if (live && a >= 0 && a < kChunkT) v = kb_phi(f + (double)(kChunkM - 1 - a), w);
+        st[p * stride + col] = v;
+    }
+    __syncwarp();
+    double* o = out + base;
+    for (int e = lane; e < kChunk * stride; e += 32) o[e] = st[e];
 }
 
 // group key of a z-segment: the cell key with its z index rounded down to a multiple of kSegZ
@@ -253,14 +240,19 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     const KBWindow win = make_window(fp.b, kChunkM);
     {
         ProfScope prof(kProfSetup, s);
+        const unsigned wb = (unsigned)((nchunks * d + kWinWarps - 1) / kWinWarps);
         if (d == 3 && kz == 24)
-            chunk_window3_k<24><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, win,
-                                                                   ps.chunk_win.p);
+            chunk_window_rows_k<3, 24><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, ps.chunk_win.p);
         else if (d == 3)
-            chunk_window3_k<16><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, win,
-                                                                   ps.chunk_win.p);
-        else if (d == 2) chunk_window_k<2><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
-        else chunk_window_k<1><<<(unsigned)nchunks, 256, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.n, win, ps.chunk_win.p);
+            chunk_window_rows_k<3, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, ps.chunk_win.p);
+        else if (d == 2)
+            chunk_window_rows_k<2, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, ps.chunk_win.p);
+        else
+            chunk_window_rows_k<1, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, ps.chunk_win.p);
         UOTK_LAUNCHED();
     }
     // cost-balanced static partition of the chunks over the work units
