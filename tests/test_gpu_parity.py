@@ -569,3 +569,14 @@ def test_fft_chain_vs_separable_chain(uk, d):
     beta, gamma, res = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=iters,
                                        opts={"method": "nfft", "flags": uk.FLAG_FFT})
     _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("method", ["direct", "nfft"])
+def test_uot_d1(uk, method):
+    """UOT in d = 1 (C1's distributions and parameters on a line): the d = 1 cell-group
+    half-step and the separable chain by default."""
+    pr = W.c1_uot(n=2000, m=1500, d=1)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, 30)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=30,
+                                       opts={"method": method})
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
