@@ -1,4 +1,5 @@
 // Library context: errors, stream-ordered buffers, host/device staging, cuFFT plan cache.
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <map>
@@ -283,6 +284,8 @@ struct Context {
     std::map<std::tuple<int, int, int>, std::pair<cufftHandle, cufftHandle>> fft;
     bool pool_configured[64] = {};
     std::map<int, cublasHandle_t> blas;
+    // (device, n, w, H) -> pruned-transform plans (pass z R2C, pass y C2C, pass x C2C)
+    std::map<std::tuple<int, int, int, int>, std::array<cufftHandle, 3>> pruned;
     std::map<int, cudaStream_t> streams;
 };
 
@@ -330,6 +333,30 @@ void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r) {
     c.fft[key] = {a, b};
     *r2c = a;
     *c2r = b;
+}
+
+void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cufftHandle* px) {
+    int dev = 0;
+    UOTK_CUDA(cudaGetDevice(&dev));
+    Context& c = ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto key = std::make_tuple(dev, n, w, H);
+    auto it = c.pruned.find(key);
+    if (it == c.pruned.end()) {
+        std::array<cufftHandle, 3> h{};
+        int len = n;
+        const int half = n / 2 + 1;
+        // z: R2C of the w * n rows g[o + x'][y][.], contiguous
+        UOTK_CUFFT(cufftPlanMany(&h[0], 1, &len, nullptr, 1, n, nullptr, 1, half, CUFFT_D2Z, w * n));
+        // y: C2C of w * (H + 1) rows of length n
+        UOTK_CUFFT(cufftPlanMany(&h[1], 1, &len, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, w * (H + 1)));
+        // x: C2C of (2H + 1) * (H + 1) rows of length n
+        UOTK_CUFFT(cufftPlanMany(&h[2], 1, &len, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, (2 * H + 1) * (H + 1)));
+        it = c.pruned.emplace(key, h).first;
+    }
+    *pz = it->second[0];
+    *py = it->second[1];
+    *px = it->second[2];
 }
 
 void get_cublas(void** handle) {

@@ -3,6 +3,7 @@
 // (forward NFFT, outer sum of (4.6)) — P:590-592.  These are the simple
 // thread-per-point kernels; the tuned cell-group kernels live in fused3d.cu / fused12d.cu.
 #include <cublas_v2.h>
+#include <cstdlib>
 
 #include <string>
 #include <utility>
@@ -365,9 +366,125 @@ __global__ void spectrum_energy_k(const double2* __restrict__ spec, const double
 // <g', g> for g' = the NFFT interpolant of the spread grid g: the quadratic form
 // sum_ij w_i w_j K_RK(z_i - z_j) of (3.5) in the Fourier domain, sum_k D_k |G_k|^2
 // (identical to spreading, FFT, D_k, inverse FFT, gathering and summing w_i t_i).
+namespace {
+
+// T1 [x'][y][kz] (kz < n/2 + 1) -> T1c [x'][kz][y] for kz <= H (32 x 32 tiles per x')
+__global__ void prune_t1_k(const double2* __restrict__ t1, int n, int H, double2* __restrict__ t1c) {
+    __shared__ double2 tile[32][33];
+    const int xp = blockIdx.z;
+    const int y0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int half = n / 2 + 1;
+    const double2* src = t1 + (int64_t)xp * n * half;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int y = y0 + i, kz = k0 + threadIdx.x;
+        tile[i][threadIdx.x] = (y < n && kz <= H) ? src[(int64_t)y * half + kz] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double2* dst = t1c + (int64_t)xp * (H + 1) * n;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int kz = k0 + i, y = y0 + threadIdx.x;
+        if (kz <= H && y < n) dst[(int64_t)kz * n + y] = tile[threadIdx.x][i];
+    }
+}
+
+// T2 [x'][kz][ky (all n)] -> T2c [ky' = ky + H][kz][o + x'] for |ky| <= H (tiles of (x', ky) per kz)
+__global__ void prune_t2_k(const double2* __restrict__ t2, int n, int H, int w, int o, double2* __restrict__ t2c) {
+    __shared__ double2 tile[32][33];
+    const int kz = blockIdx.z;
+    const int x0 = blockIdx.x * 32, j0 = blockIdx.y * 32;  // j = ky' in [0, 2H]
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int xp = x0 + i, j = j0 + threadIdx.x;
+        double2 v = make_double2(0.0, 0.0);
+        if (xp < w && j <= 2 * H) {
+            const int ky = j - H;
+            const int q = ky < 0 ? ky + n : ky;
+            v = t2[((int64_t)xp * (H + 1) + kz) * n + q];
+        }
+        tile[i][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int j = j0 + i, xp = x0 + threadIdx.x;
+        if (j <= 2 * H && xp < w) t2c[((int64_t)j * (H + 1) + kz) * n + o + xp] = tile[threadIdx.x][i];
+    }
+}
+
+// partial sums of sum D_k |G_k|^2 over kx, ky in [-H, H], kz in [0, H] (weight 2 for kz > 0)
+__global__ void pruned_energy_k(const double2* __restrict__ t3, const double* __restrict__ Dk, int n, int N,
+                                double* __restrict__ part) {
+    __shared__ double sm[256];
+    const int H = N / 2;
+    const int64_t total = (int64_t)(2 * H + 1) * (H + 1) * (2 * H + 1);
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int jx = (int)(i % (2 * H + 1));
+        const int64_t r = i / (2 * H + 1);
+        const int kz = (int)(r % (H + 1));
+        const int jy = (int)(r / (H + 1));
+        const int kx = jx - H;
+        const int qx = kx < 0 ? kx + n : kx;
+        const double2 v = t3[((int64_t)jy * (H + 1) + kz) * n + qx];
+        const double d = Dk[((int64_t)jx * (N + 1) + jy) * (H + 1) + kz];
+        acc += (kz == 0 ? 1.0 : 2.0) * d * (v.x * v.x + v.y * v.y);
+    }
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s2 = 128; s2 > 0; s2 >>= 1) {
+        if (threadIdx.x < s2) sm[threadIdx.x] += sm[threadIdx.x + s2];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+}  // namespace
+
+// sum_k D_k |G_k|^2 by a pruned 3-D transform: the grid is zero outside the footprint box
+// [o, o + w)^3 and D_k vanishes outside |k_t| <= N/2, so the z-pass transforms only the
+// w n rows of the box slab, the y-pass only the w (N/2 + 1) rows with kept kz, and the
+// x-pass only the (N + 1)(N/2 + 1) rows with kept (ky, kz) (C2-IMQ: ~20% of the full
+// transform's rows).  The intermediates live in `spec`.
+static void spectrum_energy_pruned(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts,
+                                   cudaStream_t s, void* comm) {
+    const FastParams& fp = sp.fp;
+    const int n = fp.ng, o = fp.box_lo, w = fp.box_w, N = fp.N, H = N / 2;
+    cufftHandle pz, py, px;
+    get_pruned_plans(n, w, H, &pz, &py, &px);
+    const int half = n / 2 + 1;
+    double2* t1 = spec;                                           // w n half
+    double2* t1c = t1 + (size_t)w * n * half;                     // w (H+1) n
+    double2* t2c = t1c + (size_t)w * (H + 1) * n;                 // (2H+1)(H+1) n
+    UOTK_CUFFT(cufftSetStream(pz, s));
+    UOTK_CUFFT(cufftSetStream(py, s));
+    UOTK_CUFFT(cufftSetStream(px, s));
+    UOTK_CUFFT(cufftExecD2Z(pz, grid + (size_t)o * n * n, (cufftDoubleComplex*)t1));
+    dim3 tb(32, 8);
+    prune_t1_k<<<dim3((n + 31) / 32, (H + 32) / 32, w), tb, 0, s>>>(t1, n, H, t1c);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2Z(py, (cufftDoubleComplex*)t1c, (cufftDoubleComplex*)t1c, CUFFT_FORWARD));
+    UOTK_CUDA(cudaMemsetAsync(t2c, 0, (size_t)(2 * H + 1) * (H + 1) * n * sizeof(double2), s));
+    prune_t2_k<<<dim3((w + 31) / 32, (2 * H + 1 + 31) / 32, H + 1), tb, 0, s>>>(t1c, n, H, w, o, t2c);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2Z(px, (cufftDoubleComplex*)t2c, (cufftDoubleComplex*)t2c, CUFFT_FORWARD));
+    add_launches(3);
+    if (comm) comm_allreduce_spectrum(t2c, (size_t)(2 * H + 1) * (H + 1) * n, comm, s);
+    pruned_energy_k<<<nparts, 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N, part);
+    UOTK_LAUNCHED();
+}
+
 void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
                      void* comm) {
     const FastParams& fp = sp.fp;
+    static const bool pruned = [] {
+        const char* e = getenv("UOTK_PRUNED_FFT");
+        return !(e && e[0] == '0');
+    }();
+    const size_t need = (size_t)fp.box_w * fp.ng * (fp.ng / 2 + 1) + (size_t)fp.box_w * (fp.N / 2 + 1) * fp.ng +
+                        (size_t)(fp.N + 1) * (fp.N / 2 + 1) * fp.ng;
+    if (pruned && fp.d == 3 && !(fp.flags & UOTK_FLAG_FFT) && need <= sp.spec_elems) {
+        ProfScope ps_(kProfFft, s);
+        spectrum_energy_pruned(sp, grid, spec, part, nparts, s, comm);
+        return;
+    }
     ProfScope ps_(kProfFft, s);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
