@@ -429,8 +429,14 @@ def c4_leg(uk, world, rank, comm, dev, barrier):
         per_launch_bytes = (len(x) + len(y)) / 2 * 288  # one half-step visits one point set
         achieved = per_launch_bytes / (avg / 1e3) / 1e9
         peak = hbm_peak()
-        roof = {"bound": "hbm", "kernel": "chunked2d_k<0> (fused d=2 half-step)", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "avg_launch_ms": avg,
+        traffic = None
+        try:
+            with open(TRAFFIC_FILE) as f:
+                traffic = json.load(f).get("fused2d")
+        except (OSError, ValueError):
+            pass
+        roof = {"bound": "hbm", "kernel": "sinkhorn2d_ws_k (fused d=2 half-step)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "avg_launch_ms": avg,
                 "launches_per_solve": fcnt, "share_of_solve": fms / sum(v[0] for v in prof.values())}
     return {"metric": "UOT Sinkhorn iterations/s", "value": pr.iters * steps / (ms / 1e3), "unit": "iterations/s",
             "ms_per_solve": ms / steps, "solve_ms": [round(v, 2) for v in per],
