@@ -105,6 +105,15 @@ bool capturing(cudaStream_t s) {
 
 size_t round_bytes(size_t b) { return (b + 4095) & ~size_t(4095); }
 
+// Give a cached block back to the pool.  The stream that freed it may no longer exist
+// (a caller's stream), so wait for its event on the host and free on the legacy stream.
+void release_block(const CachedBlock& b) {
+    cudaEventSynchronize(b.ev);
+    cudaFreeAsync(b.p, 0);
+    cudaEventDestroy(b.ev);
+    cudaGetLastError();
+}
+
 void* cache_alloc(size_t bytes, cudaStream_t s, bool* from_pool) {
     bytes = round_bytes(bytes);
     *from_pool = capturing(s);
@@ -163,9 +172,7 @@ void cache_free(void* p, size_t bytes, cudaStream_t s, bool from_pool) {
         CachedBlock b = g_cache.front();
         g_cache.erase(g_cache.begin());
         g_cache_bytes -= b.bytes;
-        cudaStreamWaitEvent(b.s, b.ev, 0);
-        cudaFreeAsync(b.p, b.s);
-        cudaEventDestroy(b.ev);
+        release_block(b);
     }
 }
 }  // namespace
@@ -197,10 +204,8 @@ void block_cache_release() {
             ++i;
             continue;
         }
-        cudaStreamWaitEvent(b.s, b.ev, 0);
-        cudaFreeAsync(b.p, b.s);
-        cudaEventDestroy(b.ev);
         g_cache_bytes -= b.bytes;
+        release_block(b);
         g_cache.erase(g_cache.begin() + i);
     }
 }
