@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-mmd", action="store_true")
     p.add_argument("--no-c4", action="store_true", help="skip the C4 (d=2, 16M points) side leg")
+    p.add_argument("--no-c1", action="store_true", help="skip the C1 (d=2, 1000 points) side leg")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ncu", action="store_true", help="short run for ncu launch lists (no side legs)")
     return p.parse_args()
@@ -250,6 +251,8 @@ def main_ours(args):
             out["mmd2"] = mmd_leg(uk, world, rank, comm, dev, barrier)
         if not args.no_c4 and args.workload == "C3":
             out["c4"] = c4_leg(uk, world, rank, comm, dev, barrier)
+        if not args.no_c1 and args.workload == "C3" and world == 1:
+            out["c1"] = c1_leg(uk, dev)
     if rank == 0:
         line = {
             "metric": "UOT Sinkhorn iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
@@ -443,6 +446,35 @@ def c4_leg(uk, world, rank, comm, dev, barrier):
             "config": f"C4: UOT d=2 n=m={len(pr.x)} eps={pr.eps} lam={pr.lam} "
             f"iters={pr.iters} (median of 3 whole solves incl. setup, inputs in HBM)",
             "n_grid": res.info["n_grid"], "N": res.info["N"], "plan_mass": res.plan_mass, "roofline": roof}
+
+
+def c1_leg(uk, dev):
+    """C1 (BASELINE.json configs[0]): UOT d=2, n=m=1000, eps=0.05, lam=1, 100 iterations —
+    whole solves, device-timed (median of 5), with the AUTO choice (the direct kernel at
+    1e6 pairs per sum) and with the NFFT path; both replay the iteration from CUDA graphs."""
+    import torch
+    pr = W.c1_uot()
+    args = [torch.from_numpy(v).to(dev) for v in (pr.x, pr.a, pr.y, pr.b)]
+    stream = torch.cuda.current_stream()
+    out = {"metric": "UOT Sinkhorn iterations/s", "unit": "iterations/s",
+           "config": f"C1: UOT d=2 n=m={len(pr.x)} eps={pr.eps} lam={pr.lam} iters={pr.iters} (whole solves)"}
+    for method in ("auto", "nfft"):
+        def solve():
+            return uk.uot_sinkhorn(*args, pr.eps, pr.lam, iters=pr.iters, opts={"method": method})
+        for _ in range(3):
+            solve()
+        torch.cuda.synchronize()
+        per = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, _, res = solve()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per.append(e0.elapsed_time(e1))
+        ms = statistics.median(per)
+        out[method] = {"value": pr.iters / (ms / 1e3), "ms_per_solve": ms, "method_used": res.info["method"]}
+    return out
 
 
 def hbm_peak():
