@@ -592,6 +592,153 @@ spread3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
     if (cur_key >= 0) flush();
 }
 
+// ---------------------------------------------------------------- gather only, ring
+// The forward NFFT alone (kernel sums' targets): per chunk every warp contracts its
+// a-pair and writes 32 partial sums; the warp k mod 8 waits for all eight (mbarrier),
+// reduces, applies the epilogue and — the slot being free then — refills it by TMA.
+// No CTA barrier; the reduction duty rotates over the warps.
+constexpr int kRingG = 4;
+template <int KZ>
+struct __align__(128) SmemG {
+    double win[kRingG][chunk_win3_doubles(KZ)];
+    double red[kRingG][kThreads / 32][kChunk];
+    unsigned long long full[kRingG];
+    unsigned long long red_full[kRingG];
+};
+
+template <int KZ, class Epi>
+__global__ void __launch_bounds__(kThreads, kBlocksPerSM)
+gather3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds, int ng,
+           const double* __restrict__ grid_in, Epi epi) {
+    constexpr int KS = KZ / 4;
+    constexpr int ZS = chunk_zstride3(KZ);
+    constexpr int kWD = chunk_win3_doubles(KZ);
+    constexpr uint32_t kWB = kWD * sizeof(double);
+    constexpr int kW = kThreads / 32;
+    extern __shared__ __align__(128) unsigned char g_raw[];
+    SmemG<KZ>& sm = *reinterpret_cast<SmemG<KZ>*>(g_raw);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int gq = lane >> 2;
+    const int tq = lane & 3;
+    const int a0 = 2 * warp;
+    const int64_t cbeg = bounds[blockIdx.x];
+    const int64_t nck = bounds[blockIdx.x + 1] - cbeg;
+    const int64_t ng2 = (int64_t)ng * ng;
+    if (tid == 0) {
+        for (int r = 0; r < kRingG; ++r) {
+            mbar_init(&sm.full[r], 1);
+            mbar_init(&sm.red_full[r], kW);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 0; k < kRingG && k < nck; ++k) {
+            mbar_expect_tx(&sm.full[k], kWB);
+            bulk_g2s(&sm.win[k][0], win + (cbeg + k) * kWD, kWB, &sm.full[k]);
+        }
+    }
+    auto origin = [&](int32_t kk) -> int64_t {
+        const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
+        return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
+    };
+    double Fb[4][KS];
+    int32_t cur_key = -1;
+    int4 d0 = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
+    int4 d1 = nck > 1 ? desc[cbeg + 1] : make_int4(0, 0, -1, 0);
+    for (int64_t k = 0; k < nck; ++k) {
+        const int slot = (int)(k % kRingG);
+        const int4 dsc = d0;
+        d0 = d1;
+        if (k + 2 < nck) d1 = desc[cbeg + k + 2];
+        if (dsc.z != cur_key) {
+            cur_key = dsc.z;
+            const int64_t gorg = origin(cur_key);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const int64_t row = gorg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) Fb[nt][ks] = __ldg(grid_in + row + 4 * ks + tq);
+            }
+        }
+        if (k + 1 < nck && d0.z != cur_key) {  // warm L1 with the next group's footprint
+            const int64_t norg = origin(d0.z);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const double* rowp = grid_in + norg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rowp + 4 * tq));
+            }
+        }
+        mbar_wait(&sm.full[slot], (uint32_t)((k / kRingG) & 1));
+        const double(*wx)[kStride] = reinterpret_cast<const double(*)[kStride]>(&sm.win[slot][0]);
+        const double(*wy)[kStride] = wx + kChunk;
+        const double(*wz)[ZS] = reinterpret_cast<const double(*)[ZS]>(&sm.win[slot][2 * kChunk * kStride]);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int p = 8 * mt + gq;
+            double acc[4][2];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const double az = wz[p][4 * ks + tq];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) dmma(acc[nt][0], acc[nt][1], az, Fb[nt][ks]);
+            }
+            const double2 ylo = *reinterpret_cast<const double2*>(&wy[p][2 * tq]);
+            const double2 yhi = *reinterpret_cast<const double2*>(&wy[p][8 + 2 * tq]);
+            const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+            const double xv[2] = {xa.x, xa.y};
+            double part = 0.0;
+#pragma unroll
+            for (int al = 0; al < 2; ++al) {
+                double q = acc[2 * al][0] * ylo.x;
+                q = fma(acc[2 * al][1], ylo.y, q);
+                q = fma(acc[2 * al + 1][0], yhi.x, q);
+                q = fma(acc[2 * al + 1][1], yhi.y, q);
+                part = fma(q, xv[al], part);
+            }
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if (tq == 0) sm.red[slot][warp][p] = part;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.red_full[slot]);
+        if (warp == (int)(k % kW)) {
+            // reducer of chunk k: all eight partials, the epilogue, then the slot is free
+            mbar_wait(&sm.red_full[slot], (uint32_t)((k / kRingG) & 1));
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) t += sm.red[slot][w][lane];
+            if (lane < dsc.y) epi(dsc.x + lane, t);
+            __syncwarp();
+            if (lane == 0 && k + kRingG < nck) {
+                fence_proxy_async();
+                mbar_expect_tx(&sm.full[slot], kWB);
+                bulk_g2s(&sm.win[slot][0], win + (cbeg + k + kRingG) * kWD, kWB, &sm.full[slot]);
+            }
+        }
+    }
+}
+
+template <class Epi>
+void launch_gather(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi, cudaStream_t s) {
+    if (ps.n == 0 || ps.nchunks == 0) return;
+    ProfScope prof(kProfGather, s);
+    if (ps.chunk_kz == 24) {
+        set_smem_attr((const void*)gather3d_k<24, Epi>, (int)sizeof(SmemG<24>));
+        gather3d_k<24, Epi><<<ps.chunk_blocks, kThreads, sizeof(SmemG<24>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                               ps.chunk_bounds.p, fp.ng, grid, epi);
+    } else {
+        set_smem_attr((const void*)gather3d_k<16, Epi>, (int)sizeof(SmemG<16>));
+        gather3d_k<16, Epi><<<ps.chunk_blocks, kThreads, sizeof(SmemG<16>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                               ps.chunk_bounds.p, fp.ng, grid, epi);
+    }
+    UOTK_LAUNCHED();
+}
+
 template <int MODE, class Epi>
 void launch(const PointSet& ps, const double* gin, double* gout, const double* w, const FastParams& fp,
             const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
@@ -654,6 +801,11 @@ void fused3d_spread(const PointSet& ps, const double* w, double* grid, const Fas
 
 void fused3d_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
                           cudaStream_t s) {
+    static const bool ring = [] {
+        const char* e = getenv("UOTK_GATHER_RING");
+        return !(e && e[0] == '0');
+    }();
+    if (ring) return launch_gather(ps, grid, fp, epi, s);
     EpiGatherOnly<EpiStore> e;
     static_cast<EpiStore&>(e) = epi;
     launch<2, EpiGatherOnly<EpiStore>>(ps, grid, nullptr, nullptr, fp, e, nullptr, s, kProfGather);
@@ -661,6 +813,11 @@ void fused3d_gather_store(const PointSet& ps, const double* grid, const FastPara
 
 void fused3d_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
                         cudaStream_t s) {
+    static const bool ring = [] {
+        const char* e = getenv("UOTK_GATHER_RING");
+        return !(e && e[0] == '0');
+    }();
+    if (ring) return launch_gather(ps, grid, fp, epi, s);
     EpiGatherOnly<EpiDot> e;
     static_cast<EpiDot&>(e) = epi;
     launch<2, EpiGatherOnly<EpiDot>>(ps, grid, nullptr, nullptr, fp, e, nullptr, s, kProfGather);
