@@ -99,10 +99,10 @@ typedef struct {
 /* opts.flags: which spread/gather kernels the NFFT path may use (results agree to
  * rounding; for cross-checks and benchmarks).  By default the cell-group kernels
  * (points sorted by cell, chunks of <= 32 points sharing one window footprint,
- * DESIGN.md §7) run whenever m = 8 and the point set is dense enough, else the
+ * DESIGN.md §7) run whenever m = 8 (or m = 6 in d = 3) and the point set is dense enough, else the
  * generic thread-per-point kernels.  At most one of the two bits may be set. */
 #define UOTK_FLAG_GENERIC 1  /* always the generic thread-per-point kernels          */
-#define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m must be 8)     */
+#define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m = 8; d = 3: or 6) */
 #define UOTK_FLAG_TRANSPORT 4 /* uot: also evaluate the transport term <pi, d^2>    */
 #define UOTK_FLAG_FFT 8       /* always the cuFFT chain (D2Z, D_k, Z2D), never the separable
                                  circulant GEMMs of the Gaussian (which run on one rank only) */

@@ -35,14 +35,15 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
 // Window blocks (layout per d: chunks.cuh).  One warp per (chunk, axis): lane p loads
 // its point's coordinate once and evaluates its row of taps phi(f + m - 1 - a); the rows
 // are staged in shared memory and written out coalesced.  KZ (d = 3 only): width of the
-// z rows (16, or 24 for z-segment groups: the 16 taps sit at the cell's offset).
+// z rows (16, or 24 for z-segment groups: the 16 taps sit at the cell's offset).  m: the
+// window half-width (8; or 6 in d = 3, whose 12 taps fill columns 0..11 of the same layout).
 constexpr int kWinWarps = 4;
 constexpr int kMaxRow = 28;  // widest row stride (d = 3, KZ = 24)
 
 template <int D, int KZ>
 __global__ void __launch_bounds__(kWinWarps * 32)
 chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u, const int32_t* __restrict__ key,
-                    int64_t n, int64_t nchunks, KBWindow w, double* __restrict__ out) {
+                    int64_t n, int64_t nchunks, KBWindow w, int m, double* __restrict__ out) {
     __shared__ double stage[kWinWarps][kChunk * kMaxRow];
     constexpr int kW = D == 3 ? chunk_win3_doubles(KZ) : chunk_win_doubles(D);
     const int lane = threadIdx.x & 31;
@@ -53,8 +54,8 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
     const int ax = (int)(job - c * D);
     const int4 dsc = desc[c];
     // row stride and offset of this axis' matrix inside the chunk block
-    const int stride = D == 3 ? (ax == 2 ? chunk_zstride3(KZ) : kStride3) : kChunkT;
-    const int64_t base = c * kW + (int64_t)ax * kChunk * (D == 3 ? kStride3 : kChunkT);
+    const int stride = D == 3 ? (ax == 2 ? chunk_zstride3(KZ) : chunk_xstride3(KZ)) : kChunkT;
+    const int64_t base = c * kW + (int64_t)ax * kChunk * (D == 3 ? chunk_xstride3(KZ) : kChunkT);
     double* st = stage[warp];
     const int p = lane;
     double f = 0.0;
@@ -63,14 +64,14 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
     if (live) {
         const double ut = u[ax * n + dsc.x + p];
         f = ut - floor(ut);
-        if (D == 3 && ax == 2 && KZ != 16) off = key[dsc.x + p] - dsc.z;
+        if (D == 3 && ax == 2 && KZ == 24) off = key[dsc.x + p] - dsc.z;
     }
     for (int col = 0; col < stride; ++col) {
         int a;
         if (D == 2) a = (col - 4 * p) & 15;  // swizzled column -> tap
         else a = col - off;
         double v = 0.0;
-        if (live && a >= 0 && a < kChunkT) v = kb_phi(f + (double)(kChunkM - 1 - a), w);
+        if (live && a >= 0 && a < 2 * m) v = kb_phi(f + (double)(m - 1 - a), w);
         st[p * stride + col] = v;
     }
     __syncwarp();
@@ -116,7 +117,9 @@ __global__ void chunk_bounds_k(const int32_t* __restrict__ prefix, int64_t nchun
 
 }  // namespace
 
-bool chunked_available(const FastParams& fp) { return fp.m == kChunkM && fp.d >= 1 && fp.d <= 3; }
+bool chunked_available(const FastParams& fp) {
+    return (fp.m == kChunkM && fp.d >= 1 && fp.d <= 3) || (fp.m == 6 && fp.d == 3);
+}
 
 // Build the chunk list and the per-chunk window blocks (once per point set).  Chunks pad
 // runs to multiples of 32 slots; when the padding would waste too much work (sparse
@@ -166,10 +169,10 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     const bool forced = fp.flags & UOTK_FLAG_CHUNKED;
     // d = 3 sparse clouds: group z-segments of kSegZ cells when that needs sufficiently
     // fewer chunks (each costs 1.5x a one-cell chunk: 24 instead of 16 z-columns)
-    int kz = 16;
+    int kz = fp.m == 6 ? 12 : 16;
     double chunk_cost = 1.0;
     DevBuf<int32_t> gk;
-    if (d == 3 && (double)n < 0.5 * kChunk * (double)nchunks) {
+    if (d == 3 && fp.m == kChunkM && (double)n < 0.5 * kChunk * (double)nchunks) {
         gk.alloc(n, s);
         segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, gk.p);
         UOTK_LAUNCHED();
@@ -237,22 +240,25 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
                                                         ps.chunk_desc.p);
     UOTK_LAUNCHED();
-    const KBWindow win = make_window(fp.b, kChunkM);
+    const KBWindow win = make_window(fp.b, fp.m);
     {
         ProfScope prof(kProfSetup, s);
         const unsigned wb = (unsigned)((nchunks * d + kWinWarps - 1) / kWinWarps);
-        if (d == 3 && kz == 24)
+        if (d == 3 && kz == 12)
+            chunk_window_rows_k<3, 12><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, fp.m, ps.chunk_win.p);
+        else if (d == 3 && kz == 24)
             chunk_window_rows_k<3, 24><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, ps.chunk_win.p);
+                                                                      win, fp.m, ps.chunk_win.p);
         else if (d == 3)
             chunk_window_rows_k<3, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, ps.chunk_win.p);
+                                                                      win, fp.m, ps.chunk_win.p);
         else if (d == 2)
             chunk_window_rows_k<2, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, ps.chunk_win.p);
+                                                                      win, fp.m, ps.chunk_win.p);
         else
             chunk_window_rows_k<1, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, ps.chunk_win.p);
+                                                                      win, fp.m, ps.chunk_win.p);
         UOTK_LAUNCHED();
     }
     // cost-balanced static partition of the chunks over the work units
@@ -262,7 +268,8 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
         UOTK_CUDA(cudaGetDevice(&dev));
         UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int nb = (int)std::min<int64_t>((int64_t)sms * chunk_units_per_sm(d), nchunks);
+    const bool m6 = d == 3 && fp.m == 6;
+    const int nb = (int)std::min<int64_t>((int64_t)sms * (m6 ? kCtas3M6 : chunk_units_per_sm(d)), nchunks);
     DevBuf<int32_t> cost(nchunks, s), prefix(nchunks, s);
     chunk_cost_k<<<blocks_for(nchunks, 256), 256, 0, s>>>(ps.chunk_desc.p, nchunks, d == 3 ? 2 : 1, cost.p);
     UOTK_LAUNCHED();
@@ -273,8 +280,8 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     add_launches(1);
     ps.chunk_bounds.alloc(nb + 1, s);
     chunk_bounds_k<<<blocks_for(nb + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nb, ps.chunk_bounds.p);
-    if (d == 2) {
-        const int nw = (int)std::min<int64_t>((int64_t)sms * kUnitsWS2 * kCtasWS2, nchunks);
+    if (d == 2 || m6) {
+        const int nw = (int)std::min<int64_t>((int64_t)sms * (m6 ? kCtasWS3M6 : kUnitsWS2 * kCtasWS2), nchunks);
         ps.chunk_bounds_ws.alloc(nw + 1, s);
         chunk_bounds_k<<<blocks_for(nw + 1, 256), 256, 0, s>>>(prefix.p, nchunks, nw, ps.chunk_bounds_ws.p);
         UOTK_LAUNCHED();

@@ -26,6 +26,9 @@ constexpr int kWarps1 = 8, kCtas1 = 2;
 // d = 2 warp-specialised Sinkhorn half-step: units of 2 gather warps + 1 spread warp,
 // kUnitsWS2 units per CTA, kCtasWS2 CTAs per SM, its own chunk partition
 constexpr int kUnitsWS2 = 2, kCtasWS2 = 2;
+// d = 3, m = 6 (fused3d_m6.cu): stand-alone spread/gather CTAs of 3 warps, kCtas3M6 per SM
+// (chunk_bounds); warp-specialised half-step CTAs of 3 + 3 warps, kCtasWS3M6 per SM (chunk_bounds_ws)
+constexpr int kCtas3M6 = 5, kCtasWS3M6 = 3;
 __host__ __device__ constexpr int chunk_units_per_sm(int d) {
     return d == 3 ? kCtas3 : (d == 2 ? kWarps2 * kCtas2 : kWarps1 * kCtas1);
 }
@@ -34,8 +37,13 @@ __host__ __device__ constexpr int chunk_units_per_sm(int d) {
 // footprint is 16 x 16 x KZ with KZ = 24 >= 15 + kSegZ, and each point's 16 z-taps are
 // placed at its cell's offset in a KZ-wide row (stride 28: conflict-free fragments)
 constexpr int kSegZ = 9;
-__host__ __device__ constexpr int chunk_zstride3(int kz) { return kz == 16 ? kStride3 : 28; }
-__host__ __device__ constexpr int chunk_win3_doubles(int kz) { return kChunk * (2 * kStride3 + chunk_zstride3(kz)); }
+// KZ = 12: the one-cell layout of m = 6 (fused3d_m6.cu): all three axes [slot 32][12 taps],
+// row stride 12 (no padding; 9 KB per chunk)
+__host__ __device__ constexpr int chunk_zstride3(int kz) { return kz == 12 ? 12 : (kz == 16 ? kStride3 : 28); }
+__host__ __device__ constexpr int chunk_xstride3(int kz) { return kz == 12 ? 12 : kStride3; }
+__host__ __device__ constexpr int chunk_win3_doubles(int kz) {
+    return kChunk * (2 * chunk_xstride3(kz) + chunk_zstride3(kz));
+}
 
 __host__ __device__ constexpr int chunk_win_doubles(int d) {
     return d == 3 ? chunk_win3_doubles(16) : d * kChunk * kChunkT;

@@ -757,8 +757,17 @@ void launch(const PointSet& ps, const double* gin, double* gout, const double* w
 
 }  // namespace
 
+void fused3d_m6_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
+                              const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s);
+void fused3d_m6_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s);
+void fused3d_m6_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
+                             cudaStream_t s);
+void fused3d_m6_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
+                           cudaStream_t s);
+
 void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* grid_out, const FastParams& fp,
                            const EpiSinkhorn& epi, unsigned long long* dmax, cudaStream_t s) {
+    if (fp.m == 6) return fused3d_m6_gather_spread(ps, grid_in, grid_out, fp, epi, dmax, s);
     // warp-specialised kernel by default; UOTK_FUSED_WS=0 selects the phase-locked one
     static const bool ws = [] {
         const char* e = getenv("UOTK_FUSED_WS");
@@ -777,6 +786,7 @@ void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* gr
 }
 
 void fused3d_spread(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
+    if (fp.m == 6) return fused3d_m6_spread(ps, w, grid, fp, s);
     static const bool ring = [] {
         const char* e = getenv("UOTK_SPREAD_RING");
         return !(e && e[0] == '0');
@@ -801,6 +811,7 @@ void fused3d_spread(const PointSet& ps, const double* w, double* grid, const Fas
 
 void fused3d_gather_store(const PointSet& ps, const double* grid, const FastParams& fp, const EpiStore& epi,
                           cudaStream_t s) {
+    if (fp.m == 6) return fused3d_m6_gather_store(ps, grid, fp, epi, s);
     static const bool ring = [] {
         const char* e = getenv("UOTK_GATHER_RING");
         return !(e && e[0] == '0');
@@ -813,6 +824,7 @@ void fused3d_gather_store(const PointSet& ps, const double* grid, const FastPara
 
 void fused3d_gather_dot(const PointSet& ps, const double* grid, const FastParams& fp, const EpiDot& epi,
                         cudaStream_t s) {
+    if (fp.m == 6) return fused3d_m6_gather_dot(ps, grid, fp, epi, s);
     static const bool ring = [] {
         const char* e = getenv("UOTK_GATHER_RING");
         return !(e && e[0] == '0');

@@ -117,7 +117,8 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
     fp.m = o.m > 0 ? o.m : 8;
     if (fp.m < 2 || fp.m > 8) fail(UOTK_EINVAL, "opts.m must be in [2, 8]");
     fp.flags = o.flags;
-    if ((fp.flags & UOTK_FLAG_CHUNKED) && fp.m != 8) fail(UOTK_EINVAL, "UOTK_FLAG_CHUNKED needs m = 8");
+    if ((fp.flags & UOTK_FLAG_CHUNKED) && !(fp.m == 8 || (fp.m == 6 && d == 3)))
+        fail(UOTK_EINVAL, "UOTK_FLAG_CHUNKED needs m = 8 (or m = 6 in d = 3)");
     const double sigma = o.sigma > 0 ? o.sigma : 2.0;
     if (sigma < 1.25) fail(UOTK_EINVAL, "opts.sigma must be >= 1.25");
     const double tol = o.tol > 0 ? o.tol : 1e-16;

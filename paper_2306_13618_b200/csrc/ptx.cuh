@@ -49,6 +49,10 @@ __device__ __forceinline__ void group_sync(int id) {  // named barrier over one 
     asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
 
+__device__ __forceinline__ void group_sync(int id, int nthreads) {  // named barrier over nthreads
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ void mbar_init_fence() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

@@ -8,6 +8,9 @@ targets:
            (mode 1) and gather (mode 2), cuFFT D2Z / scale_spectrum_k / Z2D on 140^3
   c4       two C4 iterations (d = 2, n = m = 16M): chunked2d_k fused half-steps, 160^2 FFTs
   c3       two C3 iterations (d = 3, n = m = 1M): sinkhorn3d_ws_k, 96^3 FFTs
+  c3m6     the same with m = 6, sigma = 3: sinkhorn3d_m6_ws_k, 144^3 grid
+  c3sum    one kernel sum on C3's points (x -> y, Gaussian eps = 0.02): stand-alone spread and
+           gather kernels on a dense cloud (env M=6 selects m = 6, sigma = 3)
   direct   direct kernel sum d = 3, n = m = 2e5 (direct_k, FP64 exp)
   sum1d    kernel sum d = 1, n = m = 1e7 (chunked1d_k)
 Each target runs its call twice (the first call warms plans and caches); the second runs
@@ -44,10 +47,20 @@ def main(target):
         pr = W.c5_sum(3, 200_000, kind=W.GAUSS)
         args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param)
         call = lambda: uk.kernel_sum(*args, opts={"method": "direct"})  # noqa: E731
-    elif target in ("c3", "c4"):
-        pr = W.c3_uot(iters=2) if target == "c3" else W.c4_uot(iters=2)
+    elif target == "c3sum":
+        pr = W.c3_uot(iters=2)
+        args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), "gauss", pr.eps)
+        o = {"method": "nfft"}
+        if os.environ.get("M") == "6":
+            o.update(m=6, sigma=3.0)
+        call = lambda: uk.kernel_sum(*args, opts=o)  # noqa: E731
+    elif target in ("c3", "c4", "c3m6"):
+        pr = W.c4_uot(iters=2) if target == "c4" else W.c3_uot(iters=2)
         args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
-        call = lambda: uk.uot_sinkhorn(*args, iters=2, opts={"method": "nfft"})  # noqa: E731
+        o = {"method": "nfft"}
+        if target == "c3m6":
+            o.update(m=6, sigma=3.0)
+        call = lambda: uk.uot_sinkhorn(*args, iters=2, opts=o)  # noqa: E731
     else:
         raise SystemExit(f"unknown target {target}")
     call()

@@ -580,3 +580,72 @@ def test_uot_d1(uk, method):
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=30,
                                        opts={"method": method})
     _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ d = 3, m = 6 cell-group kernels
+M6 = {"m": 6, "sigma": 3.0}
+
+
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+@pytest.mark.parametrize("signed", [False, True])
+def test_kernel_sum_m6_cell_group_kernels(uk, kind, signed):
+    """m = 6, sigma = 3 (12 taps per axis, fused3d_m6.cu): the cell-group kernels forced at
+    any density and the generic kernels against the oracle (ragged chunks), and against
+    each other to rounding."""
+    pr = W.random_sum(3, 6001, 3001, kind=kind, param=(0.0025 if kind == W.GAUSS else 0.05), seed=41,
+                      signed=signed)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    out = {}
+    for flags in (uk.FLAG_CHUNKED, uk.FLAG_GENERIC):
+        got, info = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), kind, pr.param,
+                                  opts=dict(M6, method="nfft", flags=flags), return_info=True)
+        assert info["m"] == 6
+        out[flags] = got.cpu().numpy()
+        assert rel_err(out[flags], ref, signed) <= 1e-9, (flags, rel_err(out[flags], ref, signed))
+    assert rel_err(out[uk.FLAG_CHUNKED], out[uk.FLAG_GENERIC], True) <= 1e-13
+
+
+@pytest.mark.parametrize("flags", ["chunked", "generic"])
+def test_uot_c3_like_reduced_m6(uk, flags):
+    """C3 at reduced n with m = 6, sigma = 3: the m = 6 warp-specialised half-step
+    (sinkhorn3d_m6_ws_k) and the generic path against the oracle."""
+    pr = W.c3_uot(n=1537, m=1201, iters=25)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    f = uk.FLAG_CHUNKED if flags == "chunked" else uk.FLAG_GENERIC
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts=dict(M6, method="nfft", flags=f))
+    assert res.info["m"] == 6
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+
+
+def test_uot_c3_full_size_sampled_m6(uk):
+    """C3 at full size with m = 6, sigma = 3 (cell-group kernels by default at this
+    density): the gamma-step identity (3.4) at 48 sampled j against the oracle, and the
+    solve against the m = 8 solve (same iterations) on the objective values."""
+    pr = W.c3_uot(iters=4)
+    args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
+    beta, gamma, res = uk.uot_sinkhorn(*args, iters=pr.iters, opts=dict(M6, method="nfft"))
+    assert res.info["m"] == 6 and res.info["n_grid"] >= 3 * res.info["N"]
+    b = beta.cpu().numpy()
+    g = gamma.cpu().numpy()
+    lam = 1.0 / pr.eps
+    c2 = pr.lam / (1.0 + pr.lam * lam)
+    idx = np.random.default_rng(4).choice(len(pr.y), 48, replace=False)
+    tt = oracle.kernel_sum_direct(pr.x, pr.a * np.exp(lam * b), pr.y[idx], W.GAUSS, pr.eps)
+    ref = -c2 * np.log(tt)
+    assert np.max(np.abs(g[idx] - ref)) <= 1e-9 * np.max(np.abs(ref))
+    _, _, r8 = uk.uot_sinkhorn(*args, iters=pr.iters, opts={"method": "nfft"})
+    assert abs(res.primal - r8.primal) <= 1e-9 * abs(r8.primal)
+    assert abs(res.dual - r8.dual) <= 1e-9 * abs(r8.dual)
+
+
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+def test_mmd2_c2_reduced_m6(uk, kind):
+    """MMD^2 (spread + Fourier-domain sum) with the m = 6 spread kernel, forced."""
+    pr = W.c2_mmd(n=2500, m=2100)
+    param = dict(pr.kernels)[kind]
+    ref = oracle.mmd2_direct(pr.x, pr.a, pr.y, pr.b, kind, param)
+    got = uk.mmd2(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), kind, param,
+                  opts=dict(M6, method="nfft", flags=uk.FLAG_CHUNKED))
+    denom = max(abs(ref), 1e-3 * _mmd_tol(pr.x, pr.a, pr.y, pr.b, kind, param))
+    assert abs(got - ref) / denom <= 1e-8, (got, ref)
