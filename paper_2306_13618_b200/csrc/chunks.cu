@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "profile.cuh"
 #include "window.cuh"
+#include "window_fit.h"
 
 namespace uotk {
 
@@ -35,15 +36,15 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
 // Window blocks (layout per d: chunks.cuh).  One warp per (chunk, axis): lane p loads
 // its point's coordinate once and evaluates its row of taps phi(f + m - 1 - a); the rows
 // are staged in shared memory and written out coalesced.  KZ (d = 3 only): width of the
-// z rows (16, or 24 for z-segment groups: the 16 taps sit at the cell's offset).  m: the
-// window half-width (8; or 6 in d = 3, whose 12 taps fill columns 0..11 of the same layout).
+// z rows (16, or 24 for z-segment groups: the 16 taps sit at the cell's offset; 12 for
+// m = 6, whose 12 taps fill the whole row).
 constexpr int kWinWarps = 4;
 constexpr int kMaxRow = 28;  // widest row stride (d = 3, KZ = 24)
 
 template <int D, int KZ>
 __global__ void __launch_bounds__(kWinWarps * 32)
 chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u, const int32_t* __restrict__ key,
-                    int64_t n, int64_t nchunks, KBWindow w, int m, double* __restrict__ out) {
+                    int64_t n, int64_t nchunks, KBHorner hc, double* __restrict__ out) {
     __shared__ double stage[kWinWarps][kChunk * kMaxRow];
     constexpr int kW = D == 3 ? chunk_win3_doubles(KZ) : chunk_win_doubles(D);
     const int lane = threadIdx.x & 31;
@@ -66,13 +67,19 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
         f = ut - floor(ut);
         if (D == 3 && ax == 2 && KZ == 24) off = key[dsc.x + p] - dsc.z;
     }
-    for (int col = 0; col < stride; ++col) {
-        int a;
-        if (D == 2) a = (col - 4 * p) & 15;  // swizzled column -> tap
-        else a = col - off;
-        double v = 0.0;
-        if (live && a >= 0 && a < 2 * m) v = kb_phi(f + (double)(m - 1 - a), w);
-        st[p * stride + col] = v;
+    // the row: zeros (empty slots, padding columns), then the 2m taps of a live point,
+    // each a degree-14 polynomial in f - 1/2 (window_fit.h)
+    for (int col = 0; col < stride; ++col) st[p * stride + col] = 0.0;
+    if (live) {
+        constexpr int TAPS = (D == 3 && KZ == 12) ? 12 : kChunkT;
+        const double t = f - 0.5;
+#pragma unroll
+        for (int a = 0; a < TAPS; ++a) {
+            double v = hc.c[a][kHornerDeg];
+#pragma unroll
+            for (int j = kHornerDeg - 1; j >= 0; --j) v = fma(v, t, hc.c[a][j]);
+            st[p * stride + (D == 2 ? swz2(p, a) : a + off)] = v;
+        }
     }
     __syncwarp();
     double* o = out + base;
@@ -240,25 +247,25 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
                                                         ps.chunk_desc.p);
     UOTK_LAUNCHED();
-    const KBWindow win = make_window(fp.b, fp.m);
+    const KBHorner win = kb_horner_fit(fp.b, fp.m);
     {
         ProfScope prof(kProfSetup, s);
         const unsigned wb = (unsigned)((nchunks * d + kWinWarps - 1) / kWinWarps);
         if (d == 3 && kz == 12)
             chunk_window_rows_k<3, 12><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, fp.m, ps.chunk_win.p);
+                                                                      win, ps.chunk_win.p);
         else if (d == 3 && kz == 24)
             chunk_window_rows_k<3, 24><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, fp.m, ps.chunk_win.p);
+                                                                      win, ps.chunk_win.p);
         else if (d == 3)
             chunk_window_rows_k<3, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, fp.m, ps.chunk_win.p);
+                                                                      win, ps.chunk_win.p);
         else if (d == 2)
             chunk_window_rows_k<2, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, fp.m, ps.chunk_win.p);
+                                                                      win, ps.chunk_win.p);
         else
             chunk_window_rows_k<1, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
-                                                                      win, fp.m, ps.chunk_win.p);
+                                                                      win, ps.chunk_win.p);
         UOTK_LAUNCHED();
     }
     // cost-balanced static partition of the chunks over the work units
