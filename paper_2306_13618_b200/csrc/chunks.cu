@@ -4,6 +4,10 @@
 // partition of the chunks over the kernels' work units (CTAs for d = 3, warps for d <= 2).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
 #include "chunks.cuh"
 #include "common.cuh"
 #include "profile.cuh"
@@ -247,7 +251,23 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
                                                         ps.chunk_desc.p);
     UOTK_LAUNCHED();
-    const KBHorner win = kb_horner_fit(fp.b, fp.m);
+    // the polynomial fit costs ~0.1 ms of host time: keep the last few (b, m) fits
+    static std::mutex fit_mu;
+    static std::vector<std::pair<std::pair<double, int>, KBHorner>> fits;
+    KBHorner win;
+    {
+        std::lock_guard<std::mutex> lk(fit_mu);
+        auto it = std::find_if(fits.begin(), fits.end(), [&](const auto& e) {
+            return e.first.first == fp.b && e.first.second == fp.m;
+        });
+        if (it != fits.end()) {
+            win = it->second;
+        } else {
+            win = kb_horner_fit(fp.b, fp.m);
+            if (fits.size() >= 8) fits.erase(fits.begin());
+            fits.push_back({{fp.b, fp.m}, win});
+        }
+    }
     {
         ProfScope prof(kProfSetup, s);
         const unsigned wb = (unsigned)((nchunks * d + kWinWarps - 1) / kWinWarps);

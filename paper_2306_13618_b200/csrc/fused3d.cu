@@ -179,6 +179,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         if (GATHER) {
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {  // 8 points per m-tile
+                if (8 * mt >= cnt) break;  // m-tiles past the chunk's points hold no point
                 const int p = 8 * mt + gq;
                 double acc[4][2];
 #pragma unroll
@@ -229,6 +230,7 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         if (SPREAD) {
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {  // 4 points per k-step
+                if (4 * ks >= cnt) break;  // k-steps past the chunk's points add zero windows
                 const int p = 4 * ks + tq;
                 const double wp = __shfl_sync(0xffffffffu, wn, p);
                 // B[p][c] = w_p Z_p[c] for c = 8 nz + gq
@@ -360,6 +362,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             double(*red)[kChunk] = sm.red[k & 1];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
+                if (8 * mt >= cnt) break;  // m-tiles past the chunk's points hold no point
                 const int p = 8 * mt + gq;
                 double acc[8][2];
 #pragma unroll
@@ -430,7 +433,9 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
-            const int32_t key = desc[c].z;
+            const int4 dk = desc[c];
+            const int32_t key = dk.z;
+            const int cnt = dk.y;
             if (key != cur_key) {
                 if (cur_key >= 0) flush();
                 cur_key = key;
@@ -447,6 +452,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             const double(*xw)[kStride] = sm.xw[k & 1];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
+                if (4 * ks >= cnt) break;  // k-steps past the chunk's points add zero windows
                 const int p = 4 * ks + tq;
                 const double b0 = wz[p][gq];
                 const double b1 = wz[p][8 + gq];
@@ -563,6 +569,7 @@ spread3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
         const double(*wz)[ZS] = reinterpret_cast<const double(*)[ZS]>(&sm.win[slot][2 * kChunk * kStride]);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
+            if (4 * ks >= dsc.y) break;  // k-steps past the chunk's points add zero windows
             const int p = 4 * ks + tq;
             const double wp = __shfl_sync(0xffffffffu, w_cur, p);
             double bz[NZ];
@@ -677,6 +684,7 @@ gather3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
         const double(*wz)[ZS] = reinterpret_cast<const double(*)[ZS]>(&sm.win[slot][2 * kChunk * kStride]);
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
+            if (8 * mt >= dsc.y) break;  // m-tiles past the chunk's points hold no point
             const int p = 8 * mt + gq;
             double acc[4][2];
 #pragma unroll

@@ -121,9 +121,10 @@ __device__ __forceinline__ double gather_mtile(const double (&Fb)[3 * NP][3], co
 template <int NP, bool WEIGHTED_B>
 __device__ __forceinline__ void spread_chunk(double (&S)[3 * NP][2][2], const double (*xr)[kStride],
                                              const double (*wy)[kStride], const double (*wz)[kStride], double w_lane,
-                                             int r0, int gq, int tq) {
+                                             int cnt, int r0, int gq, int tq) {
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
+        if (4 * ks >= cnt) break;  // k-steps past the chunk's points add zero windows
         const int p = 4 * ks + tq;
         double b0 = wz[p][gq];
         double b1 = gq < 4 ? wz[p][8 + gq] : 0.0;  // columns c = 12..15 do not exist
@@ -237,7 +238,7 @@ spread3d_m6_k(const int4* __restrict__ desc, const double* __restrict__ win, con
         }
         mbar_wait(&sm.full[slot], (uint32_t)((k / kRingS) & 1));
         const double(*wx)[kStride] = reinterpret_cast<const double(*)[kStride]>(&sm.win[slot][0]);
-        spread_chunk<kNP, true>(S, wx, wx + kChunk, wx + 2 * kChunk, w_cur, r0, gq, tq);
+        spread_chunk<kNP, true>(S, wx, wx + kChunk, wx + 2 * kChunk, w_cur, dsc.y, r0, gq, tq);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);
         if (tid == 0 && k + kRingS < nck) {
@@ -308,6 +309,7 @@ gather3d_m6_k(const int4* __restrict__ desc, const double* __restrict__ win, con
         const double(*wx)[kStride] = reinterpret_cast<const double(*)[kStride]>(&sm.win[slot][0]);
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
+            if (8 * mt >= dsc.y) break;  // m-tiles past the chunk's points hold no point
             const double part = gather_mtile<kNP>(Fb, wx, wx + kChunk, wx + 2 * kChunk, mt, r0, gq, tq);
             if (tq == 0) sm.red[slot][warp][8 * mt + gq] = part;
         }
@@ -417,6 +419,7 @@ sinkhorn3d_m6_ws_k(const int4* __restrict__ desc, const double* __restrict__ win
             if (k >= kRingR) mbar_wait(&sm.red_empty[rslot], (uint32_t)(((k / kRingR) - 1) & 1));
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
+                if (8 * mt >= dsc.y) break;  // m-tiles past the chunk's points hold no point
                 const double part = gather_mtile<kNPG>(Fb, wx, wy, wz, mt, r0, gq, tq);
                 if (tq == 0) sm.red[rslot][g][8 * mt + gq] = part;
             }
@@ -452,13 +455,14 @@ sinkhorn3d_m6_ws_k(const int4* __restrict__ desc, const double* __restrict__ win
         double S[3 * kNPS][2][2];
         int32_t cur_key = -1;
         int64_t org = 0;
-        int32_t key1 = nck > 0 ? desc[cbeg].z : -1;  // group keys loaded two chunks ahead
-        int32_t key2 = nck > 1 ? desc[cbeg + 1].z : -1;
+        int4 dk1 = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);  // descriptors two chunks ahead
+        int4 dk2 = nck > 1 ? desc[cbeg + 1] : make_int4(0, 0, -1, 0);
         for (int64_t k = 0; k < nck; ++k) {
             const int wslot = (int)(k % kRingW);
-            const int32_t key = key1;
-            key1 = key2;
-            if (k + 2 < nck) key2 = desc[cbeg + k + 2].z;
+            const int32_t key = dk1.z;
+            const int cnt = dk1.y;
+            dk1 = dk2;
+            if (k + 2 < nck) dk2 = desc[cbeg + k + 2];
             if (key != cur_key) {
                 if (cur_key >= 0) flush_footprint<kNPS>(S, grid_out, org, ng, r0, gq, tq);
                 cur_key = key;
@@ -468,7 +472,7 @@ sinkhorn3d_m6_ws_k(const int4* __restrict__ desc, const double* __restrict__ win
             mbar_wait(&sm.xw_full[k & 1], (uint32_t)((k >> 1) & 1));
             // the window slot is complete: the reducer read it before publishing xw
             const double(*wx)[kStride] = reinterpret_cast<const double(*)[kStride]>(&sm.win[wslot][0]);
-            spread_chunk<kNPS, false>(S, sm.xw[k & 1], wx + kChunk, wx + 2 * kChunk, 0.0, r0, gq, tq);
+            spread_chunk<kNPS, false>(S, sm.xw[k & 1], wx + kChunk, wx + 2 * kChunk, 0.0, cnt, r0, gq, tq);
             group_sync(1, 32 * kSW);  // all spread warps are done with xw[k & 1] and the window slot
             if (sw == 0 && lane == 0) {
                 mbar_arrive(&sm.xw_empty[k & 1]);

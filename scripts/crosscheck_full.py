@@ -1,7 +1,8 @@
 """Full-size cross-check of the NFFT path against the GPU direct kernel (K6, itself
 oracle-validated in tests/test_gpu_parity.py) on complete solves (SURVEY §8(d) parity
 (iii)): C3 with all 200 iterations (2 x 1e12 pairs per iteration on the direct side,
-~11 min on one B200) and C2's MMD^2 (Gaussian and IMQ).  Writes one JSON object.
+~11 min on one B200), with the paper's window (m = 8, sigma = 2) and with m = 6,
+sigma = 3, and C2's MMD^2 (Gaussian and IMQ).  Writes one JSON object.
 
     python scripts/crosscheck_full.py [--iters 200] > profiles/r01/crosscheck_full.json
 """
@@ -34,26 +35,29 @@ def main():
     pr = W.c3_uot(iters=a.iters)
     args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
     t0 = time.time()
-    b1, g1, r1 = uk.uot_sinkhorn(*args, iters=a.iters, opts={"method": "nfft"})
-    torch.cuda.synchronize()
-    t_nfft = time.time() - t0
-    t0 = time.time()
     b2, g2, r2 = uk.uot_sinkhorn(*args, iters=a.iters, opts={"method": "direct"})
     torch.cuda.synchronize()
     t_direct = time.time() - t0
-    resid = float(torch.linalg.norm(b1 - b2) / torch.linalg.norm(b2) + torch.linalg.norm(g1 - g2) / torch.linalg.norm(g2))
-    out["C3"] = {
-        "n": len(pr.x), "m": len(pr.y), "iters": a.iters,
-        "residual_beta_gamma": resid,
-        "primal_nfft": r1.primal, "primal_direct": r2.primal,
-        "primal_rel_diff": abs(r1.primal - r2.primal) / abs(r2.primal),
-        "dual_rel_diff": abs(r1.dual - r2.dual) / abs(r2.dual),
-        "plan_mass_rel_diff": abs(r1.plan_mass - r2.plan_mass) / r2.plan_mass,
-        "max_abs_dbeta": float(torch.max(torch.abs(b1 - b2))),
-        "seconds_nfft": t_nfft, "seconds_direct": t_direct,
-        "pass_1e-8": resid <= 1e-8 and abs(r1.primal - r2.primal) <= 1e-8 * abs(r2.primal),
-    }
-    print(json.dumps(out["C3"]), file=sys.stderr, flush=True)
+    # the paper's window (m = 8, sigma = 2, the default) and the m = 6, sigma = 3 window
+    for key, o in (("C3", {}), ("C3_m6_sigma3", {"m": 6, "sigma": 3.0})):
+        t0 = time.time()
+        b1, g1, r1 = uk.uot_sinkhorn(*args, iters=a.iters, opts=dict(o, method="nfft"))
+        torch.cuda.synchronize()
+        t_nfft = time.time() - t0
+        resid = float(torch.linalg.norm(b1 - b2) / torch.linalg.norm(b2)
+                      + torch.linalg.norm(g1 - g2) / torch.linalg.norm(g2))
+        out[key] = {
+            "n": len(pr.x), "m": len(pr.y), "iters": a.iters, "window": r1.info,
+            "residual_beta_gamma": resid,
+            "primal_nfft": r1.primal, "primal_direct": r2.primal,
+            "primal_rel_diff": abs(r1.primal - r2.primal) / abs(r2.primal),
+            "dual_rel_diff": abs(r1.dual - r2.dual) / abs(r2.dual),
+            "plan_mass_rel_diff": abs(r1.plan_mass - r2.plan_mass) / r2.plan_mass,
+            "max_abs_dbeta": float(torch.max(torch.abs(b1 - b2))),
+            "seconds_nfft": t_nfft, "seconds_direct": t_direct,
+            "pass_1e-8": resid <= 1e-8 and abs(r1.primal - r2.primal) <= 1e-8 * abs(r2.primal),
+        }
+        print(json.dumps(out[key]), file=sys.stderr, flush=True)
     m = W.c2_mmd()
     x, aa, y, b = cuda(m.x), cuda(m.a), cuda(m.y), cuda(m.b)
     out["C2"] = {}
