@@ -256,6 +256,13 @@ const char* uotk_last_error(void);
 /* Returns UOTK_ABI_VERSION. */
 int uotk_abi_version(void);
 
+/* Releases everything the library caches between calls on the current device: the
+ * Fourier-side tables D_k / circulant factors and their cuFFT plans (rebuilt on the next
+ * call that needs them), the recycled device buffers, and the stream-ordered pool's
+ * reserved memory.  Synchronises the device first.  Returns 0 or UOTK_ECUDA.  After it
+ * the next call runs "cold" (bench.py's cold MMD^2 number). */
+int uotk_release_caches(void);
+
 /* Number of this library's kernels launched by the calling thread since the last
  * reset (bench.py's "gpu_launches"); uotk_launch_counter_reset sets it to 0. */
 int64_t uotk_launch_counter(void);

@@ -31,7 +31,7 @@ FLAG_TRANSPORT = 4
 FLAG_FFT = 8  # always the cuFFT spectral chain (the multi-rank path), never the separable GEMMs
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 
-__all__ = ["kernel_sum", "uot_sinkhorn", "uot_sinkhorn_scaling", "mmd2", "uot_cstar", "sinkhorn_divergence", "Comm", "UOTResult", "GAUSS",
+__all__ = ["kernel_sum", "uot_sinkhorn", "uot_sinkhorn_scaling", "mmd2", "uot_cstar", "sinkhorn_divergence", "release_caches", "Comm", "UOTResult", "GAUSS",
            "IMQ", "UotkError",
            "launch_counter", "reset_launch_counter", "library_path"]
 
@@ -327,6 +327,12 @@ class Comm:
         if self.handle:
             _native.check(_native.load().uotk_comm_destroy(self.handle))
             self.handle = None
+
+
+def release_caches():
+    """Drop the library's cached Fourier tables, cuFFT plans and device buffers (the next
+    call runs cold; see uotk_release_caches in include/uotk.h)."""
+    _native.check(_native.load().uotk_release_caches())
 
 
 def launch_counter():

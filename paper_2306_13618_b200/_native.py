@@ -23,7 +23,7 @@ EXPORTED = (
     "uotk_uot_cstar", "uotk_sinkhorn_divergence", "uotk_uot_sinkhorn_scaling", "uotk_uot_sinkhorn_ex",
     "uotk_comm_unique_id", "uotk_comm_create", "uotk_comm_destroy",
     "uotk_last_error", "uotk_abi_version", "uotk_launch_counter", "uotk_launch_counter_reset",
-    "uotk_profile_enable", "uotk_profile_reset", "uotk_profile_read",
+    "uotk_profile_enable", "uotk_profile_reset", "uotk_profile_read", "uotk_release_caches",
 )
 
 
@@ -117,6 +117,8 @@ def load():
     lib.uotk_profile_enable.restype = None
     lib.uotk_profile_reset.argtypes = []
     lib.uotk_profile_reset.restype = None
+    lib.uotk_release_caches.argtypes = []
+    lib.uotk_release_caches.restype = ctypes.c_int
     lib.uotk_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), ctypes.POINTER(I64)]
     lib.uotk_profile_read.restype = INT
     _lib = lib

@@ -761,6 +761,21 @@ const char* uotk_last_error(void) { return g_last_error.c_str(); }
 
 int uotk_abi_version(void) { return UOTK_ABI_VERSION; }
 
+int uotk_release_caches(void) {
+    return uotk::guarded([&] {
+        UOTK_CUDA(cudaDeviceSynchronize());
+        uotk::release_plan_cache();
+        uotk::release_fft_plans();
+        uotk::block_cache_release();
+        int dev = 0;
+        UOTK_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        cudaGetLastError();
+        UOTK_CUDA(cudaDeviceSynchronize());
+    });
+}
+
 int64_t uotk_launch_counter(void) { return g_launches; }
 
 void uotk_launch_counter_reset(void) { g_launches = 0; }

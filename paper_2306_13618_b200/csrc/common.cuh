@@ -60,6 +60,8 @@ struct DevBuf {
 bool is_device_pointer(const void* ptr);
 size_t block_cache_bytes();   // freed device blocks the library keeps for reuse (this device)
 void block_cache_release();   // return them to the stream-ordered pool
+void release_plan_cache();    // nfft_plan.cu: drop the cached D_k / circulant tables
+void release_fft_plans();     // context.cu: destroy the cached cuFFT plans
 
 // A caller array that may live on the host or the device: `d` is always a device
 // pointer valid for the duration of the call.

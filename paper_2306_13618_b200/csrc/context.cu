@@ -311,6 +311,19 @@ static void configure_pool(int dev) {
     c.pool_configured[dev] = true;
 }
 
+void release_fft_plans() {
+    Context& c = ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto& e : c.fft) {
+        cufftDestroy(e.second.first);
+        cufftDestroy(e.second.second);
+    }
+    c.fft.clear();
+    for (auto& e : c.pruned)
+        for (cufftHandle h : e.second) cufftDestroy(h);
+    c.pruned.clear();
+}
+
 void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r) {
     int dev = 0;
     UOTK_CUDA(cudaGetDevice(&dev));

@@ -282,6 +282,11 @@ void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s);
 
 }  // namespace
 
+void release_plan_cache() {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plans.clear();  // tables still referenced by a live SpectralPlan stay until it ends
+}
+
 void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     const FastParams& fp = sp.fp;
     const int d = fp.d, ng = fp.ng;

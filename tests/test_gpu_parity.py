@@ -649,3 +649,19 @@ def test_mmd2_c2_reduced_m6(uk, kind):
                   opts=dict(M6, method="nfft", flags=uk.FLAG_CHUNKED))
     denom = max(abs(ref), 1e-3 * _mmd_tol(pr.x, pr.a, pr.y, pr.b, kind, param))
     assert abs(got - ref) / denom <= 1e-8, (got, ref)
+
+
+def test_release_caches_then_cold_calls_agree(uk):
+    """uotk_release_caches drops the cached tables, plans and buffers; the following calls
+    (cold: tables and plans rebuilt) give the same results as the warm ones."""
+    pr = W.c2_mmd(n=3001, m=2503)
+    args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b))
+    warm = [uk.mmd2(*args, kind, param, opts={"method": "nfft"}) for kind, param in pr.kernels]
+    s_warm = uk.kernel_sum(args[0], args[1], args[2], "imq", 0.05, opts={"method": "nfft"})
+    uk.release_caches()
+    cold = [uk.mmd2(*args, kind, param, opts={"method": "nfft"}) for kind, param in pr.kernels]
+    s_cold = uk.kernel_sum(args[0], args[1], args[2], "imq", 0.05, opts={"method": "nfft"})
+    for w, c in zip(warm, cold):
+        assert abs(w - c) <= 1e-13 * abs(w)
+    assert float(torch.max(torch.abs(s_warm - s_cold))) <= 1e-13 * float(torch.max(torch.abs(s_warm)))
+    uk.release_caches()
