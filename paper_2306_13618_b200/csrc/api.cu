@@ -228,7 +228,7 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         PointSet PS, PT;
         make_pointset(PS, S.d, n_src, ns.fp, s);
         trace_mark("pointset src");
-        make_pointset(PT, T.d, n_tgt, ns.fp, s);
+        make_pointset(PT, T.d, n_tgt, ns.fp, s, kUseGatherOnly);
         trace_mark("pointset tgt");
         DevBuf<double> w(n_src, s), grid(grid_elems(ns.fp), s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);

@@ -137,7 +137,7 @@ bool chunked_available(const FastParams& fp) {
 // clouds: d = 3 below ~3 points per chunk, d = 2 below 2) or the window blocks would not fit
 // comfortably in free device memory, the point set stays on the generic kernels
 // (ps.chunked = false).
-void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
+void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUse use) {
     ps.chunked = false;
     ps.nchunks = 0;
     if (!chunked_available(fp) || ps.n == 0 || (fp.flags & UOTK_FLAG_GENERIC)) return;
@@ -203,6 +203,8 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s) {
     // d = 1: any)
     const double min_fill = d == 3 ? 0.09 : (d == 2 ? 1.0 / 16 : 0.0);
     if (!forced && (double)n < min_fill * chunk_cost * kChunk * (double)nchunks) return;
+    // a gather-only set this sparse is gathered by the generic kernel anyway (nfft.cu)
+    if (!forced && use == kUseGatherOnly && d == 3 && (double)n < kGatherMinFill3 * kChunk * (double)nchunks) return;
     const int wd = d == 3 ? chunk_win3_doubles(kz) : chunk_win_doubles(d);
     const size_t win_bytes = (size_t)nchunks * wd * sizeof(double);
     // cudaMemGetInfo can stall the host (milliseconds, and seconds when the stream-ordered

@@ -49,6 +49,11 @@ __host__ __device__ constexpr int chunk_win_doubles(int d) {
     return d == 3 ? chunk_win3_doubles(16) : d * kChunk * kChunkT;
 }
 
+// d = 3 stand-alone gathers on sets whose chunks are filled below this fraction use the
+// generic per-point kernel (its per-point loads beat the padded GEMMs there; nfft.cu), and
+// gather-only sets that sparse get no chunk list at all (chunks.cu)
+constexpr double kGatherMinFill3 = 0.3;
+
 // d = 2 swizzle: column of tap a in slot row p
 __host__ __device__ __forceinline__ int swz2(int p, int a) { return (a + 4 * p) & 15; }
 

@@ -8,6 +8,7 @@
 #include <string>
 #include <utility>
 
+#include "chunks.cuh"
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "profile.cuh"
@@ -208,7 +209,6 @@ void spread(const PointSet& ps, const double* w_sorted, double* grid, const Fast
 // Stand-alone gathers (kernel sums, marginals) on sparse d = 3 clouds stay on the generic
 // kernel: with few points per chunk its per-point loads beat the padded DMMA GEMMs (the
 // spread still profits from the cell groups: footprint flushes instead of per-tap atomics).
-constexpr double kGatherMinFill3 = 0.3;
 
 template <class Epi>
 void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,

@@ -10,7 +10,7 @@
 namespace uotk {
 
 void comm_allreduce_minmax(double* dmin, int nmin, double* dmax, int nmax, void* comm, cudaStream_t s);  // comm.cu
-void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s);  // chunks.cu
+void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUse use);  // chunks.cu
 
 namespace {
 
@@ -201,7 +201,8 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
     return g;
 }
 
-void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s) {
+void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
+                   PointUse use) {
     const int d = fp.d;
     ps.d = d;
     ps.n = n;
@@ -234,7 +235,7 @@ void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams&
     else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
     else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
     UOTK_LAUNCHED();
-    chunked_prepare(ps, fp, s);  // chunk list + precomputed windows (tuned cell-group kernels)
+    chunked_prepare(ps, fp, s, use);  // chunk list + precomputed windows (tuned cell-group kernels)
 }
 
 void permute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s) {
