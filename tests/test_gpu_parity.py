@@ -665,3 +665,18 @@ def test_release_caches_then_cold_calls_agree(uk):
         assert abs(w - c) <= 1e-13 * abs(w)
     assert float(torch.max(torch.abs(s_warm - s_cold))) <= 1e-13 * float(torch.max(torch.abs(s_warm)))
     uk.release_caches()
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 97])
+def test_kernel_sum_m6_tiny_and_ragged(uk, n):
+    """m = 6 cell-group kernels (forced) at sizes below, at and just above one chunk."""
+    pr = W.random_sum(3, n, n + 5, kind=W.GAUSS, param=0.02, seed=50 + n, signed=False)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    got = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param,
+                        opts=dict(M6, method="nfft", flags=uk.FLAG_CHUNKED))
+    assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9
+    pr2 = W.c3_uot(n=n, m=n + 3, iters=5)
+    ref2 = oracle.uot_sinkhorn_direct(pr2.x, pr2.a, pr2.y, pr2.b, pr2.eps, pr2.lam, pr2.lam, pr2.iters)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr2.x), cuda(pr2.a), cuda(pr2.y), cuda(pr2.b), pr2.eps, pr2.lam,
+                                       iters=pr2.iters, opts=dict(M6, method="nfft", flags=uk.FLAG_CHUNKED))
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref2)
