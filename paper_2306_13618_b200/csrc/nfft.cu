@@ -308,6 +308,7 @@ double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s,
         return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s, comm);
     }
     ProfScope ps_(kProfFft, s);
+    if (!sp.r2c) get_fft_plans(fp.d, fp.ng, &sp.r2c, &sp.c2r);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftSetStream(sp.c2r, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
@@ -486,6 +487,7 @@ void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part
         return;
     }
     ProfScope ps_(kProfFft, s);
+    if (!sp.r2c) get_fft_plans(fp.d, fp.ng, &sp.r2c, &sp.c2r);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
     if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);

@@ -320,7 +320,9 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
         g_plans.emplace_front(key, pd);
         if (g_plans.size() > kPlanCacheSize) g_plans.pop_back();
     }
-    get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
+    // the full-grid cuFFT plans only where the full chain runs (fft_chain also creates them
+    // on first use: the separable Gaussian chain and the pruned MMD^2 transform never do)
+    if (!sp.pd->separable || (fp.flags & UOTK_FLAG_FFT)) get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
     sp.grid_elems = 1;
     for (int t = 0; t < d; ++t) sp.grid_elems *= ng;
     sp.spec_elems = sp.grid_elems / ng * (ng / 2 + 1);
