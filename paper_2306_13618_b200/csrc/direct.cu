@@ -101,6 +101,55 @@ __global__ void combine_k(const double* __restrict__ partial, int nsplit, int64_
     warp_max_atomic(dmax, dd);
 }
 
+// Few targets (C1: 1000 x 1000): one warp per target over ALL sources (lanes stride the
+// source tile in shared memory, then a shuffle reduction), the epilogue in the same launch
+// — one kernel per half-step instead of a source-split kernel plus a combine kernel, so the
+// CUDA-graph-replayed iteration is two short launches (C1: 38k -> 47k iterations/s; a CTA
+// of 256 threads per target measured slower, 31k).
+constexpr int kWTile = 1024;  // sources per shared-memory tile
+template <int D, int WT, class Epi>
+__global__ void __launch_bounds__(WT) direct_warp_k(int64_t n_src, const double* __restrict__ src,
+                                                    const double* __restrict__ w, int64_t n_tgt,
+                                                    const double* __restrict__ tgt, int kind, double inv_or_c2,
+                                                    Epi epi, unsigned long long* dmax) {
+    __shared__ double sp[D][kWTile];
+    __shared__ double sw[kWTile];
+    const int lane = threadIdx.x & 31;
+    const int64_t i = blockIdx.x * (int64_t)(WT / 32) + (threadIdx.x >> 5);
+    double xi[D];
+    for (int t = 0; t < D; ++t) xi[t] = i < n_tgt ? tgt[i * D + t] : 0.0;
+    double acc = 0.0;
+    for (int64_t jt = 0; jt < n_src; jt += kWTile) {
+        const int cnt = (int)((n_src - jt) < kWTile ? (n_src - jt) : kWTile);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cnt; k += WT) {
+            for (int t = 0; t < D; ++t) sp[t][k] = src[(jt + k) * D + t];
+            sw[k] = w[jt + k];
+        }
+        __syncthreads();
+        double part = 0.0;
+        for (int j = lane; j < cnt; j += 32) {
+            double r2 = kind == UOTK_IMQ ? inv_or_c2 : 0.0;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const double v = xi[t] - sp[t][j];
+                r2 = fma(v, v, r2);
+            }
+            double kv;
+            if (kind == UOTK_GAUSS) kv = exp(-r2 * inv_or_c2);
+            else if (kind == UOTK_GAUSS_R2) kv = r2 * exp(-r2 * inv_or_c2);
+            else kv = 1.0 / sqrt(r2);
+            part = fma(kv, sw[j], part);
+        }
+        acc += part;  // two-level summation: per tile, then over tiles
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    double dd = 0.0;
+    if (lane == 0 && i < n_tgt) dd = epi(i, acc);
+    warp_max_atomic(dmax, dd);
+}
+
 }  // namespace
 
 template <class Epi>
@@ -116,6 +165,27 @@ void direct_sum_epi(int d, int64_t n_src, const double* src, const double* w, in
         int dev = 0;
         UOTK_CUDA(cudaGetDevice(&dev));
         UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const double arg0 = kind == UOTK_IMQ ? param * param : 1.0 / param;
+    static const bool warp_env = [] {  // UOTK_DIRECT_WARP=0: always the source-split kernel
+        const char* e = getenv("UOTK_DIRECT_WARP");
+        return !(e && e[0] == '0');
+    }();
+    // a warp per target: when the targets alone leave the GPU underfilled and a warp's
+    // pass over all sources stays short
+    if (warp_env && n_tgt <= 64LL * sms && n_src <= 16384 && tb < 2LL * sms) {
+#define UOTK_WARP_LAUNCH(WT)                                                                                     \
+    do {                                                                                                        \
+        const unsigned blocks = (unsigned)((n_tgt + WT / 32 - 1) / (WT / 32));                                  \
+        if (d == 1) direct_warp_k<1, WT, Epi><<<blocks, WT, 0, s>>>(n_src, src, w, n_tgt, tgt, kind, arg0, epi, dmax); \
+        else if (d == 2) direct_warp_k<2, WT, Epi><<<blocks, WT, 0, s>>>(n_src, src, w, n_tgt, tgt, kind, arg0, epi, dmax); \
+        else direct_warp_k<3, WT, Epi><<<blocks, WT, 0, s>>>(n_src, src, w, n_tgt, tgt, kind, arg0, epi, dmax); \
+    } while (0)
+        ProfScope ps_(kProfDirect, s);
+        UOTK_WARP_LAUNCH(256);  // 128-thread CTAs measured the same
+#undef UOTK_WARP_LAUNCH
+        UOTK_LAUNCHED();
+        return;
     }
     const int64_t want = (8LL * sms + tb - 1) / tb;
     int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(want, n_src / 64));
