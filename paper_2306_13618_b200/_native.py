@@ -117,8 +117,9 @@ def load():
     lib.uotk_profile_enable.restype = None
     lib.uotk_profile_reset.argtypes = []
     lib.uotk_profile_reset.restype = None
-    lib.uotk_release_caches.argtypes = []
-    lib.uotk_release_caches.restype = ctypes.c_int
+    if getattr(lib, "uotk_release_caches", None) is not None:  # absent from older A/B builds
+        lib.uotk_release_caches.argtypes = []
+        lib.uotk_release_caches.restype = ctypes.c_int
     lib.uotk_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), ctypes.POINTER(I64)]
     lib.uotk_profile_read.restype = INT
     _lib = lib

@@ -43,6 +43,7 @@ def timed(fn, reps=3):
     events on the current stream); then one profiled call for the per-tag kernel times
     (profiling brackets every launch with events and disables the CUDA-graph replay)."""
     fn()
+    fn()  # a second warm-up: the first calls grow the memory pool and build plans
     spin_up()
     torch.cuda.synchronize()
     uk.reset_launch_counter()
@@ -90,7 +91,7 @@ def case_c2():
     for kind, param in pr.kernels:
         for method in ("nfft", "direct"):
             ms, prof, nl, out = timed(lambda: uk.mmd2(x, a, y, b, kind, param, opts={"method": method},
-                                                      return_info=True), reps=2)
+                                                      return_info=True), reps=3)
             emit(case="C2", kind=kind, method=method, ms_per_call=ms, evals_per_s=1e3 / ms, prof=prof, launches=nl,
                  info=out[1], mmd2=out[0])
 
@@ -118,7 +119,7 @@ def case_c5(max_n, dims=(1, 2, 3), min_n=10_000):
                 for method in methods:
                     ms, prof, nl, out = timed(lambda: uk.kernel_sum(s, al, t, kind, pr.param,
                                                                     opts={"method": method}, return_info=True),
-                                              reps=2)
+                                              reps=3 if method == "nfft" else 1)
                     emit(case="C5", d=d, kind=kind, n=n, method=method, ms_per_call=ms, prof=prof, launches=nl,
                          info=out[1], pts_per_s=2 * n / ms * 1e3)
                 del s, al, t, pr
