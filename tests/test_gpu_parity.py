@@ -680,3 +680,19 @@ def test_kernel_sum_m6_tiny_and_ragged(uk, n):
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr2.x), cuda(pr2.a), cuda(pr2.y), cuda(pr2.b), pr2.eps, pr2.lam,
                                        iters=pr2.iters, opts=dict(M6, method="nfft", flags=uk.FLAG_CHUNKED))
     _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref2)
+
+
+def test_error_paths_overflow_and_nonfinite(uk):
+    """UOTK_EOVERFLOW when the Sinkhorn kernel sums underflow to 0 (far-apart clouds,
+    eps tiny: exp(-0.04 / 1e-5) = 0 in fp64), and UOTK_EDOMAIN for a non-finite coordinate."""
+    x = np.zeros((3, 2))
+    y = np.full((4, 2), 0.2)
+    with pytest.raises(uk.UotkError) as e:
+        uk.uot_sinkhorn(cuda(x), cuda(np.ones(3)), cuda(y), cuda(np.ones(4)), 1e-5, 1.0, iters=3,
+                        opts={"method": "direct"})
+    assert e.value.code == -3
+    xs = W.uniform_ball(np.random.default_rng(1), 200, 3, 0.2)
+    xs[17, 1] = np.nan
+    with pytest.raises(uk.UotkError) as e:
+        uk.kernel_sum(cuda(xs), cuda(np.ones(200)), cuda(xs), "gauss", 0.0025, opts={"method": "nfft"})
+    assert e.value.code == -2
