@@ -124,8 +124,18 @@ size_t grid_elems(const FastParams& fp) {
     return g;
 }
 
-// Sinkhorn iterations below this many points (n + m) are replayed from CUDA graphs.
-constexpr int64_t kGraphMaxPoints = 1 << 18;
+// Sinkhorn iterations are replayed from CUDA graphs (at every size: the small problems are
+// launch-bound, and the large ones lose the gaps around the spectral chain's short
+// kernels — C3 266 -> 261 ms per solve); UOTK_GRAPH_MAX=<points> limits it to n + m below
+// that (0: never).
+static int64_t graph_max_points() {
+    static const int64_t v = [] {
+        const char* e = getenv("UOTK_GRAPH_MAX");
+        return e ? (int64_t)atoll(e) : INT64_MAX;
+    }();
+    return v;
+}
+#define kGraphMaxPoints graph_max_points()
 constexpr int kGraphIters = 16;  // iterations per captured graph
 
 // Runs iterate(0) .. iterate(iters - 1) in order on stream s.  With use_graph the first
