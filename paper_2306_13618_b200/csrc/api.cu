@@ -665,8 +665,6 @@ int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a, int64_
         on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
             uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, st);
         });
-        return;
-        uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, cs);
     });
 }
 
