@@ -236,7 +236,7 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         setup_nfft(ns, d, kind, param, S.d, n_src, T.d, n_tgt, o, comm, s);
         fill_info(info, method, &ns.fp);
         PointSet PS, PT;
-        make_pointset(PS, S.d, n_src, ns.fp, s);
+        make_pointset(PS, S.d, n_src, ns.fp, s, kUseSpreadOnly);
         trace_mark("pointset src");
         make_pointset(PT, T.d, n_tgt, ns.fp, s, kUseGatherOnly);
         trace_mark("pointset tgt");
@@ -622,7 +622,7 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
         setup_nfft(ns, d, kind, param, z.p, nz, nullptr, 0, o, comm, s);
         fill_info(info, method, &ns.fp);
         PointSet PZ;
-        make_pointset(PZ, z.p, nz, ns.fp, s);
+        make_pointset(PZ, z.p, nz, ns.fp, s, kUseSpreadOnly);
         constexpr int kParts = 296;
         DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s), part(kParts, s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);

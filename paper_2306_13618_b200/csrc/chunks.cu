@@ -43,7 +43,7 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
 // z rows (16, or 24 for z-segment groups: the 16 taps sit at the cell's offset; 12 for
 // m = 6, whose 12 taps fill the whole row).
 constexpr int kWinWarps = 4;
-constexpr int kMaxRow = 28;  // widest row stride (d = 3, KZ = 24)
+constexpr int kMaxRow = 44;  // widest row stride (d = 3, KZ = 40)
 
 template <int D, int KZ>
 __global__ void __launch_bounds__(kWinWarps * 32)
@@ -69,7 +69,7 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
     if (live) {
         const double ut = u[ax * n + dsc.x + p];
         f = ut - floor(ut);
-        if (D == 3 && ax == 2 && KZ == 24) off = key[dsc.x + p] - dsc.z;
+        if (D == 3 && ax == 2 && (KZ == 24 || KZ == 40)) off = key[dsc.x + p] - dsc.z;
     }
     // the row: zeros (empty slots, padding columns), then the 2m taps of a live point,
     // each a degree-14 polynomial in f - 1/2 (window_fit.h)
@@ -91,11 +91,12 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
 }
 
 // group key of a z-segment: the cell key with its z index rounded down to a multiple of kSegZ
-__global__ void segment_key_k(const int32_t* __restrict__ key, int64_t n, int ng, int32_t* __restrict__ gk) {
+__global__ void segment_key_k(const int32_t* __restrict__ key, int64_t n, int ng, int segz,
+                              int32_t* __restrict__ gk) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
         const int32_t k = key[i];
-        gk[i] = k - (k % ng) % kSegZ;
+        gk[i] = k - (k % ng) % segz;
     }
 }
 
@@ -185,7 +186,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     DevBuf<int32_t> gk;
     if (d == 3 && fp.m == kChunkM && (double)n < 0.5 * kChunk * (double)nchunks) {
         gk.alloc(n, s);
-        segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, gk.p);
+        segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, kSegZ, gk.p);
         UOTK_LAUNCHED();
         const int64_t nseg = encode(gk.p);
         if (1.5 * (double)nseg < (double)nchunks) {
@@ -194,6 +195,25 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
             nchunks = nseg;
         } else {
             nchunks = encode(ps.key.p);  // back to one-cell groups
+        }
+        static const bool seg40_env = [] {
+            const char* e = getenv("UOTK_SEG40");
+            return !(e && e[0] == '0');
+        }();
+        // a spread-only set still below 1/4 fill: 25-cell segments if they merge groups
+        if (kz == 24 && use == kUseSpreadOnly && seg40_env && (double)n < 0.25 * kChunk * (double)nchunks) {
+            segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, kSegZ40, gk.p);
+            UOTK_LAUNCHED();
+            const int64_t nseg40 = encode(gk.p);
+            if ((double)nseg40 < 0.7 * (double)nchunks) {
+                kz = 40;
+                chunk_cost = 2.5;
+                nchunks = nseg40;
+            } else {  // back to the 9-cell segments
+                segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, kSegZ, gk.p);
+                UOTK_LAUNCHED();
+                nchunks = encode(gk.p);
+            }
         }
         trace_mark("chunks: z-segments");
     }
@@ -275,6 +295,9 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
         const unsigned wb = (unsigned)((nchunks * d + kWinWarps - 1) / kWinWarps);
         if (d == 3 && kz == 12)
             chunk_window_rows_k<3, 12><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, ps.chunk_win.p);
+        else if (d == 3 && kz == 40)
+            chunk_window_rows_k<3, 40><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
                                                                       win, ps.chunk_win.p);
         else if (d == 3 && kz == 24)
             chunk_window_rows_k<3, 24><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,

@@ -37,9 +37,14 @@ __host__ __device__ constexpr int chunk_units_per_sm(int d) {
 // footprint is 16 x 16 x KZ with KZ = 24 >= 15 + kSegZ, and each point's 16 z-taps are
 // placed at its cell's offset in a KZ-wide row (stride 28: conflict-free fragments)
 constexpr int kSegZ = 9;
+// spread-only sets sparser still (kernel-sum sources, MMD^2): segments of 25 cells,
+// footprint 16 x 16 x 40 — the group flushes (fp64 atomics), not the DMMAs, bind there
+constexpr int kSegZ40 = 25;
 // KZ = 12: the one-cell layout of m = 6 (fused3d_m6.cu): all three axes [slot 32][12 taps],
 // row stride 12 (no padding; 9 KB per chunk)
-__host__ __device__ constexpr int chunk_zstride3(int kz) { return kz == 12 ? 12 : (kz == 16 ? kStride3 : 28); }
+__host__ __device__ constexpr int chunk_zstride3(int kz) {
+    return kz == 12 ? 12 : (kz == 16 ? kStride3 : (kz == 24 ? 28 : 44));
+}
 __host__ __device__ constexpr int chunk_xstride3(int kz) { return kz == 12 ? 12 : kStride3; }
 __host__ __device__ constexpr int chunk_win3_doubles(int kz) {
     return kChunk * (2 * chunk_xstride3(kz) + chunk_zstride3(kz));

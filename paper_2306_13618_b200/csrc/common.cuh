@@ -173,7 +173,7 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
 // scale, key and sort one point set; weights are permuted separately by permute_values
 // use: what the point set will be used for (the chunk layout is skipped where no kernel
 // would use it: gather-only d = 3 sets below kGatherMinFill3)
-enum PointUse { kUseBoth = 0, kUseGatherOnly = 1 };
+enum PointUse { kUseBoth = 0, kUseGatherOnly = 1, kUseSpreadOnly = 2 };
 void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
                    PointUse use = kUseBoth);
 void permute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);

@@ -734,6 +734,7 @@ gather3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
 template <class Epi>
 void launch_gather(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi, cudaStream_t s) {
     if (ps.n == 0 || ps.nchunks == 0) return;
+    if (ps.chunk_kz == 40) fail(UOTK_EUNSUPPORTED, "internal: gather on a spread-only point set");
     ProfScope prof(kProfGather, s);
     if (ps.chunk_kz == 24) {
         set_smem_attr((const void*)gather3d_k<24, Epi>, (int)sizeof(SmemG<24>));
@@ -751,6 +752,7 @@ template <int MODE, class Epi>
 void launch(const PointSet& ps, const double* gin, double* gout, const double* w, const FastParams& fp,
             const Epi& epi, unsigned long long* dmax, cudaStream_t s, int tag) {
     if (ps.n == 0 || ps.nchunks == 0) return;
+    if (ps.chunk_kz == 40) fail(UOTK_EUNSUPPORTED, "internal: 25-cell segments on the phase-locked kernels");
     ProfScope prof(tag, s);
     if (ps.chunk_kz == 24)
         chunked3d_k<MODE, Epi, 24><<<ps.chunk_blocks, kThreads, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p,
@@ -805,7 +807,11 @@ void fused3d_spread(const PointSet& ps, const double* w, double* grid, const Fas
     }
     if (ps.n == 0 || ps.nchunks == 0) return;
     ProfScope prof(kProfSpread, s);
-    if (ps.chunk_kz == 24) {
+    if (ps.chunk_kz == 40) {
+        set_smem_attr((const void*)spread3d_k<40>, (int)sizeof(SmemS<40>));
+        spread3d_k<40><<<ps.chunk_blocks, kThreads, sizeof(SmemS<40>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,
+                                                                            ps.chunk_bounds.p, fp.ng, grid, w);
+    } else if (ps.chunk_kz == 24) {
         set_smem_attr((const void*)spread3d_k<24>, (int)sizeof(SmemS<24>));
         spread3d_k<24><<<ps.chunk_blocks, kThreads, sizeof(SmemS<24>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,
                                                                             ps.chunk_bounds.p, fp.ng, grid, w);
