@@ -186,7 +186,7 @@ void spread(const PointSet& ps, const double* w_sorted, double* grid, const Fast
 double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
 void get_cublas(void** handle);  // per-device cuBLAS handle (context.cu)
 // cuFFT plans of the pruned 3-D forward transform (box width w, kept modes |k| <= H)
-void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cufftHandle* px);
+void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cufftHandle* px, cufftHandle* pzi);
 void gather(const PointSet& ps, const double* grid, double* out_sorted, const FastParams& fp, cudaStream_t s);
 template <class Epi>
 void gather_epi(const PointSet& ps, const double* grid, const FastParams& fp, const Epi& epi,

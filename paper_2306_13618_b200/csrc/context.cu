@@ -290,7 +290,7 @@ struct Context {
     bool pool_configured[64] = {};
     std::map<int, cublasHandle_t> blas;
     // (device, n, w, H) -> pruned-transform plans (pass z R2C, pass y C2C, pass x C2C)
-    std::map<std::tuple<int, int, int, int>, std::array<cufftHandle, 3>> pruned;
+    std::map<std::tuple<int, int, int, int>, std::array<cufftHandle, 4>> pruned;
     std::map<int, cudaStream_t> streams;
 };
 
@@ -353,7 +353,7 @@ void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r) {
     *c2r = b;
 }
 
-void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cufftHandle* px) {
+void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cufftHandle* px, cufftHandle* pzi) {
     int dev = 0;
     UOTK_CUDA(cudaGetDevice(&dev));
     Context& c = ctx();
@@ -361,7 +361,7 @@ void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cuf
     auto key = std::make_tuple(dev, n, w, H);
     auto it = c.pruned.find(key);
     if (it == c.pruned.end()) {
-        std::array<cufftHandle, 3> h{};
+        std::array<cufftHandle, 4> h{};
         int len = n;
         const int half = n / 2 + 1;
         // z: R2C of the w * n rows g[o + x'][y][.], contiguous
@@ -370,11 +370,14 @@ void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cuf
         UOTK_CUFFT(cufftPlanMany(&h[1], 1, &len, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, w * (H + 1)));
         // x: C2C of (2H + 1) * (H + 1) rows of length n
         UOTK_CUFFT(cufftPlanMany(&h[2], 1, &len, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, (2 * H + 1) * (H + 1)));
+        // z inverse (kernel-sum chain): C2R of the w * n rows back into the box slab
+        UOTK_CUFFT(cufftPlanMany(&h[3], 1, &len, nullptr, 1, half, nullptr, 1, n, CUFFT_Z2D, w * n));
         it = c.pruned.emplace(key, h).first;
     }
     *pz = it->second[0];
     *py = it->second[1];
     *px = it->second[2];
+    *pzi = it->second[3];
 }
 
 void get_cublas(void** handle) {

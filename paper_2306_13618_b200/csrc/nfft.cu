@@ -301,6 +301,8 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
     return spare;
 }
 
+static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s);
+
 double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
     if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT)) {
@@ -308,6 +310,16 @@ double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s,
         return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s, comm);
     }
     ProfScope ps_(kProfFft, s);
+    {
+        static const bool pruned_env = [] {
+            const char* e = getenv("UOTK_PRUNED_FFT");
+            return !(e && e[0] == '0');
+        }();
+        const size_t need = (size_t)fp.box_w * fp.ng * (fp.ng / 2 + 1) + (size_t)fp.box_w * (fp.N / 2 + 1) * fp.ng +
+                            (size_t)(fp.N + 1) * (fp.N / 2 + 1) * fp.ng;
+        if (pruned_env && fp.d == 3 && !comm && !(fp.flags & UOTK_FLAG_FFT) && need <= sp.spec_elems)
+            return fft_chain_pruned(sp, grid, spec, s);
+    }
     if (!sp.r2c) get_fft_plans(fp.d, fp.ng, &sp.r2c, &sp.c2r);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftSetStream(sp.c2r, s));
@@ -437,6 +449,70 @@ __global__ void pruned_energy_k(const double2* __restrict__ t3, const double* __
     if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
 }
 
+// the kernel-sum chain's inverse half of the pruned transform (fft_chain_pruned):
+// t2c [ky'][kz][kx] *= D_k for |kx| <= H (zero beyond), in place
+__global__ void prune_scale_k(double2* __restrict__ t3, const double* __restrict__ Dk, int n, int N) {
+    const int H = N / 2;
+    const int64_t total = (int64_t)(2 * H + 1) * (H + 1) * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int qx = (int)(i % n);
+        const int64_t r = i / n;
+        const int kz = (int)(r % (H + 1));
+        const int jy = (int)(r / (H + 1));
+        const int kx = qx < n / 2 ? qx : qx - n;
+        double2 v = t3[i];
+        if (kx < -H || kx > H) {
+            v = make_double2(0.0, 0.0);
+        } else {
+            const double d = Dk[((int64_t)(kx + H) * (N + 1) + jy) * (H + 1) + kz];
+            v.x *= d;
+            v.y *= d;
+        }
+        t3[i] = v;
+    }
+}
+
+// T2c [ky' = ky + H][kz][x (all n)] -> T2 [x'][kz][ky (all n)] for x = o + x', zero for |ky| > H
+// (the inverse of prune_t2_k; T2 is zeroed first)
+__global__ void unprune_t2_k(const double2* __restrict__ t2c, int n, int H, int w, int o, double2* __restrict__ t2) {
+    __shared__ double2 tile[32][33];
+    const int kz = blockIdx.z;
+    const int x0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int j = j0 + i, xp = x0 + threadIdx.x;
+        tile[i][threadIdx.x] = (j <= 2 * H && xp < w) ? t2c[((int64_t)j * (H + 1) + kz) * n + o + xp]
+                                                      : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int xp = x0 + i, j = j0 + threadIdx.x;
+        if (xp < w && j <= 2 * H) {
+            const int ky = j - H;
+            const int q = ky < 0 ? ky + n : ky;
+            t2[((int64_t)xp * (H + 1) + kz) * n + q] = tile[threadIdx.x][i];
+        }
+    }
+}
+
+// T1c [x'][kz][y] -> T1 [x'][y][kz] (kz < n/2 + 1; zero for kz > H; the inverse of prune_t1_k)
+__global__ void unprune_t1_k(const double2* __restrict__ t1c, int n, int H, double2* __restrict__ t1) {
+    __shared__ double2 tile[32][33];
+    const int xp = blockIdx.z;
+    const int y0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int half = n / 2 + 1;
+    const double2* src = t1c + (int64_t)xp * (H + 1) * n;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int kz = k0 + i, y = y0 + threadIdx.x;
+        tile[i][threadIdx.x] = (kz <= H && y < n) ? src[(int64_t)kz * n + y] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double2* dst = t1 + (int64_t)xp * n * half;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int y = y0 + i, kz = k0 + threadIdx.x;
+        if (y < n && kz < half) dst[(int64_t)y * half + kz] = tile[threadIdx.x][i];
+    }
+}
+
 }  // namespace
 
 // sum_k D_k |G_k|^2 by a pruned 3-D transform: the grid is zero outside the footprint box
@@ -448,8 +524,8 @@ static void spectrum_energy_pruned(SpectralPlan& sp, double* grid, double2* spec
                                    cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
     const int n = fp.ng, o = fp.box_lo, w = fp.box_w, N = fp.N, H = N / 2;
-    cufftHandle pz, py, px;
-    get_pruned_plans(n, w, H, &pz, &py, &px);
+    cufftHandle pz, py, px, pzi;
+    get_pruned_plans(n, w, H, &pz, &py, &px, &pzi);
     const int half = n / 2 + 1;
     double2* t1 = spec;                                           // w n half
     double2* t1c = t1 + (size_t)w * n * half;                     // w (H+1) n
@@ -470,6 +546,45 @@ static void spectrum_energy_pruned(SpectralPlan& sp, double* grid, double2* spec
     if (comm) comm_allreduce_spectrum(t2c, (size_t)(2 * H + 1) * (H + 1) * n, comm, s);
     pruned_energy_k<<<nparts, 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N, part);
     UOTK_LAUNCHED();
+}
+
+// The kernel-sum chain F^-1 (D . F g) by pruned transforms (d = 3, non-separable kernels,
+// one rank): the forward half as in spectrum_energy_pruned, then D_k on the kept
+// (kx, ky, kz), the inverse x-pass on the (N + 1)(N/2 + 1) kept rows, the inverse y-pass
+// on the w (N/2 + 1) rows of the box slab, the inverse z-pass (C2R) on its w n rows —
+// g' is produced on the box slab [o, o + w) x n x n of `grid` (all a gather reads).
+static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s) {
+    const FastParams& fp = sp.fp;
+    const int n = fp.ng, o = fp.box_lo, w = fp.box_w, N = fp.N, H = N / 2;
+    cufftHandle pz, py, px, pzi;
+    get_pruned_plans(n, w, H, &pz, &py, &px, &pzi);
+    const int half = n / 2 + 1;
+    double2* t1 = spec;                            // w n half
+    double2* t1c = t1 + (size_t)w * n * half;      // w (H+1) n
+    double2* t2c = t1c + (size_t)w * (H + 1) * n;  // (2H+1)(H+1) n
+    for (cufftHandle h : {pz, py, px, pzi}) UOTK_CUFFT(cufftSetStream(h, s));
+    double* slab = grid + (size_t)o * n * n;
+    UOTK_CUFFT(cufftExecD2Z(pz, slab, (cufftDoubleComplex*)t1));
+    dim3 tb(32, 8);
+    prune_t1_k<<<dim3((n + 31) / 32, (H + 32) / 32, w), tb, 0, s>>>(t1, n, H, t1c);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2Z(py, (cufftDoubleComplex*)t1c, (cufftDoubleComplex*)t1c, CUFFT_FORWARD));
+    UOTK_CUDA(cudaMemsetAsync(t2c, 0, (size_t)(2 * H + 1) * (H + 1) * n * sizeof(double2), s));
+    prune_t2_k<<<dim3((w + 31) / 32, (2 * H + 1 + 31) / 32, H + 1), tb, 0, s>>>(t1c, n, H, w, o, t2c);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2Z(px, (cufftDoubleComplex*)t2c, (cufftDoubleComplex*)t2c, CUFFT_FORWARD));
+    prune_scale_k<<<296, 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2Z(px, (cufftDoubleComplex*)t2c, (cufftDoubleComplex*)t2c, CUFFT_INVERSE));
+    UOTK_CUDA(cudaMemsetAsync(t1c, 0, (size_t)w * (H + 1) * n * sizeof(double2), s));
+    unprune_t2_k<<<dim3((w + 31) / 32, (2 * H + 1 + 31) / 32, H + 1), tb, 0, s>>>(t2c, n, H, w, o, t1c);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2Z(py, (cufftDoubleComplex*)t1c, (cufftDoubleComplex*)t1c, CUFFT_INVERSE));
+    unprune_t1_k<<<dim3((n + 31) / 32, (half + 31) / 32, w), tb, 0, s>>>(t1c, n, H, t1);
+    UOTK_LAUNCHED();
+    UOTK_CUFFT(cufftExecZ2D(pzi, (cufftDoubleComplex*)t1, slab));
+    add_launches(6);
+    return grid;
 }
 
 void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
