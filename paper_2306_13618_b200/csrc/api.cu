@@ -31,8 +31,15 @@ void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* gr
 
 namespace {
 
-// AUTO: below this many source-target pairs the direct kernel wins (measured).
-constexpr double kDirectCrossoverPairs = 4.0e7;
+// AUTO: below this many source-target pairs the direct kernel wins (measured, DESIGN.md
+// §10: the direct kernel evaluates ~4e11 pairs/s; a single NFFT kernel sum or MMD^2 costs
+// a fixed ~0.4 ms (d <= 2), ~1 ms (d = 3 Gaussian), ~2.4 ms (d = 3 IMQ, 384^3 grid); a
+// Sinkhorn iteration replayed from a graph ~35 us at C1's size).
+constexpr double kDirectCrossoverPairs = 4.0e7;  // Sinkhorn
+double direct_crossover_sum(int d, int kind) {   // one kernel sum / MMD^2
+    if (d < 3) return 1.5e8;
+    return kind == UOTK_IMQ ? 8.0e8 : 4.0e8;
+}
 
 template <class F>
 int guarded(F&& f) {
@@ -79,14 +86,14 @@ void check_points_arg(int d, int64_t n, const void* p, const char* what) {
     (void)d;
 }
 
-int pick_method(const uotk_opts& o, double pairs, void* comm) {
+int pick_method(const uotk_opts& o, double pairs, void* comm, double crossover = kDirectCrossoverPairs) {
     if (o.method == UOTK_DIRECT) {
         if (comm && comm_nranks(comm) > 1) fail(UOTK_EUNSUPPORTED, "DIRECT method with a multi-rank communicator");
         return UOTK_DIRECT;
     }
     if (o.method == UOTK_NFFT) return UOTK_NFFT;
     if (comm && comm_nranks(comm) > 1) return UOTK_NFFT;
-    return pairs <= kDirectCrossoverPairs ? UOTK_DIRECT : UOTK_NFFT;
+    return pairs <= crossover ? UOTK_DIRECT : UOTK_NFFT;
 }
 
 void fill_info(uotk_info* info, int method, const FastParams* fp) {
@@ -224,7 +231,7 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
     T.bind(tgt, (size_t)n_tgt * d, s);
     OutArr O;
     O.bind(out, (size_t)n_tgt, s);
-    const int method = pick_method(o, (double)n_src * (double)n_tgt, comm);
+    const int method = pick_method(o, (double)n_src * (double)n_tgt, comm, direct_crossover_sum(d, kind));
     if (method == UOTK_DIRECT) {
         fill_info(info, method, nullptr);
         if (n_tgt > 0) {
@@ -604,7 +611,7 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     if (n) UOTK_CUDA(cudaMemcpyAsync(z.p, X.d, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (m) UOTK_CUDA(cudaMemcpyAsync(z.p + (size_t)n * d, Y.d, (size_t)m * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
     signed_concat(A.d, n, B.d, m, w.p, s);
-    const int method = pick_method(o, (double)nz * (double)nz, comm);
+    const int method = pick_method(o, (double)nz * (double)nz, comm, direct_crossover_sum(d, kind));
     if (nz == 0) {
         fill_info(info, method, nullptr);
         *mmd2 = 0.0;
