@@ -10,6 +10,7 @@ targets:
   c3       two C3 iterations (d = 3, n = m = 1M): sinkhorn3d_ws_k, 96^3 FFTs
   c3m6     the same with m = 6, sigma = 3: sinkhorn3d_m6_ws_k, 144^3 grid
   mmd      MMD^2 at n = m = 1M (C2 distributions, Gaussian l = 0.05), the bench's MMD leg
+  mmdimq   the same with the inverse multiquadric (c = 0.05)
   c3sum    one kernel sum on C3's points (x -> y, Gaussian eps = 0.02): stand-alone spread and
            gather kernels on a dense cloud (env M=6 selects m = 6, sigma = 3)
   direct   direct kernel sum d = 3, n = m = 2e5 (direct_k, FP64 exp)
@@ -53,9 +54,10 @@ def main(target):
         pr = W.c5_sum(3, 200_000, kind=W.GAUSS)
         args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param)
         call = lambda: uk.kernel_sum(*args, opts={"method": "direct"})  # noqa: E731
-    elif target == "mmd":
+    elif target in ("mmd", "mmdimq"):
         pr = W.c2_mmd(n=1_000_000)
-        args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.kernels[0][0], pr.kernels[0][1])
+        kk = pr.kernels[0] if target == "mmd" else pr.kernels[1]
+        args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), kk[0], kk[1])
         call = lambda: uk.mmd2(*args, opts={"method": "nfft"})  # noqa: E731
     elif target == "c3sum":
         pr = W.c3_uot(iters=2)
