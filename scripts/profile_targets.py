@@ -15,6 +15,7 @@ targets:
            gather kernels on a dense cloud (env M=6 selects m = 6, sigma = 3)
   direct   direct kernel sum d = 3, n = m = 2e5 (direct_k, FP64 exp)
   sum3dimq kernel sum d=3, n = m = 1e6, IMQ c = 0.05 (N = 192, grid 384^3)
+  c1       five C1 solves (d = 2, 1000 + 1000 points, DIRECT: direct_warp_k)
   sum1d    kernel sum d = 1, n = m = 1e7 (chunked1d_k)
 Each target runs its call twice (the first call warms plans and caches); the second runs
 inside the NVTX range "prof" (ncu --nvtx --nvtx-include "prof/").
@@ -46,6 +47,10 @@ def main(target):
         pr = W.c5_sum(3, 1_000_000, kind=W.IMQ)
         args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "imq", pr.param)
         call = lambda: uk.kernel_sum(*args, opts={"method": "nfft"})  # noqa: E731
+    elif target == "c1":
+        pr = W.c1_uot()
+        args = (cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam)
+        call = lambda: uk.uot_sinkhorn(*args, iters=pr.iters, opts={"method": "direct"})  # noqa: E731
     elif target == "sum1d":
         pr = W.c5_sum(1, 10_000_000, kind=W.GAUSS)
         args = (cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), "gauss", pr.param)
