@@ -696,3 +696,20 @@ def test_error_paths_overflow_and_nonfinite(uk):
     with pytest.raises(uk.UotkError) as e:
         uk.kernel_sum(cuda(xs), cuda(np.ones(200)), cuda(xs), "gauss", 0.0025, opts={"method": "nfft"})
     assert e.value.code == -2
+
+
+def test_auto_method_crossover(uk):
+    """AUTO picks the direct kernel below the measured crossover (DESIGN.md §1 a0): a d = 3
+    kernel sum of 1e4 x 1e4 pairs (1e8 < 4e8) runs direct, 3e4 x 3e4 (9e8) runs the NFFT;
+    both agree with each other."""
+    small = W.random_sum(3, 10_000, 10_000, kind=W.GAUSS, param=0.0025, seed=7)
+    got, info = uk.kernel_sum(cuda(small.src), cuda(small.alpha), cuda(small.tgt), "gauss", small.param,
+                              return_info=True)
+    assert info["method"] == "direct"
+    big = W.random_sum(3, 30_000, 30_000, kind=W.GAUSS, param=0.0025, seed=8)
+    got_b, info_b = uk.kernel_sum(cuda(big.src), cuda(big.alpha), cuda(big.tgt), "gauss", big.param,
+                                  return_info=True)
+    assert info_b["method"] == "nfft"
+    ref_b = uk.kernel_sum(cuda(big.src), cuda(big.alpha), cuda(big.tgt), "gauss", big.param,
+                          opts={"method": "direct"})
+    assert rel_err(got_b.cpu().numpy(), ref_b.cpu().numpy(), False) <= 1e-9
