@@ -80,7 +80,10 @@ typedef struct {
     int32_t method;   /* uotk_method                                                     */
     int32_t N;        /* bandwidth per axis of I_N (Eq. 4.4), even; 0 = auto       */
     double sigma;     /* oversampling: grid n_g = sigma * N per axis (even); 0 = 2.0      */
-    int32_t m;        /* window half-width; 2m taps per axis (footnote P:653); 0 = 8      */
+    int32_t m;        /* window half-width; 2m taps per axis (footnote P:653); 0 = 8.
+                         Tuned cell-group kernels: m = 8 (d = 1..3) and m = 6 (d = 3; with
+                         sigma = 3 its window error ~4e-12, R23); other m run on
+                         the generic kernels                                              */
     int32_t p;        /* IMQ boundary polynomial order (K_B); 0 = 12          */
     double eps_B;     /* IMQ boundary band width in torus units; 0 = auto                 */
     double h;         /* torus scaling h (Eq. 4.7, Rem. 4.3 P:610); 0 = auto        */
