@@ -34,9 +34,15 @@
  *    (NCCL all-reduce) so each rank obtains the sums at its own targets from
  *    all ranks' sources.  Scalar results (uot result, mmd2) are global and
  *    identical on all ranks.
+ *    A rank's local shard may be empty (n = 0 or m = 0) with a multi-rank
+ *    communicator: it still takes part in every collective.  Input and numeric
+ *    errors (UOTK_EDOMAIN, UOTK_EOVERFLOW) are decided on flags or-ed over all ranks,
+ *    so every rank returns the same status, and the stopping rule's sup-norm changes
+ *    are maxed over ranks (all ranks stop at the same iteration).
  *  - Return value: UOTK_OK (0) or a negative status; uotk_last_error() returns a
  *    thread-local description of the last failure.  No C++ exception crosses
- *    the ABI.  Not re-entrant on one device from several host threads.
+ *    the ABI.  Several host threads may call the library concurrently on one
+ *    device only as the ranks of one loopback group (uotk_comm_create_loopback).
  */
 #ifndef UOTK_H
 #define UOTK_H
@@ -47,7 +53,7 @@
 extern "C" {
 #endif
 
-#define UOTK_ABI_VERSION 2
+#define UOTK_ABI_VERSION 3
 
 /* Status codes (mirroring SPEC's split of input vs numeric errors). */
 enum {
@@ -117,6 +123,16 @@ typedef struct {
     int32_t n_grid;      /* oversampled grid points per axis (0 for DIRECT) */
     int32_t m;           /* window half-width (0 for DIRECT) */
     double h;            /* torus scaling (0 for DIRECT) */
+    /* Cell-group layout of the two point sets on the NFFT path: 0 = the
+     * generic thread-per-point kernels; otherwise the z extent of a group's window
+     * footprint: 16 = one-cell groups (m = 8; in d = 3 the warp-specialised half-step
+     * sinkhorn3d_ws_k), 12 = one-cell groups with m = 6, 24 / 40 = z-segment groups of
+     * sparse d = 3 clouds.  Set 1 = src (kernel sum), x (UOT) or z = x u y (MMD^2);
+     * set 2 = tgt (kernel sum) or y (UOT), 0 for MMD^2. */
+    int32_t groups1;
+    int32_t groups2;
+    int32_t nranks;      /* ranks of the communicator (1 without one) */
+    int32_t reserved;
 } uotk_info;
 
 /* Result of uotk_uot_sinkhorn, all global over ranks.
@@ -252,6 +268,19 @@ int uotk_uot_sinkhorn_scaling(int d, int64_t n, const double* x, const double* a
 int uotk_comm_unique_id(void* id128);
 int uotk_comm_create(const void* id128, int nranks, int rank, void** comm_out);
 int uotk_comm_destroy(void* comm);
+
+/* Loopback group: nranks (1..16) communicator handles for ONE process on ONE GPU, written
+ * to comms_out[0..nranks-1] (handle k = rank k).  It stands in for nranks processes (the
+ * multi-rank path tested with a single device): each handle is used by one host thread,
+ * all nranks threads call the same entry point concurrently with their own shards and
+ * streams.  Every all-reduce of the exchange step (Fourier coefficients, bounding box,
+ * scalars) is performed by a library kernel that sums (or maxes) the nranks device
+ * buffers in rank order, ordered by CUDA events and host barriers — no kernel waits on
+ * another.  A rank whose call fails aborts the group (the others fail with UOTK_ENCCL at
+ * their next collective; a rank that never arrives times out after 120 s).  Results equal
+ * NCCL's up to the summation order; timings are not representative.  Destroy each
+ * handle with uotk_comm_destroy. */
+int uotk_comm_create_loopback(int nranks, void** comms_out);
 
 /* Thread-local description of the last error (never NULL). */
 const char* uotk_last_error(void);

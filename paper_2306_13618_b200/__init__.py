@@ -128,7 +128,8 @@ def _comm_ptr(comm):
 
 def _info_dict(info):
     return {"method": {1: "nfft", 2: "direct"}.get(info.method_used, "?"), "N": info.N,
-            "n_grid": info.n_grid, "m": info.m, "h": info.h}
+            "n_grid": info.n_grid, "m": info.m, "h": info.h, "groups": (info.groups1, info.groups2),
+            "nranks": info.nranks}
 
 
 def kernel_sum(src, alpha, tgt, kind="gauss", param=None, opts=None, comm=None, stream=None, out=None,
@@ -313,6 +314,20 @@ class Comm:
         buf = ctypes.create_string_buffer(128)
         _native.check(_native.load().uotk_comm_unique_id(buf))
         return buf.raw
+
+    @classmethod
+    def loopback(cls, nranks: int):
+        """nranks rank handles of one loopback group (uotk_comm_create_loopback): the
+        multi-rank path in one process on one GPU, one host thread per rank."""
+        lib = _native.load()
+        hs = (ctypes.c_void_p * nranks)()
+        _native.check(lib.uotk_comm_create_loopback(nranks, hs))
+        out = []
+        for k in range(nranks):
+            c = cls.__new__(cls)
+            c.handle, c.nranks, c.rank = hs[k], nranks, k
+            out.append(c)
+        return out
 
     @classmethod
     def from_torch_distributed(cls):

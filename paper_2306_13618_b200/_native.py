@@ -21,7 +21,7 @@ STATUS = {
 EXPORTED = (
     "uotk_opts_init", "uotk_kernel_sum", "uotk_uot_sinkhorn", "uotk_mmd2",
     "uotk_uot_cstar", "uotk_sinkhorn_divergence", "uotk_uot_sinkhorn_scaling", "uotk_uot_sinkhorn_ex",
-    "uotk_comm_unique_id", "uotk_comm_create", "uotk_comm_destroy",
+    "uotk_comm_unique_id", "uotk_comm_create", "uotk_comm_create_loopback", "uotk_comm_destroy",
     "uotk_last_error", "uotk_abi_version", "uotk_launch_counter", "uotk_launch_counter_reset",
     "uotk_profile_enable", "uotk_profile_reset", "uotk_profile_read", "uotk_release_caches",
 )
@@ -40,7 +40,8 @@ class UotkOpts(ctypes.Structure):
 class UotkInfo(ctypes.Structure):
     _fields_ = [
         ("method_used", ctypes.c_int32), ("N", ctypes.c_int32), ("n_grid", ctypes.c_int32),
-        ("m", ctypes.c_int32), ("h", ctypes.c_double),
+        ("m", ctypes.c_int32), ("h", ctypes.c_double), ("groups1", ctypes.c_int32),
+        ("groups2", ctypes.c_int32), ("nranks", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -103,6 +104,8 @@ def load():
     lib.uotk_comm_unique_id.restype = INT
     lib.uotk_comm_create.argtypes = [P, INT, INT, ctypes.POINTER(P)]
     lib.uotk_comm_create.restype = INT
+    lib.uotk_comm_create_loopback.argtypes = [INT, ctypes.POINTER(P)]
+    lib.uotk_comm_create_loopback.restype = INT
     lib.uotk_comm_destroy.argtypes = [P]
     lib.uotk_comm_destroy.restype = INT
     lib.uotk_last_error.argtypes = []

@@ -17,7 +17,11 @@ void comm_unique_id(void* id128);
 void* comm_create(const void* id128, int nranks, int rank);
 void comm_destroy(void* comm);
 void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);
+void comm_allreduce_i32(int32_t* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);
 int comm_nranks(void* comm);
+bool comm_capturable(void* comm);
+void comm_create_loopback(int nranks, void** out);
+void comm_abort(void* comm, const std::string& why);
 void ensure_pool();
 cudaStream_t private_stream();  // context.cu
 
@@ -41,19 +45,26 @@ double direct_crossover_sum(int d, int kind) {   // one kernel sum / MMD^2
     return kind == UOTK_IMQ ? 8.0e8 : 4.0e8;
 }
 
+// Runs f, mapping exceptions to status codes.  With a communicator the thread's resource
+// slot is the rank's (loopback groups), and a failing rank aborts a loopback group so
+// that its other ranks fail at their next collective instead of waiting for it.
 template <class F>
-int guarded(F&& f) {
+int guarded(F&& f, void* comm = nullptr) {
+    SlotScope slot(comm);
     try {
         f();
         return UOTK_OK;
     } catch (const Error& e) {
         g_last_error = e.msg;
+        comm_abort(comm, e.msg);
         return e.code;
     } catch (const std::exception& e) {
         g_last_error = std::string("internal error: ") + e.what();
+        comm_abort(comm, g_last_error);
         return UOTK_ECUDA;
     } catch (...) {
         g_last_error = "internal error";
+        comm_abort(comm, g_last_error);
         return UOTK_ECUDA;
     }
 }
@@ -96,15 +107,21 @@ int pick_method(const uotk_opts& o, double pairs, void* comm, double crossover =
     return pairs <= crossover ? UOTK_DIRECT : UOTK_NFFT;
 }
 
-void fill_info(uotk_info* info, int method, const FastParams* fp) {
+int group_code(const PointSet* ps) { return (ps && ps->chunked) ? ps->chunk_kz : 0; }
+
+void fill_info(uotk_info* info, int method, const FastParams* fp, void* comm, const PointSet* p1 = nullptr,
+               const PointSet* p2 = nullptr) {
     if (!info) return;
     memset(info, 0, sizeof *info);
     info->method_used = method;
+    info->nranks = comm_nranks(comm);
     if (fp) {
         info->N = fp->N;
         info->n_grid = fp->ng;
         info->m = fp->m;
         info->h = fp->h;
+        info->groups1 = group_code(p1);
+        info->groups2 = group_code(p2);
     }
 }
 
@@ -151,14 +168,16 @@ constexpr int kGraphIters = 16;  // iterations per captured graph
 // the remaining iterations (including the last, whose epilogue differs) run eagerly.
 template <class F>
 int run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s, int check_every = 0,
-                   double stop_tol = 0.0, const unsigned long long* dmax = nullptr) {
+                   double stop_tol = 0.0, unsigned long long* dmax = nullptr, void* comm = nullptr) {
     if (check_every > 0) {
         // stopping rule: after every check_every-th iteration read the two sup-norm
         // changes (non-negative doubles stored as their bit patterns) and stop if both
-        // are <= stop_tol
+        // are <= stop_tol.  With a communicator the changes are maxed over ranks first, so
+        // every rank takes the same decision (and issues the same collectives).
         for (int it = 0; it < iters; ++it) {
             iterate(it);
             if ((it + 1) % check_every == 0 && it + 1 < iters) {
+                if (comm) comm_allreduce(reinterpret_cast<double*>(dmax), 2, 1, comm, s);
                 unsigned long long h[2];
                 UOTK_CUDA(cudaMemcpyAsync(h, dmax, sizeof h, cudaMemcpyDeviceToHost, s));
                 UOTK_CUDA(cudaStreamSynchronize(s));
@@ -201,7 +220,17 @@ int run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s, int c
     return iters;
 }
 
-int read_flag(const DevBuf<int>& flag, cudaStream_t s) {
+// reads the status flag (bits: 1|2 overflow in the loop, 4 bad mass, 8 non-finite
+// coordinate); with a communicator the flags of all ranks are or-ed first (one max
+// all-reduce of the bits spread over 4 words), so every rank fails or succeeds together
+int read_flag(const DevBuf<int>& flag, cudaStream_t s, void* comm = nullptr) {
+    if (comm) {
+        // or over ranks, bit by bit: spread the bits into 4 words, max-reduce, fold back
+        DevBuf<int32_t> bits(4, s);
+        split_bits(flag.p, bits.p, s);
+        comm_allreduce_i32(bits.p, 4, 1, comm, s);
+        join_bits(bits.p, flag.p, s);
+    }
     int h = 0;
     UOTK_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     UOTK_CUDA(cudaStreamSynchronize(s));
@@ -233,7 +262,13 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
     O.bind(out, (size_t)n_tgt, s);
     const int method = pick_method(o, (double)n_src * (double)n_tgt, comm, direct_crossover_sum(d, kind));
     if (method == UOTK_DIRECT) {
-        fill_info(info, method, nullptr);
+        fill_info(info, method, nullptr, comm);
+        // the NFFT path validates coordinates in compute_geometry; here a flag kernel does
+        DevBuf<int> flag(1, s);
+        flag.zero();
+        check_finite(S.d, n_src * d, flag.p, 8, s);
+        check_finite(T.d, n_tgt * d, flag.p, 8, s);
+        if (read_flag(flag, s) & 8) fail(UOTK_EDOMAIN, "non-finite point coordinate");
         if (n_tgt > 0) {
             if (n_src == 0) UOTK_CUDA(cudaMemsetAsync(O.d, 0, n_tgt * sizeof(double), s));
             else direct_sum_epi(d, n_src, S.d, A.d, n_tgt, T.d, kind, param, EpiStore{O.d, nullptr}, nullptr, s);
@@ -241,12 +276,12 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
     } else {
         NfftSetup ns;
         setup_nfft(ns, d, kind, param, S.d, n_src, T.d, n_tgt, o, comm, s);
-        fill_info(info, method, &ns.fp);
         PointSet PS, PT;
         make_pointset(PS, S.d, n_src, ns.fp, s, kUseSpreadOnly);
         trace_mark("pointset src");
         make_pointset(PT, T.d, n_tgt, ns.fp, s, kUseGatherOnly);
         trace_mark("pointset tgt");
+        fill_info(info, method, &ns.fp, comm, &PS, &PT);
         DevBuf<double> w(n_src, s), grid(grid_elems(ns.fp), s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
         permute_values(w.p, A.d, PS.perm.p, n_src, s);
@@ -257,7 +292,9 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         trace_mark("passes enqueued");
     }
     O.flush();
-    if (O.host) UOTK_CUDA(cudaStreamSynchronize(s));
+    // host outputs, and host inputs staged by asynchronous copies (pinned memory), must be
+    // complete before the call returns: the library keeps no caller pointer afterwards
+    if (O.host || S.host || A.host || T.host) UOTK_CUDA(cudaStreamSynchronize(s));
 }
 
 // ============================================================== UOT Sinkhorn
@@ -266,8 +303,12 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                      double* gamma_out, uotk_uot_result* res, const uotk_opts* opts_in, void* comm, cudaStream_t s,
                      double* p_out = nullptr, double* q_out = nullptr) {
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
-    need(n >= 1 && m >= 1, "n and m must be >= 1");
-    need(x && a && y && b && beta_out && gamma_out, "null pointer argument");
+    // a rank's local shard may be empty (it still takes part in every collective)
+    if (comm_nranks(comm) > 1) need(n >= 0 && m >= 0, "n and m must be >= 0");
+    else need(n >= 1 && m >= 1, "n and m must be >= 1");
+    need((x || n == 0) && (a || n == 0) && (y || m == 0) && (b || m == 0) && (beta_out || n == 0) &&
+             (gamma_out || m == 0),
+         "null pointer argument");
     need(eps > 0 && std::isfinite(eps), "eps must be positive and finite");
     need(lam1 > 0 && lam2 > 0 && std::isfinite(lam1) && std::isfinite(lam2), "lam1, lam2 must be positive");
     need(iters >= 0, "iters must be >= 0");
@@ -298,6 +339,10 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     dmax.zero();
 
     const int method = pick_method(o, (double)n * (double)m, comm);
+    if (method == UOTK_DIRECT) {
+        check_finite(X.d, n * d, flag.p, 8, s);
+        check_finite(Y.d, m * d, flag.p, 8, s);
+    }
     // per-point state: potentials, masses, next weights, t at x (final) and t~ at y (last)
     DevBuf<double> pot_x(n, s), pot_y(m, s), mass_x(n, s), mass_y(m, s), wx(n, s), wy(m, s), tx(n, s), ty(m, s);
     DevBuf<double> tpx;  // t' at x for the transport term
@@ -327,7 +372,11 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         if (gamma_init) permute_values(pot_y.p, G0.d, perm_y, m, s);
         else pot_y.zero();
     }
-    if (read_flag(flag, s) & 4) fail(UOTK_EDOMAIN, "masses must be positive and finite (KL needs mu_i > 0)");
+    {
+        const int f0 = read_flag(flag, s, comm);
+        if (f0 & 8) fail(UOTK_EDOMAIN, "non-finite point coordinate");
+        if (f0 & 4) fail(UOTK_EDOMAIN, "masses must be positive and finite (KL needs mu_i > 0)");
+    }
 
     // v = e^{lam gamma^0}: weights of the first beta-step
     scaled_mass(mass_y.p, pot_y.p, m, lam, wy.p, s);
@@ -337,7 +386,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     // small problems are launch-bound: replay the iteration from a CUDA graph
     const bool stop_rule = o.stop_tol > 0;
     const bool use_graph =
-        comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints && !profiling_enabled() && !stop_rule;
+        comm_capturable(comm) && iters >= 4 && n + m <= kGraphMaxPoints && !profiling_enabled() && !stop_rule;
     // iterations whose sup-norm changes are recorded: the last one, and with the stopping
     // rule every check_every-th one (dmax is reset before each of them)
     auto records = [&](int it) { return it == iters - 1 || (stop_rule && (it + 1) % o.check_every == 0); };
@@ -351,7 +400,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
             if (last) e2.t_store = ty.p;
             direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
         };
-        done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p);
+        done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p, comm);
         // marginals of the recovered plan: t at x from the final gamma
         direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, EpiStore{tx.p, nullptr}, nullptr, s);
         // <pi, d^2>: t' at x with the kernel d^2 k (UOTK_GAUSS_R2) against the same weights
@@ -394,7 +443,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                 spread(PY, wy.p, grid.p, fp, s);
             }
         };
-        done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p);
+        done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p, comm);
         // grid holds the spread of nu (.) v with the final v: t at x for the marginals
         if (want_transport) {
             // the same spread grid through the D_k of the kernel d^2 k (same N, n_g, h)
@@ -460,7 +509,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     GO.flush();
     if (p_out) PO.flush();
     if (q_out) QO.flush();
-    const int fl = read_flag(flag, s);  // synchronises the stream
+    const int fl = read_flag(flag, s, comm);  // synchronises the stream
     if (fl & 3) fail(UOTK_EOVERFLOW, "non-positive or non-finite kernel sum / scaling in the Sinkhorn loop");
 
     if (res) {
@@ -478,7 +527,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         res->max_dbeta = hs[10];
         res->max_dgamma = hs[11];
         res->iters = done;
-        fill_info(&res->info, method, fpp);
+        fill_info(&res->info, method, fpp, comm, &PX, &PY);
         res->transport = want_transport ? hs[12] : std::nan("");
     }
 }
@@ -540,8 +589,9 @@ static void cstar_impl(int d, int64_t n, const double* x, const double* a, int64
                        const double* b, double eps, double lam1, double lam2, double* cstar, void* comm,
                        cudaStream_t s) {
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
-    need(n >= 1 && m >= 1, "n and m must be >= 1");
-    need(x && a && y && b && cstar, "null pointer argument");
+    if (comm_nranks(comm) > 1) need(n >= 0 && m >= 0, "n and m must be >= 0");  // empty shards take part
+    else need(n >= 1 && m >= 1, "n and m must be >= 1");
+    need((x || n == 0) && (a || n == 0) && (y || m == 0) && (b || m == 0) && cstar, "null pointer argument");
     need(eps > 0 && std::isfinite(eps), "eps must be positive and finite");
     need(lam1 > 0 && lam2 > 0 && std::isfinite(lam1) && std::isfinite(lam2), "lam1, lam2 must be positive");
     ensure_pool();
@@ -554,7 +604,13 @@ static void cstar_impl(int d, int64_t n, const double* x, const double* a, int64
     flag.zero();
     check_mass(A.d, n, flag.p, s);
     check_mass(B.d, m, flag.p, s);
-    if (read_flag(flag, s) & 4) fail(UOTK_EDOMAIN, "masses must be positive and finite");
+    check_finite(X.d, n * d, flag.p, 8, s);
+    check_finite(Y.d, m * d, flag.p, 8, s);
+    {
+        const int f0 = read_flag(flag, s, comm);
+        if (f0 & 8) fail(UOTK_EDOMAIN, "non-finite point coordinate");
+        if (f0 & 4) fail(UOTK_EDOMAIN, "masses must be positive and finite");
+    }
     const int nc = 2 + d;
     DevBuf<double> cols((size_t)nc * std::max(n, m), s), sums(2 * nc, s), cen(2 * d, s);
     // <mu x nu | d^2> = A B |mx - my|^2 + B sum a |x - mx|^2 + A sum b |y - my|^2 with the
@@ -612,13 +668,17 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     if (m) UOTK_CUDA(cudaMemcpyAsync(z.p + (size_t)n * d, Y.d, (size_t)m * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
     signed_concat(A.d, n, B.d, m, w.p, s);
     const int method = pick_method(o, (double)nz * (double)nz, comm, direct_crossover_sum(d, kind));
-    if (nz == 0) {
-        fill_info(info, method, nullptr);
+    if (nz == 0 && comm_nranks(comm) == 1) {  // with several ranks an empty shard still takes part
+        fill_info(info, method, nullptr, comm);
         *mmd2 = 0.0;
         return;
     }
     if (method == UOTK_DIRECT) {
-        fill_info(info, method, nullptr);
+        fill_info(info, method, nullptr, comm);
+        DevBuf<int> flag(1, s);
+        flag.zero();
+        check_finite(z.p, nz * d, flag.p, 8, s);
+        if (read_flag(flag, s) & 8) fail(UOTK_EDOMAIN, "non-finite point coordinate");
         direct_sum_epi(d, nz, z.p, w.p, nz, z.p, kind, param, EpiDot{w.p, prod.p}, nullptr, s);
         sum_columns(prod.p, nz, 1, sum.p, s);
     } else {
@@ -627,9 +687,9 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
         // spectrum is all-reduced first, so every rank forms the same global value.
         NfftSetup ns;
         setup_nfft(ns, d, kind, param, z.p, nz, nullptr, 0, o, comm, s);
-        fill_info(info, method, &ns.fp);
         PointSet PZ;
         make_pointset(PZ, z.p, nz, ns.fp, s, kUseSpreadOnly);
+        fill_info(info, method, &ns.fp, comm, &PZ);
         constexpr int kParts = 296;
         DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s), part(kParts, s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
@@ -660,7 +720,7 @@ int uotk_kernel_sum(int d, int64_t n_src, const double* src, const double* alpha
     return guarded([&] {
         kernel_sum_impl(d, n_src, src, alpha, n_tgt, tgt, kind, param, out, opts, info, comm,
                         (cudaStream_t)cuda_stream);
-    });
+    }, comm);
 }
 
 int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
@@ -668,11 +728,11 @@ int uotk_uot_sinkhorn(int d, int64_t n, const double* x, const double* a, int64_
                       double* gamma, uotk_uot_result* res, const uotk_opts* opts, void* comm, void* cuda_stream) {
     return guarded([&] {
         cudaStream_t cs = (cudaStream_t)cuda_stream;
-        const bool graphable = comm == nullptr && iters >= 4 && n >= 0 && m >= 0 && n + m <= kGraphMaxPoints;
+        const bool graphable = comm_capturable(comm) && iters >= 4 && n >= 0 && m >= 0 && n + m <= kGraphMaxPoints;
         on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
             uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, st);
         });
-    });
+    }, comm);
 }
 
 int uotk_mmd2(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
@@ -680,7 +740,7 @@ int uotk_mmd2(int d, int64_t n, const double* x, const double* a, int64_t m, con
               void* cuda_stream) {
     return guarded([&] {
         mmd2_impl(d, n, x, a, m, y, b, kind, param, mmd2, opts, info, comm, (cudaStream_t)cuda_stream);
-    });
+    }, comm);
 }
 
 int uotk_uot_cstar(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y, const double* b,
@@ -695,11 +755,11 @@ int uotk_sinkhorn_divergence(int d, int64_t n, const double* x, const double* a,
         need(n >= 1 && m >= 1, "n and m must be >= 1");
         need(iters >= 0, "iters must be >= 0");
         cudaStream_t cs = (cudaStream_t)cuda_stream;
-        const bool graphable = comm == nullptr && iters >= 4 && 2 * std::max(n, m) <= kGraphMaxPoints;
+        const bool graphable = comm_capturable(comm) && iters >= 4 && 2 * std::max(n, m) <= kGraphMaxPoints;
         on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
             sd_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, sd, terms, opts, comm, st);
         });
-    });
+    }, comm);
 }
 
 int uotk_uot_sinkhorn_ex(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
@@ -708,12 +768,12 @@ int uotk_uot_sinkhorn_ex(int d, int64_t n, const double* x, const double* a, int
                          const uotk_opts* opts, void* comm, void* cuda_stream) {
     return guarded([&] {
         cudaStream_t cs = (cudaStream_t)cuda_stream;
-        const bool graphable = comm == nullptr && iters >= 4 && n >= 0 && m >= 0 && n + m <= kGraphMaxPoints;
+        const bool graphable = comm_capturable(comm) && iters >= 4 && n >= 0 && m >= 0 && n + m <= kGraphMaxPoints;
         on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
             uot_impl(d, n, x, a, m, y, b, eps, lam1, lam2, iters, gamma_init, beta, gamma, res, opts, comm, st, p,
                      q);
         });
-    });
+    }, comm);
 }
 
 int uotk_uot_sinkhorn_scaling(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
@@ -725,7 +785,7 @@ int uotk_uot_sinkhorn_scaling(int d, int64_t n, const double* x, const double* a
         for (int k = 0; k < n_eps; ++k) need(eps_list[k] > 0 && std::isfinite(eps_list[k]), "eps_list: eps > 0");
         need(n >= 1 && m >= 1 && beta && gamma, "n, m >= 1 and beta, gamma required");
         cudaStream_t cs = (cudaStream_t)cuda_stream;
-        const bool graphable = comm == nullptr && iters >= 4 && n + m <= kGraphMaxPoints;
+        const bool graphable = comm_capturable(comm) && iters >= 4 && n + m <= kGraphMaxPoints;
         on_capturable_stream(cs, graphable, [&](cudaStream_t st) {
             // the previous stage's gamma (device, caller order) warm-starts the next stage
             DevBuf<double> g0(m, st), bt(n, st);
@@ -751,7 +811,7 @@ int uotk_uot_sinkhorn_scaling(int d, int64_t n, const double* x, const double* a
             r.iters = total;
             if (res) *res = r;
         });
-    });
+    }, comm);
 }
 
 int uotk_comm_unique_id(void* id128) {
@@ -765,6 +825,13 @@ int uotk_comm_create(const void* id128, int nranks, int rank, void** comm_out) {
     return guarded([&] {
         if (!id128 || !comm_out) fail(UOTK_EINVAL, "null argument");
         *comm_out = comm_create(id128, nranks, rank);
+    });
+}
+
+int uotk_comm_create_loopback(int nranks, void** comms_out) {
+    return guarded([&] {
+        if (!comms_out) fail(UOTK_EINVAL, "null argument");
+        comm_create_loopback(nranks, comms_out);
     });
 }
 

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -37,6 +38,16 @@ void add_launches(int k);                      // launches made by library code 
 // trace_mark prints the host microseconds since the previous mark to stderr
 void trace_mark(const char* what);
 
+// Per-thread resource slot (comm.cu comm_slot): the rank of a loopback communicator whose
+// ranks run concurrently on one device from several host threads, else 0.  The cuFFT
+// plans and the cuBLAS handle are cached per (device, slot).
+extern thread_local int g_slot;
+struct SlotScope {
+    int prev;
+    explicit SlotScope(void* comm);
+    ~SlotScope() { g_slot = prev; }
+};
+
 // ------------------------------------------------------------------ device buffers
 // Device allocation through the library's block cache (context.cu), backed by the
 // stream-ordered pool (cudaMallocAsync on the call's stream).
@@ -67,6 +78,7 @@ void release_fft_plans();     // context.cu: destroy the cached cuFFT plans
 // pointer valid for the duration of the call.
 struct InArr {
     const double* d = nullptr;
+    bool host = false;  // staged from host memory (an async copy when the memory is pinned)
     DevBuf<double> staged;
     void bind(const double* user, size_t count, cudaStream_t s);
 };
@@ -141,6 +153,11 @@ struct PlanData {
     bool separable = false;
     DevBuf<double> Csep;
     cudaEvent_t ready = nullptr;
+    // completion of the last use on each stream that used the tables (recorded when a
+    // call's SpectralPlan ends): the destructor waits for exactly these, not the device
+    std::mutex use_mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+    void note_use(cudaStream_t s);
     PlanData() = default;
     PlanData(const PlanData&) = delete;
     PlanData& operator=(const PlanData&) = delete;
@@ -154,6 +171,10 @@ struct SpectralPlan {
     cufftHandle r2c = 0, c2r = 0;  // owned by the context cache
     size_t grid_elems = 0;   // ng^d
     size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
+    cudaStream_t use_stream = nullptr;  // the call's stream (build_spectral_plan)
+    ~SpectralPlan() {
+        if (pd) pd->note_use(use_stream);
+    }
 };
 
 // ------------------------------------------------------------------ library context

@@ -15,6 +15,9 @@ namespace uotk {
 
 thread_local std::string g_last_error = "no error";
 thread_local int64_t g_launches = 0;
+thread_local int g_slot = 0;
+int comm_slot(void* comm);  // comm.cu
+SlotScope::SlotScope(void* comm) : prev(g_slot) { g_slot = comm_slot(comm); }
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
 
@@ -262,6 +265,7 @@ void InArr::bind(const double* user, size_t count, cudaStream_t s) {
     staged.alloc(count, s);
     UOTK_CUDA(cudaMemcpyAsync(staged.p, user, count * sizeof(double), cudaMemcpyHostToDevice, s));
     d = staged.p;
+    host = true;
 }
 
 void OutArr::bind(double* user_ptr, size_t cnt, cudaStream_t stream) {
@@ -285,12 +289,12 @@ void OutArr::flush() {
 // ------------------------------------------------------------------ context
 struct Context {
     std::mutex mu;
-    // (device, d, n) -> (r2c, c2r)
-    std::map<std::tuple<int, int, int>, std::pair<cufftHandle, cufftHandle>> fft;
+    // (device, slot, d, n) -> (r2c, c2r)
+    std::map<std::tuple<int, int, int, int>, std::pair<cufftHandle, cufftHandle>> fft;
     bool pool_configured[64] = {};
-    std::map<int, cublasHandle_t> blas;
-    // (device, n, w, H) -> pruned-transform plans (pass z R2C, pass y C2C, pass x C2C)
-    std::map<std::tuple<int, int, int, int>, std::array<cufftHandle, 4>> pruned;
+    std::map<std::pair<int, int>, cublasHandle_t> blas;  // (device, slot)
+    // (device, slot, n, w, H) -> pruned-transform plans (pass z R2C, pass y C2C, pass x C2C)
+    std::map<std::tuple<int, int, int, int, int>, std::array<cufftHandle, 4>> pruned;
     std::map<int, cudaStream_t> streams;
 };
 
@@ -330,7 +334,7 @@ void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r) {
     Context& c = ctx();
     std::lock_guard<std::mutex> lk(c.mu);
     configure_pool(dev);
-    auto key = std::make_tuple(dev, d, n);
+    auto key = std::make_tuple(dev, g_slot, d, n);
     auto it = c.fft.find(key);
     if (it != c.fft.end()) {
         *r2c = it->second.first;
@@ -358,7 +362,7 @@ void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cuf
     UOTK_CUDA(cudaGetDevice(&dev));
     Context& c = ctx();
     std::lock_guard<std::mutex> lk(c.mu);
-    auto key = std::make_tuple(dev, n, w, H);
+    auto key = std::make_tuple(dev, g_slot, n, w, H);
     auto it = c.pruned.find(key);
     if (it == c.pruned.end()) {
         std::array<cufftHandle, 4> h{};
@@ -385,11 +389,11 @@ void get_cublas(void** handle) {
     UOTK_CUDA(cudaGetDevice(&dev));
     Context& c = ctx();
     std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.blas.find(dev);
+    auto it = c.blas.find({dev, g_slot});
     if (it == c.blas.end()) {
         cublasHandle_t h;
         if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cublasCreate failed");
-        it = c.blas.emplace(dev, h).first;
+        it = c.blas.emplace(std::make_pair(dev, g_slot), h).first;
     }
     *handle = it->second;
 }

@@ -150,6 +150,128 @@ __global__ void scale_spectrum_k(double2* __restrict__ spec, const double* __res
     spec[i] = v;
 }
 
+// ---- the exchange step of the multi-rank path on the truncated spectrum only (SURVEY
+// §8(e)): the ranks' partial coefficients are needed on I_N alone (D_k vanishes outside),
+// so they are packed into the D_k layout ((N+1)^(d-1) (N/2+1) complex: 1/8 of the half
+// spectrum in d = 3 at sigma = 2), all-reduced, and unpacked (zeros elsewhere).
+
+// decode a D_k-layout index into the half-spectrum index of an n_g^d grid
+template <int D>
+__device__ __forceinline__ int64_t compact_to_spec(int64_t i, int ng, int N) {
+    const int nh = N / 2 + 1;
+    const int kl = (int)(i % nh);
+    int64_t rem = i / nh;
+    int64_t sidx = kl, sstride = ng / 2 + 1;
+#pragma unroll
+    for (int t = D - 2; t >= 0; --t) {
+        const int k = (int)(rem % (N + 1)) - N / 2;
+        rem /= (N + 1);
+        sidx += (int64_t)(k < 0 ? k + ng : k) * sstride;
+        sstride *= ng;
+    }
+    return sidx;
+}
+
+// compact[i] = spec[...] (* Dk[i] if Dk)
+template <int D>
+__global__ void pack_spectrum_k(const double2* __restrict__ spec, const double* __restrict__ Dk, int ng, int N,
+                                int64_t ndk, double2* __restrict__ compact) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ndk; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 v = spec[compact_to_spec<D>(i, ng, N)];
+        if (Dk) {
+            const double f = Dk[i];
+            v.x *= f;
+            v.y *= f;
+        }
+        compact[i] = v;
+    }
+}
+
+// spec = the compact values on I_N, zero elsewhere (the whole half spectrum is written)
+template <int D>
+__global__ void unpack_spectrum_k(const double2* __restrict__ compact, int ng, int N, int64_t total,
+                                  double2* __restrict__ spec) {
+    const int nh = ng / 2 + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rem = i / nh;
+        const int kl = (int)(i % nh);
+        bool inside = kl <= N / 2;
+        int64_t didx = kl;
+        int64_t dstride = N / 2 + 1;
+#pragma unroll
+        for (int t = D - 2; t >= 0; --t) {
+            const int q = (int)(rem % ng);
+            rem /= ng;
+            const int k = q < ng / 2 ? q : q - ng;
+            inside = inside && (k >= -N / 2) && (k <= N / 2);
+            didx += (int64_t)(k + N / 2) * dstride;
+            dstride *= (N + 1);
+        }
+        spec[i] = inside ? compact[didx] : make_double2(0.0, 0.0);
+    }
+}
+
+// partial sums of sum_k D_k |G_k|^2 over the compact I_N values (weight 2 for k_last > 0:
+// the conjugate-symmetric half; k_last <= N/2 < n_g/2)
+__global__ void compact_energy_k(const double2* __restrict__ compact, const double* __restrict__ Dk, int N,
+                                 int64_t ndk, double* __restrict__ part) {
+    __shared__ double sm[256];
+    const int nh = N / 2 + 1;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ndk; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = compact[i];
+        acc += (i % nh == 0 ? 1.0 : 2.0) * Dk[i] * (v.x * v.x + v.y * v.y);
+    }
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+// the pruned transform's layout t2c [ky' = ky + H][kz][qx (n)] <-> D_k layout [kx + H][ky + H][kz]
+__global__ void pack_pruned_k(const double2* __restrict__ t2c, const double* __restrict__ Dk, int n, int N,
+                              double2* __restrict__ compact) {
+    const int H = N / 2;
+    const int64_t total = (int64_t)(N + 1) * (N + 1) * (H + 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(i % (H + 1));
+        const int64_t r = i / (H + 1);
+        const int jy = (int)(r % (N + 1));
+        const int jx = (int)(r / (N + 1));
+        const int kx = jx - H;
+        double2 v = t2c[((int64_t)jy * (H + 1) + kz) * n + (kx < 0 ? kx + n : kx)];
+        if (Dk) {
+            const double f = Dk[i];
+            v.x *= f;
+            v.y *= f;
+        }
+        compact[i] = v;
+    }
+}
+
+__global__ void unpack_pruned_k(const double2* __restrict__ compact, int n, int N, double2* __restrict__ t2c) {
+    const int H = N / 2;
+    const int64_t total = (int64_t)(2 * H + 1) * (H + 1) * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int qx = (int)(i % n);
+        const int64_t r = i / n;
+        const int kz = (int)(r % (H + 1));
+        const int jy = (int)(r / (H + 1));
+        const int kx = qx < n / 2 ? qx : qx - n;
+        t2c[i] = (kx < -H || kx > H) ? make_double2(0.0, 0.0)
+                                      : compact[((int64_t)(kx + H) * (N + 1) + jy) * (H + 1) + kz];
+    }
+}
+
+inline int64_t dk_elems(int d, int N) {
+    int64_t e = N / 2 + 1;
+    for (int t = 0; t < d - 1; ++t) e *= (N + 1);
+    return e;
+}
+
 template <int D, int M>
 void spread_dm(const PointSet& ps, const double* w, double* grid, const FastParams& fp, cudaStream_t s) {
     KBWindow win = make_window(fp.b, M);
@@ -301,7 +423,7 @@ static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cu
     return spare;
 }
 
-static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s);
+static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
 
 double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
@@ -317,19 +439,35 @@ double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s,
         }();
         const size_t need = (size_t)fp.box_w * fp.ng * (fp.ng / 2 + 1) + (size_t)fp.box_w * (fp.N / 2 + 1) * fp.ng +
                             (size_t)(fp.N + 1) * (fp.N / 2 + 1) * fp.ng;
-        if (pruned_env && fp.d == 3 && !comm && !(fp.flags & UOTK_FLAG_FFT) && need <= sp.spec_elems)
-            return fft_chain_pruned(sp, grid, spec, s);
+        if (pruned_env && fp.d == 3 && !(fp.flags & UOTK_FLAG_FFT) && need <= sp.spec_elems)
+            return fft_chain_pruned(sp, grid, spec, s, comm);
     }
     if (!sp.r2c) get_fft_plans(fp.d, fp.ng, &sp.r2c, &sp.c2r);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftSetStream(sp.c2r, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
     const int64_t total = (int64_t)sp.spec_elems;
-    if (fp.d == 1) scale_spectrum_k<1><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
-    else if (fp.d == 2) scale_spectrum_k<2><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
-    else scale_spectrum_k<3><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
-    UOTK_LAUNCHED();
-    if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
+    if (comm) {
+        // D_k . G on I_N packed, summed over ranks, unpacked (zero outside I_N)
+        const int64_t ndk = dk_elems(fp.d, fp.N);
+        DevBuf<double2> compact(ndk, s);
+        const int gb = (int)std::min<int64_t>(2368, (ndk + 255) / 256);
+        if (fp.d == 1) pack_spectrum_k<1><<<gb, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, ndk, compact.p);
+        else if (fp.d == 2) pack_spectrum_k<2><<<gb, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, ndk, compact.p);
+        else pack_spectrum_k<3><<<gb, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, ndk, compact.p);
+        UOTK_LAUNCHED();
+        comm_allreduce_spectrum(compact.p, ndk, comm, s);
+        const int gu = (int)std::min<int64_t>(2368, (total + 255) / 256);
+        if (fp.d == 1) unpack_spectrum_k<1><<<gu, 256, 0, s>>>(compact.p, fp.ng, fp.N, total, spec);
+        else if (fp.d == 2) unpack_spectrum_k<2><<<gu, 256, 0, s>>>(compact.p, fp.ng, fp.N, total, spec);
+        else unpack_spectrum_k<3><<<gu, 256, 0, s>>>(compact.p, fp.ng, fp.N, total, spec);
+        UOTK_LAUNCHED();
+    } else {
+        if (fp.d == 1) scale_spectrum_k<1><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
+        else if (fp.d == 2) scale_spectrum_k<2><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
+        else scale_spectrum_k<3><<<blocks_for(total, 256), 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total);
+        UOTK_LAUNCHED();
+    }
     UOTK_CUFFT(cufftExecZ2D(sp.c2r, (cufftDoubleComplex*)spec, grid));
     return grid;
 }
@@ -543,7 +681,17 @@ static void spectrum_energy_pruned(SpectralPlan& sp, double* grid, double2* spec
     UOTK_LAUNCHED();
     UOTK_CUFFT(cufftExecZ2Z(px, (cufftDoubleComplex*)t2c, (cufftDoubleComplex*)t2c, CUFFT_FORWARD));
     add_launches(3);
-    if (comm) comm_allreduce_spectrum(t2c, (size_t)(2 * H + 1) * (H + 1) * n, comm, s);
+    if (comm) {
+        // the ranks' G on I_N (D_k layout), summed, then the energy of the sum
+        const int64_t ndk = dk_elems(3, N);
+        DevBuf<double2> compact(ndk, s);
+        pack_pruned_k<<<(int)std::min<int64_t>(2368, (ndk + 255) / 256), 256, 0, s>>>(t2c, nullptr, n, N, compact.p);
+        UOTK_LAUNCHED();
+        comm_allreduce_spectrum(compact.p, ndk, comm, s);
+        compact_energy_k<<<nparts, 256, 0, s>>>(compact.p, sp.pd->Dk.p, N, ndk, part);
+        UOTK_LAUNCHED();
+        return;
+    }
     pruned_energy_k<<<nparts, 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N, part);
     UOTK_LAUNCHED();
 }
@@ -553,7 +701,7 @@ static void spectrum_energy_pruned(SpectralPlan& sp, double* grid, double2* spec
 // (kx, ky, kz), the inverse x-pass on the (N + 1)(N/2 + 1) kept rows, the inverse y-pass
 // on the w (N/2 + 1) rows of the box slab, the inverse z-pass (C2R) on its w n rows —
 // g' is produced on the box slab [o, o + w) x n x n of `grid` (all a gather reads).
-static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s) {
+static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
     const FastParams& fp = sp.fp;
     const int n = fp.ng, o = fp.box_lo, w = fp.box_w, N = fp.N, H = N / 2;
     cufftHandle pz, py, px, pzi;
@@ -573,8 +721,19 @@ static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, c
     prune_t2_k<<<dim3((w + 31) / 32, (2 * H + 1 + 31) / 32, H + 1), tb, 0, s>>>(t1c, n, H, w, o, t2c);
     UOTK_LAUNCHED();
     UOTK_CUFFT(cufftExecZ2Z(px, (cufftDoubleComplex*)t2c, (cufftDoubleComplex*)t2c, CUFFT_FORWARD));
-    prune_scale_k<<<296, 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N);
-    UOTK_LAUNCHED();
+    if (comm) {  // D_k . G on I_N packed, summed over ranks, unpacked
+        const int64_t ndk = dk_elems(3, N);
+        DevBuf<double2> compact(ndk, s);
+        pack_pruned_k<<<(int)std::min<int64_t>(2368, (ndk + 255) / 256), 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N,
+                                                                                      compact.p);
+        UOTK_LAUNCHED();
+        comm_allreduce_spectrum(compact.p, ndk, comm, s);
+        unpack_pruned_k<<<296, 256, 0, s>>>(compact.p, n, N, t2c);
+        UOTK_LAUNCHED();
+    } else {
+        prune_scale_k<<<296, 256, 0, s>>>(t2c, sp.pd->Dk.p, n, N);
+        UOTK_LAUNCHED();
+    }
     UOTK_CUFFT(cufftExecZ2Z(px, (cufftDoubleComplex*)t2c, (cufftDoubleComplex*)t2c, CUFFT_INVERSE));
     UOTK_CUDA(cudaMemsetAsync(t1c, 0, (size_t)w * (H + 1) * n * sizeof(double2), s));
     unprune_t2_k<<<dim3((w + 31) / 32, (2 * H + 1 + 31) / 32, H + 1), tb, 0, s>>>(t2c, n, H, w, o, t1c);
@@ -605,7 +764,20 @@ void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part
     if (!sp.r2c) get_fft_plans(fp.d, fp.ng, &sp.r2c, &sp.c2r);
     UOTK_CUFFT(cufftSetStream(sp.r2c, s));
     UOTK_CUFFT(cufftExecD2Z(sp.r2c, grid, (cufftDoubleComplex*)spec));
-    if (comm) comm_allreduce_spectrum(spec, sp.spec_elems, comm, s);
+    if (comm) {
+        // the ranks' G on I_N (D_k layout), summed, then the energy of the sum
+        const int64_t ndk = dk_elems(fp.d, fp.N);
+        DevBuf<double2> compact(ndk, s);
+        const int gb = (int)std::min<int64_t>(2368, (ndk + 255) / 256);
+        if (fp.d == 1) pack_spectrum_k<1><<<gb, 256, 0, s>>>(spec, nullptr, fp.ng, fp.N, ndk, compact.p);
+        else if (fp.d == 2) pack_spectrum_k<2><<<gb, 256, 0, s>>>(spec, nullptr, fp.ng, fp.N, ndk, compact.p);
+        else pack_spectrum_k<3><<<gb, 256, 0, s>>>(spec, nullptr, fp.ng, fp.N, ndk, compact.p);
+        UOTK_LAUNCHED();
+        comm_allreduce_spectrum(compact.p, ndk, comm, s);
+        compact_energy_k<<<nparts, 256, 0, s>>>(compact.p, sp.pd->Dk.p, fp.N, ndk, part);
+        UOTK_LAUNCHED();
+        return;
+    }
     const int64_t total = (int64_t)sp.spec_elems;
     if (fp.d == 1) spectrum_energy_k<1><<<nparts, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total, part);
     else if (fp.d == 2) spectrum_energy_k<2><<<nparts, 256, 0, s>>>(spec, sp.pd->Dk.p, fp.ng, fp.N, total, part);

@@ -258,11 +258,48 @@ __global__ void dk_kernel(double* Dk, const double2* bspec, const double* psi, i
     Dk[i] = fac * bspec[bidx].x * invN;
 }
 
-PlanData::~PlanData() {
-    // evicted tables may still be read by kernels queued on other streams
-    cudaDeviceSynchronize();
+cudaStream_t private_stream();  // context.cu
+
+void PlanData::note_use(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(use_mu);
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return;  // (never inside a capture: plans end with their call)
+    }
+    for (auto& u : uses)
+        if (u.first == s) {
+            cudaEventRecord(u.second, s);
+            cudaGetLastError();
+            return;
+        }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess && cudaEventRecord(e, s) == cudaSuccess)
+        uses.emplace_back(s, e);
+    else if (e)
+        cudaEventDestroy(e);
     cudaGetLastError();
-    if (ready) cudaEventDestroy(ready);
+}
+
+PlanData::~PlanData() {
+    // evicted tables may still be read by kernels queued on the streams that used them:
+    // wait for those uses only (not the whole device: unrelated streams, NCCL's included,
+    // keep running), then hand the buffers back on the library's own stream
+    for (auto& u : uses) {
+        cudaEventSynchronize(u.second);
+        cudaEventDestroy(u.second);
+    }
+    if (ready) {
+        cudaEventSynchronize(ready);
+        cudaEventDestroy(ready);
+    }
+    cudaGetLastError();
+    try {
+        cudaStream_t ps = private_stream();
+        Dk.s = ps;
+        Csep.s = ps;
+    } catch (...) {
+    }
 }
 
 namespace {
@@ -323,6 +360,7 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     // the full-grid cuFFT plans only where the full chain runs (fft_chain also creates them
     // on first use: the separable Gaussian chain and the pruned MMD^2 transform never do)
     if (!sp.pd->separable || (fp.flags & UOTK_FLAG_FFT)) get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
+    sp.use_stream = s;
     sp.grid_elems = 1;
     for (int t = 0; t < d; ++t) sp.grid_elems *= ng;
     sp.spec_elems = sp.grid_elems / ng * (ng / 2 + 1);

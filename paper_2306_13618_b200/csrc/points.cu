@@ -195,7 +195,8 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
     UOTK_CUDA(cudaStreamSynchronize(s));
     trace_mark("geometry: reductions + sync");
     if (h[2 * d] != 0) fail(UOTK_EDOMAIN, "non-finite point coordinate");
-    if (n1 + n2 == 0) return g;
+    // no point on any rank (a rank's own shard may be empty: the box is global)
+    if (!(h[0] <= h[d])) return g;
     for (int t = 0; t < d; ++t) g.center[t] = 0.5 * (h[t] + h[d + t]);
     g.rmax = std::sqrt(h[2 * d + 1]);
     return g;

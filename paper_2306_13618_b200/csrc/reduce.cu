@@ -71,6 +71,19 @@ __global__ void check_mass_k(const double* __restrict__ a, int64_t n, int* __res
     }
 }
 
+__global__ void check_finite_k(const double* __restrict__ a, int64_t n, int* __restrict__ flag, int bit) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && !isfinite(a[i])) atomicOr(flag, bit);
+}
+
+__global__ void split_bits_k(const int* __restrict__ flag, int32_t* __restrict__ bits) {
+    if (threadIdx.x < 4) bits[threadIdx.x] = (*flag >> threadIdx.x) & 1;
+}
+
+__global__ void join_bits_k(const int32_t* __restrict__ bits, int* __restrict__ flag) {
+    if (threadIdx.x == 0) *flag = bits[0] | (bits[1] << 1) | (bits[2] << 2) | (bits[3] << 3);
+}
+
 // w = mass * exp(lam * pot)
 __global__ void scaled_mass_k(const double* __restrict__ mass, const double* __restrict__ pot, int64_t n, double lam,
                               double* __restrict__ w) {
@@ -144,6 +157,22 @@ void uot_terms(const double* pot, const double* mass, const double* t, int64_t n
 void check_mass(const double* a, int64_t n, int* flag, cudaStream_t s) {
     if (n == 0) return;
     check_mass_k<<<blocks_for(n, 256), 256, 0, s>>>(a, n, flag);
+    UOTK_LAUNCHED();
+}
+
+void check_finite(const double* a, int64_t n, int* flag, int bit, cudaStream_t s) {
+    if (n == 0) return;
+    check_finite_k<<<blocks_for(n, 256), 256, 0, s>>>(a, n, flag, bit);
+    UOTK_LAUNCHED();
+}
+
+void split_bits(const int* flag, int32_t* bits, cudaStream_t s) {
+    split_bits_k<<<1, 32, 0, s>>>(flag, bits);
+    UOTK_LAUNCHED();
+}
+
+void join_bits(const int32_t* bits, int* flag, cudaStream_t s) {
+    join_bits_k<<<1, 32, 0, s>>>(bits, flag);
     UOTK_LAUNCHED();
 }
 

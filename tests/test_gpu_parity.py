@@ -103,10 +103,25 @@ def test_kernel_sum_c5_full_size_sampled(uk):
 
 
 # ------------------------------------------------------------------ UOT Sinkhorn
-def _uot_check(res, beta, gamma, ref, tol=1e-8):
+def _pot_err(got, ref, c):
+    """Element-wise potential error max_i |d_i| / (|ref_i| + c): a potential is
+    -c log t (3.3)/(3.4), so a relative error rho of the kernel sum t_i moves it by c rho;
+    c floors the denominator where a potential crosses zero."""
+    return float(np.max(np.abs(got - ref) / (np.abs(ref) + c))) if len(ref) else 0.0
+
+
+def _uot_check(res, beta, gamma, ref, eps, lam1, lam2=None, tol=1e-8):
+    """UOT parity: the paper's residual ||dbeta||/||beta|| + ||dgamma||/||gamma||,
+    every potential element by element (c1 = eta1/(1 + eta1/eps), c2 likewise: the scale
+    of (3.3)/(3.4)), and the objective values."""
+    lam2 = lam1 if lam2 is None else lam2
     resid = (np.linalg.norm(beta - ref.beta) / np.linalg.norm(ref.beta)
              + np.linalg.norm(gamma - ref.gamma) / np.linalg.norm(ref.gamma))
     assert resid <= tol, resid
+    c1 = lam1 / (1.0 + lam1 / eps)
+    c2 = lam2 / (1.0 + lam2 / eps)
+    eb, eg = _pot_err(beta, ref.beta, c1), _pot_err(gamma, ref.gamma, c2)
+    assert eb <= tol and eg <= tol, (eb, eg)
     assert abs(res.primal - ref.primal) <= tol * abs(ref.primal), (res.primal, ref.primal)
     assert abs(res.dual - ref.dual) <= tol * abs(ref.dual), (res.dual, ref.dual)
     assert abs(res.plan_mass - ref.plan_mass) <= tol * ref.plan_mass
@@ -122,7 +137,7 @@ def test_uot_c1_full(uk, method):
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
                                        iters=pr.iters, opts={"method": method})
     assert res.info["method"] == method
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
     assert abs(res.max_dbeta - ref.max_dbeta) <= 1e-6 * max(ref.max_dbeta, 1e-12) + 1e-14
 
 
@@ -133,7 +148,24 @@ def test_uot_c3_like_reduced(uk, method):
     ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
                                        iters=pr.iters, opts={"method": method})
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
+
+
+@pytest.mark.parametrize("n,m", [(6000, 5003), (300, 257)])
+def test_uot_c3_dense_reduced_ws_kernel(uk, n, m):
+    """The headline's warp-specialised half-step (sinkhorn3d_ws_k: one-cell groups, m = 8)
+    at reduced n against the oracle element by element: C3's parameters and per-cell
+    density (workloads.c3_dense_uot), ragged chunks (groups of up to ~1000 points cut into
+    32-point chunks with ragged tails), and a small case of ~9 chunks in 8 cells (most
+    CTAs idle, every chunk partial)."""
+    pr = W.c3_dense_uot(n=n, m=m, iters=10)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": "nfft"})
+    assert res.info["groups"] == (16, 16), res.info  # one-cell groups on both sets: sinkhorn3d_ws_k
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
+    assert abs(res.max_dbeta - ref.max_dbeta) <= 1e-6 * ref.max_dbeta
+    assert abs(res.max_dgamma - ref.max_dgamma) <= 1e-6 * ref.max_dgamma
 
 
 def test_uot_unequal_penalties_gamma_init_and_zero_iters(uk):
@@ -143,7 +175,7 @@ def test_uot_unequal_penalties_gamma_init_and_zero_iters(uk):
         ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, 0.7, 2.5, 12, gamma0=g0)
         beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, 0.7, lam2=2.5,
                                            iters=12, gamma_init=cuda(g0), opts={"method": method})
-        _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+        _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, 0.7, 2.5)
         ref0 = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, 1.0, 1.0, 0)
         beta, gamma, res = uk.uot_sinkhorn(pr.x, pr.a, pr.y, pr.b, pr.eps, 1.0, iters=0, opts={"method": method})
         assert np.all(gamma == 0) and np.all(beta == 0)
@@ -331,7 +363,7 @@ def test_uot_c4_like_reduced(uk, c4_reduced, flags, N):
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
                                        iters=pr.iters, opts={"method": "nfft", "flags": f, "N": N})
     assert res.info["n_grid"] == (4096 if N else 160)
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
 
 
 def test_uot_c1_chunked_nfft(uk):
@@ -340,7 +372,7 @@ def test_uot_c1_chunked_nfft(uk):
     ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, pr.iters)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
                                        iters=pr.iters, opts={"method": "nfft", "flags": uk.FLAG_CHUNKED})
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
 
 
 def test_uot_c4_full_size_sampled(uk):
@@ -358,6 +390,35 @@ def test_uot_c4_full_size_sampled(uk):
     tt = oracle.kernel_sum_direct(pr.x, pr.a * np.exp(lam * b), pr.y[idx], W.GAUSS, pr.eps)
     ref = -c2 * np.log(tt)
     assert np.max(np.abs(g[idx] - ref)) <= 1e-9 * np.max(np.abs(ref))
+    assert abs(res.mass_a - pr.a.sum()) <= 1e-12 * pr.a.sum()
+
+
+def test_uot_c4_full_size_grid4096_sampled(uk):
+    """C4 at full size with the config's literal "oversampled grid 4096^2" (opts.N = 2048,
+    reading R19; 134 MB grids, beyond L2): 3 iterations, then the last gamma-step identity
+    (3.4) at 24 sampled j and the last beta-step identity (3.3) at 24 sampled i, each
+    against the oracle with the returned potentials."""
+    pr = W.c4_uot(iters=3)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
+                                       iters=pr.iters, opts={"method": "nfft", "N": 2048})
+    assert res.info["n_grid"] == 4096 and res.info["groups"] == (16, 16), res.info
+    b = beta.cpu().numpy()
+    g = gamma.cpu().numpy()
+    lam = 1.0 / pr.eps
+    c = pr.lam / (1.0 + pr.lam * lam)
+    rng = np.random.default_rng(8)
+    jdx = rng.choice(len(pr.y), 24, replace=False)
+    tt = oracle.kernel_sum_direct(pr.x, pr.a * np.exp(lam * b), pr.y[jdx], W.GAUSS, pr.eps)
+    assert _pot_err(g[jdx], -c * np.log(tt), c) <= 1e-9
+    # the beta-step of the last iteration saw the gamma of the previous one; the marginal
+    # p_i = mu_i e^{lam beta_i} t_i (t from the final gamma) is the plan's row sum (P:488)
+    idx = rng.choice(len(pr.x), 24, replace=False)
+    t = oracle.kernel_sum_direct(pr.y, pr.b * np.exp(lam * g), pr.x[idx], W.GAUSS, pr.eps)
+    p_ref = pr.a[idx] * np.exp(lam * b[idx]) * t
+    _, _, r2 = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=pr.iters,
+                               opts={"method": "nfft", "N": 2048}, marginals=True)
+    p = r2.p.cpu().numpy()[idx]
+    assert np.max(np.abs(p - p_ref) / p_ref) <= 1e-8
     assert abs(res.mass_a - pr.a.sum()) <= 1e-12 * pr.a.sum()
 
 
@@ -389,7 +450,7 @@ def test_uot_d3_sparse_cloud(uk, flags):
     if flags == "chunked":
         opts["flags"] = uk.FLAG_CHUNKED
     beta, gamma, res = uk.uot_sinkhorn(cuda(x), cuda(a), cuda(y), cuda(b), 0.02, 0.5, iters=8, opts=opts)
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, 0.02, 0.5)
 
 
 def test_mmd2_c2_imq_chunked_vs_generic(uk):
@@ -449,9 +510,9 @@ def test_uot_small_graph_replay_on_user_stream(uk, method):
         with torch.cuda.stream(st):
             beta, gamma, res = uk.uot_sinkhorn(*args, iters=iters, opts={"method": method}, stream=st)
         st.synchronize()
-        _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+        _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
         beta2, gamma2, res2 = uk.uot_sinkhorn(*args, iters=iters, opts={"method": method})
-        _uot_check(res2, beta2.cpu().numpy(), gamma2.cpu().numpy(), ref)
+        _uot_check(res2, beta2.cpu().numpy(), gamma2.cpu().numpy(), ref, pr.eps, pr.lam)
 
 
 # ------------------------------------------------------------------ solver variants
@@ -479,7 +540,7 @@ def test_uot_gamma_init_cstar(uk, method):
     ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, 20, gamma0=np.full(500, c))
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=20,
                                        gamma_init="cstar", opts={"method": method})
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
 
 
 @pytest.mark.parametrize("method", ["direct", "nfft"])
@@ -494,7 +555,7 @@ def test_uot_stopping_rule(uk, method):
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=400,
                                        opts={"method": method, "stop_tol": 1e-9, "check_every": 5})
     assert res.iters == ref.iters
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
     assert res.max_dbeta <= 1e-9 and res.max_dgamma <= 1e-9
 
 
@@ -522,7 +583,7 @@ def test_uot_lambda_scaling(uk, method):
     beta, gamma, res = uk.uot_sinkhorn_scaling(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), eps_list, pr.lam,
                                                iters=15, opts={"method": method})
     assert res.iters == 45 == ref.iters
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, eps_list[-1], pr.lam)
 
 
 # ------------------------------------------------------------------ transport term and marginals (8(f) f4)
@@ -547,7 +608,7 @@ def test_uot_transport_and_marginals(uk, method, d):
     t_ref = oracle.transport_cost(pr.x, pr.a, pr.y, pr.b, ref.beta, ref.gamma, pr.eps)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=iters,
                                        opts={"method": method}, marginals=True, transport=True)
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
     assert rel_err(res.p.cpu().numpy(), p_ref, False) <= 1e-8
     assert rel_err(res.q.cpu().numpy(), q_ref, False) <= 1e-8
     assert abs(res.transport - t_ref) <= 1e-8 * abs(t_ref), (res.transport, t_ref)
@@ -568,7 +629,7 @@ def test_fft_chain_vs_separable_chain(uk, d):
     ref = oracle.uot_sinkhorn_direct(u.x, u.a, u.y, u.b, u.eps, u.lam, u.lam, iters)
     beta, gamma, res = uk.uot_sinkhorn(cuda(u.x), cuda(u.a), cuda(u.y), cuda(u.b), u.eps, u.lam, iters=iters,
                                        opts={"method": "nfft", "flags": uk.FLAG_FFT})
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, u.eps, u.lam)
 
 
 @pytest.mark.parametrize("method", ["direct", "nfft"])
@@ -579,7 +640,7 @@ def test_uot_d1(uk, method):
     ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, 30)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=30,
                                        opts={"method": method})
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
 
 
 # ------------------------------------------------------------------ d = 3, m = 6 cell-group kernels
@@ -615,7 +676,7 @@ def test_uot_c3_like_reduced_m6(uk, flags):
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
                                        iters=pr.iters, opts=dict(M6, method="nfft", flags=f))
     assert res.info["m"] == 6
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
 
 
 def test_uot_c3_full_size_sampled_m6(uk):
@@ -679,7 +740,7 @@ def test_kernel_sum_m6_tiny_and_ragged(uk, n):
     ref2 = oracle.uot_sinkhorn_direct(pr2.x, pr2.a, pr2.y, pr2.b, pr2.eps, pr2.lam, pr2.lam, pr2.iters)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr2.x), cuda(pr2.a), cuda(pr2.y), cuda(pr2.b), pr2.eps, pr2.lam,
                                        iters=pr2.iters, opts=dict(M6, method="nfft", flags=uk.FLAG_CHUNKED))
-    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref2)
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref2, pr2.eps, pr2.lam)
 
 
 def test_error_paths_overflow_and_nonfinite(uk):

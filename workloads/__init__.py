@@ -136,6 +136,24 @@ def c3_uot(n=1_000_000, m=None, seed=0, iters=200):
     return UOTProblem("C3", x, a, y, b, eps=0.02, lam=0.5, iters=iters)
 
 
+def c3_dense_uot(n=6000, m=None, seed=0, iters=10):
+    """C3's parameters (d=3, eps=0.02, lam=0.5, masses U(0.1,1.0)) and C3's per-cell
+    density at reduced n: the mixture geometry of ``c3_uot`` shrunk by s = (n/1e6)^(1/3)
+    (means in the ball of radius 0.12 s, sigma 0.025 s, clip 0.2 s), so the points fill
+    the grid cells as densely as at 1M and the NFFT path forms one-cell groups — the
+    layout the headline's warp-specialised half-step runs on (tests only)."""
+    m = n if m is None else m
+    s = (max(n, m) / 1e6) ** (1.0 / 3.0)
+    rng = np.random.default_rng(seed)
+    mx = uniform_ball(rng, 8, 3, 0.12 * s)
+    my = uniform_ball(rng, 8, 3, 0.12 * s)
+    x = gaussian_mixture(rng, n, mx, 0.025 * s, clip=0.2 * s)
+    y = gaussian_mixture(rng, m, my, 0.025 * s, clip=0.2 * s)
+    a = rng.uniform(0.1, 1.0, n)
+    b = rng.uniform(0.1, 1.0, m)
+    return UOTProblem("C3-dense", x, a, y, b, eps=0.02, lam=0.5, iters=iters, meta={"shrink": s})
+
+
 def c4_uot(n=16_000_000, m=None, seed=0, iters=50):
     """C4: UOT d=2, n=m=16M uniform ball R=0.2, eps=0.002, lam=2.0, 50 iterations;
     masses a~U(0.5,1.5), b~U(0.2,2.0) (reading R16)."""
