@@ -91,13 +91,15 @@ def primal_of_plan(pi, d2, mu, nu, lam, eta1, eta2):
             + eta1 * kl(pi.sum(axis=1), mu) + eta2 * kl(pi.sum(axis=0), nu))
 
 
-def brute_force_uot(x, mu, y, nu, eps, eta1, eta2):
-    """Minimise the primal (2.9)/ over all plans pi in R_+^{n x m} with a
-    generic quasi-Newton optimiser on log pi.  Tiny n, m only."""
+def brute_force_uot(x, mu, y, nu, eps, eta1, eta2, r=2):
+    """Minimise the primal (2.9)/(P:462) with cost d^r over all plans pi in R_+^{n x m}
+    with a generic quasi-Newton optimiser on log pi.  Tiny n, m only."""
     lam = 1.0 / eps
     x = np.asarray(x, dtype=np.float64).reshape(len(mu), -1)
     y = np.asarray(y, dtype=np.float64).reshape(len(nu), -1)
     d2 = np.sum((x[:, None, :] - y[None, :, :]) ** 2, axis=2)
+    if r == 1:
+        d2 = np.sqrt(d2)  # the cost matrix d^r (named d2 below)
     n, m = d2.shape
 
     def f(z):
@@ -127,3 +129,55 @@ def balanced_sinkhorn(x, a, y, b, eps, iters):
         u = a / (K @ v)
         v = b / (K.T @ u)
     return u[:, None] * K * v[None, :]
+
+
+# ---------------------------------------------------------------- Laplace / energy kernels (NEXT-f2)
+def laplace_segment_integral(L, ell):
+    """int_{-L}^{L} exp(-|y|/l) dy = 2 l (1 - e^{-L/l})."""
+    return 2.0 * ell * (1.0 - math.exp(-L / ell))
+
+
+def laplace_disk_integral(R, ell):
+    """int_{|y| <= R} exp(-|y|/l) dy over the disk in R^2 = 2 pi l^2 (1 - e^{-R/l}(1 + R/l))."""
+    u = R / ell
+    return 2.0 * math.pi * ell ** 2 * (1.0 - math.exp(-u) * (1.0 + u))
+
+
+def laplace_ball_integral(R, ell):
+    """int_{|y| <= R} exp(-|y|/l) dy over the ball in R^3 = 4 pi l^3 (2 - e^{-R/l}(u^2 + 2u + 2)), u = R/l."""
+    u = R / ell
+    return 4.0 * math.pi * ell ** 3 * (2.0 - math.exp(-u) * (u * u + 2.0 * u + 2.0))
+
+
+def energy_segment_integral(L, x):
+    """int_{-L}^{L} -|x - y| dy = -(L^2 + x^2) for |x| <= L."""
+    return -(L * L + x * x)
+
+
+def polar_rule(R, nr, nt):
+    """Product quadrature on the disk of radius R: Gauss-Legendre in r on [0, R] (weight r),
+    the trapezoidal rule in the angle (exact for trigonometric polynomials)."""
+    t, w = np.polynomial.legendre.leggauss(nr)
+    r = 0.5 * R * (t + 1.0)
+    wr = 0.5 * R * w * r
+    th = 2.0 * math.pi * np.arange(nt) / nt
+    pts = np.stack([np.outer(r, np.cos(th)).ravel(), np.outer(r, np.sin(th)).ravel()], axis=1)
+    wts = np.outer(wr, np.full(nt, 2.0 * math.pi / nt)).ravel()
+    return pts, wts
+
+
+def spherical_rule(R, nr, nc, nphi):
+    """Product quadrature on the ball of radius R: Gauss-Legendre in r (weight r^2) and in
+    cos(theta), the trapezoidal rule in phi."""
+    t, w = np.polynomial.legendre.leggauss(nr)
+    r = 0.5 * R * (t + 1.0)
+    wr = 0.5 * R * w * r * r
+    c, wc = np.polynomial.legendre.leggauss(nc)
+    s = np.sqrt(1.0 - c * c)
+    ph = 2.0 * math.pi * np.arange(nphi) / nphi
+    R_, C_, P_ = np.meshgrid(r, c, ph, indexing="ij")
+    S_ = np.sqrt(1.0 - C_ * C_)
+    pts = np.stack([(R_ * S_ * np.cos(P_)).ravel(), (R_ * S_ * np.sin(P_)).ravel(), (R_ * C_).ravel()], axis=1)
+    W = np.einsum("i,j,k->ijk", wr, wc, np.full(nphi, 2.0 * math.pi / nphi)).ravel()
+    del s
+    return pts, W
