@@ -69,9 +69,15 @@ enum {
 };
 
 /* Radial kernels of Eq. (4.2), P:560 (Table 1), as functions of r = ||x - y||:
- *   UOTK_GAUSS: k(r) = exp(-r^2 / param)          (param = l^2 = eps in the configs' form)
- *   UOTK_IMQ:   k(r) = 1 / sqrt(r^2 + param^2)    (param = c)                            */
-typedef enum { UOTK_GAUSS = 0, UOTK_IMQ = 1, UOTK_GAUSS_R2 = 2 } uotk_kernel_kind;
+ *   UOTK_GAUSS:  k(r) = exp(-r^2 / param)          (param = l^2 = eps in the configs' form)
+ *   UOTK_IMQ:    k(r) = 1 / sqrt(r^2 + param^2)    (param = c)
+ *   UOTK_LAP:    k(r) = exp(-r / param)            (param = l; Laplace kernel K^Lap)
+ *   UOTK_ENERGY: k(r) = -r                         (Table 1's energy kernel k^e = -K^abs;
+ *                                                   param is ignored, pass any value > 0)
+ * LAP and ENERGY are not smooth at r = 0: their NFFT path regularises the kernel inside
+ * ||y|| < eps_I (torus units, eps_I = p/N) and adds the exact near-field correction
+ * sum_{||x_i - y_j|| < eps_I h} (k - K_R)(x_i - y_j) alpha_j (reading R24). */
+typedef enum { UOTK_GAUSS = 0, UOTK_IMQ = 1, UOTK_GAUSS_R2 = 2, UOTK_LAP = 3, UOTK_ENERGY = 4 } uotk_kernel_kind;
 /*   UOTK_GAUSS_R2: k(r) = r^2 exp(-r^2 / param)  (kernel sums only: the transport-cost
  *                  kernel of the Gibbs plan, d^2 k_ij, giving <pi, d^2> of P:462)    */
 
@@ -95,7 +101,11 @@ typedef struct {
     double h;         /* torus scaling h (Eq. 4.7, Rem. 4.3 P:610); 0 = auto        */
     double tol;       /* target truncation tolerance of the auto rules; 0 = 1e-16        */
     int32_t flags;    /* UOTK_FLAG_* bits below; 0 = automatic                           */
-    int32_t reserved; /* must be 0                                                       */
+    int32_t deterministic; /* 1 = bitwise reproducible results (run to run, any launch
+                         configuration): every spread pulls each grid value in the points'
+                         sorted order instead of accumulating with fp64 atomics, and the
+                         fused half-steps run as gather + spread; slower.
+                         0 = default (atomics; results reproducible to ~1e-15)            */
     /* Sinkhorn stopping rule (reading R20 of DESIGN.md; the paper's "while stopping
      * criteria"): with stop_tol > 0, after every check_every-th iteration the
      * loop ends once the sup-norm changes of beta and gamma within that iteration are
@@ -114,7 +124,11 @@ typedef struct {
 #define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m = 8; d = 3: or 6) */
 #define UOTK_FLAG_TRANSPORT 4 /* uot: also evaluate the transport term <pi, d^2>    */
 #define UOTK_FLAG_FFT 8       /* always the cuFFT chain (D2Z, D_k, Z2D), never the separable
-                                 circulant GEMMs of the Gaussian (which run on one rank only) */
+                                 circulant GEMMs of the Gaussian (with a communicator their
+                                 first pass's box is the all-reduced quantity)             */
+#define UOTK_FLAG_COST_R1 16  /* uot: cost d^1 instead of d^2, i.e. the Laplace Gibbs kernel
+                                 exp(-||x - y|| / eps) (Algorithm 2's r = 1);
+                                 not combinable with UOTK_FLAG_TRANSPORT                     */
 
 /* What a call actually used (any pointer to it may be NULL). */
 typedef struct {

@@ -23,12 +23,15 @@ from ._native import UotkError, UotkOpts, UotkInfo, UotkUotResult  # noqa: F401
 GAUSS = 0
 IMQ = 1
 GAUSS_R2 = 2  # k(r) = r^2 exp(-r^2/param): kernel sums only (transport-cost kernel)
+LAP = 3       # k(r) = exp(-r/param)
+ENERGY = 4    # k(r) = -r (Table 1's energy kernel; param ignored)
 AUTO, NFFT, DIRECT = 0, 1, 2
 FLAG_GENERIC, FLAG_CHUNKED = 1, 2  # opts["flags"]: kernel family of the NFFT passes (uotk.h)
-_KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, "gauss_r2": GAUSS_R2, GAUSS: GAUSS, IMQ: IMQ,
-         GAUSS_R2: GAUSS_R2}
+_KIND = {"gauss": GAUSS, "gaussian": GAUSS, "imq": IMQ, "gauss_r2": GAUSS_R2, "laplace": LAP, "lap": LAP,
+         "energy": ENERGY, GAUSS: GAUSS, IMQ: IMQ, GAUSS_R2: GAUSS_R2, LAP: LAP, ENERGY: ENERGY}
 FLAG_TRANSPORT = 4
 FLAG_FFT = 8  # always the cuFFT spectral chain (the multi-rank path), never the separable GEMMs
+FLAG_COST_R1 = 16  # uot: cost d^1, the Laplace Gibbs kernel exp(-|x-y|/eps) (Algorithm 2, r = 1)
 _METHOD = {"auto": AUTO, "nfft": NFFT, "direct": DIRECT, AUTO: AUTO, NFFT: NFFT, DIRECT: DIRECT}
 
 __all__ = ["kernel_sum", "uot_sinkhorn", "uot_sinkhorn_scaling", "mmd2", "uot_cstar", "sinkhorn_divergence", "release_caches", "Comm", "UOTResult", "GAUSS",

@@ -32,7 +32,7 @@ class UotkOpts(ctypes.Structure):
         ("method", ctypes.c_int32), ("N", ctypes.c_int32), ("sigma", ctypes.c_double),
         ("m", ctypes.c_int32), ("p", ctypes.c_int32), ("eps_B", ctypes.c_double),
         ("h", ctypes.c_double), ("tol", ctypes.c_double), ("flags", ctypes.c_int32),
-        ("reserved", ctypes.c_int32), ("stop_tol", ctypes.c_double), ("check_every", ctypes.c_int32),
+        ("deterministic", ctypes.c_int32), ("stop_tol", ctypes.c_double), ("check_every", ctypes.c_int32),
         ("reserved2", ctypes.c_int32),
     ]
 

@@ -24,9 +24,13 @@ void comm_create_loopback(int nranks, void** out);
 void comm_abort(void* comm, const std::string& why);
 void ensure_pool();
 cudaStream_t private_stream();  // context.cu
+int64_t guard_violations();     // context.cu (UOTK_GUARD=1)
 
 void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
                      void* comm);  // nfft.cu
+
+void apply_sinkhorn_update(const double* t, int64_t n, const EpiSinkhorn& epi, unsigned long long* dmax,
+                           cudaStream_t s);  // nearfield.cu
 
 // Fused NFFT half-step on chunked point sets (fused12d.cu / fused3d.cu).
 bool chunked_available(const FastParams& fp);
@@ -41,8 +45,17 @@ namespace {
 // Sinkhorn iteration replayed from a graph ~35 us at C1's size).
 constexpr double kDirectCrossoverPairs = 4.0e7;  // Sinkhorn
 double direct_crossover_sum(int d, int kind) {   // one kernel sum / MMD^2
+    if (kind == UOTK_LAP || kind == UOTK_ENERGY) return d < 3 ? 1.0e9 : 4.0e9;  // N = 256 grids + near field
     if (d < 3) return 1.5e8;
     return kind == UOTK_IMQ ? 8.0e8 : 4.0e8;
+}
+
+bool nonsmooth(int kind) { return kind == UOTK_LAP || kind == UOTK_ENERGY; }
+
+// the near-field correction needs every partner of a target within eps_I: one rank only
+void check_nearfield_ranks(int kind, const uotk_opts& o, void* comm) {
+    if (nonsmooth(kind) && o.method != UOTK_DIRECT && comm_nranks(comm) > 1)
+        fail(UOTK_EUNSUPPORTED, "Laplace / energy kernels (near-field correction) with a multi-rank communicator");
 }
 
 // Runs f, mapping exceptions to status codes.  With a communicator the thread's resource
@@ -51,8 +64,11 @@ double direct_crossover_sum(int d, int kind) {   // one kernel sum / MMD^2
 template <class F>
 int guarded(F&& f, void* comm = nullptr) {
     SlotScope slot(comm);
+    const int64_t guard0 = guard_violations();
     try {
         f();
+        if (guard_violations() != guard0)
+            fail(UOTK_ECUDA, "UOTK_GUARD: a kernel wrote outside a library buffer (see stderr)");
         return UOTK_OK;
     } catch (const Error& e) {
         g_last_error = e.msg;
@@ -73,9 +89,12 @@ uotk_opts resolve(const uotk_opts* o) {
     uotk_opts r;
     memset(&r, 0, sizeof r);
     if (o) r = *o;
-    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED | UOTK_FLAG_TRANSPORT | UOTK_FLAG_FFT)) != 0 ||
-        r.reserved != 0)
-        fail(UOTK_EINVAL, "unknown opts.flags bits, or opts.reserved != 0");
+    if ((r.flags & ~(UOTK_FLAG_GENERIC | UOTK_FLAG_CHUNKED | UOTK_FLAG_TRANSPORT | UOTK_FLAG_FFT |
+                     UOTK_FLAG_COST_R1)) != 0)
+        fail(UOTK_EINVAL, "unknown opts.flags bits");
+    if (r.deterministic != 0 && r.deterministic != 1) fail(UOTK_EINVAL, "opts.deterministic must be 0 or 1");
+    if ((r.flags & UOTK_FLAG_COST_R1) && (r.flags & UOTK_FLAG_TRANSPORT))
+        fail(UOTK_EUNSUPPORTED, "UOTK_FLAG_TRANSPORT with the r = 1 cost");
     if ((r.flags & UOTK_FLAG_GENERIC) && (r.flags & UOTK_FLAG_CHUNKED))
         fail(UOTK_EINVAL, "opts.flags: UOTK_FLAG_GENERIC and UOTK_FLAG_CHUNKED are exclusive");
     if (r.method < 0 || r.method > 2) fail(UOTK_EINVAL, "opts.method must be AUTO, NFFT or DIRECT");
@@ -246,13 +265,14 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
                             const double* tgt, int kind, double param, double* out, const uotk_opts* opts_in,
                             uotk_info* info, void* comm, cudaStream_t s) {
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
-    need(kind == UOTK_GAUSS || kind == UOTK_IMQ || kind == UOTK_GAUSS_R2, "unknown kernel kind");
+    need(kind >= UOTK_GAUSS && kind <= UOTK_ENERGY, "unknown kernel kind");
     need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");
     check_points_arg(d, n_src, src, "src");
     check_points_arg(d, n_src, alpha, "alpha");
     check_points_arg(d, n_tgt, tgt, "tgt");
     check_points_arg(d, n_tgt, out, "out");
     const uotk_opts o = resolve(opts_in);
+    check_nearfield_ranks(kind, o, comm);
     ensure_pool();
     InArr S, A, T;
     S.bind(src, (size_t)n_src * d, s);
@@ -289,6 +309,12 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         spread(PS, w.p, grid.p, ns.fp, s);
         const double* gp = fft_chain(ns.sp, grid.p, spec.p, s, comm);
         gather_epi(PT, gp, ns.fp, EpiStore{O.d, PT.perm.p}, nullptr, s);
+        if (nearfield_needed(ns.fp)) {  // + sum over close pairs of (K - K_R) alpha
+            NearField NS, NT;
+            build_nearfield(NS, PS, ns.fp, s);
+            build_nearfield(NT, PT, ns.fp, s);
+            nearfield_apply(NS, w.p, NT, ns.fp, PT.perm.p, O.d, s);
+        }
         trace_mark("passes enqueued");
     }
     O.flush();
@@ -327,6 +353,9 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
     if (q_out) QO.bind(q_out, (size_t)m, s);
     const bool want_transport = (o.flags & UOTK_FLAG_TRANSPORT) != 0;
 
+    // the Gibbs kernel exp(-lambda d^r): Gaussian (r = 2) or Laplace with l = eps (r = 1)
+    const int gk = (o.flags & UOTK_FLAG_COST_R1) ? UOTK_LAP : UOTK_GAUSS;
+    check_nearfield_ranks(gk, o, comm);
     const double lam = 1.0 / eps;                 // paper lambda (Def. 2.7)
     const double c1 = lam1 / (1.0 + lam1 * lam);  // (3.3): beta = -c1 log t
     const double c2 = lam2 / (1.0 + lam2 * lam);  // (3.4): gamma = -c2 log t~
@@ -360,7 +389,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         if (gamma_init) UOTK_CUDA(cudaMemcpyAsync(pot_y.p, G0.d, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
         else pot_y.zero();
     } else {
-        setup_nfft(ns, d, UOTK_GAUSS, eps, X.d, n, Y.d, m, o, comm, s);
+        setup_nfft(ns, d, gk, eps, X.d, n, Y.d, m, o, comm, s);
         fpv = ns.fp;
         fpp = &fpv;
         make_pointset(PX, X.d, n, ns.fp, s);
@@ -395,28 +424,51 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         auto iterate = [&](int it) {
             const bool last = records(it);
             if (last) dmax.zero();
-            direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, ex, last ? dmax.p : nullptr, s);  // (3.3)
+            direct_sum_epi(d, m, Y.d, wy.p, n, X.d, gk, eps, ex, last ? dmax.p : nullptr, s);  // (3.3)
             EpiSinkhorn e2 = ey;
             if (last) e2.t_store = ty.p;
-            direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
+            direct_sum_epi(d, n, X.d, wx.p, m, Y.d, gk, eps, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
         };
         done = run_iterations(iters, iterate, use_graph, s, stop_rule ? o.check_every : 0, o.stop_tol, dmax.p, comm);
         // marginals of the recovered plan: t at x from the final gamma
-        direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS, eps, EpiStore{tx.p, nullptr}, nullptr, s);
+        direct_sum_epi(d, m, Y.d, wy.p, n, X.d, gk, eps, EpiStore{tx.p, nullptr}, nullptr, s);
         // <pi, d^2>: t' at x with the kernel d^2 k (UOTK_GAUSS_R2) against the same weights
         if (want_transport) direct_sum_epi(d, m, Y.d, wy.p, n, X.d, UOTK_GAUSS_R2, eps, EpiStore{tpx.p, nullptr},
                                            nullptr, s);
         if (iters == 0) {
             scaled_mass(mass_x.p, pot_x.p, n, lam, wx.p, s);
-            direct_sum_epi(d, n, X.d, wx.p, m, Y.d, UOTK_GAUSS, eps, EpiStore{ty.p, nullptr}, nullptr, s);
+            direct_sum_epi(d, n, X.d, wx.p, m, Y.d, gk, eps, EpiStore{ty.p, nullptr}, nullptr, s);
         }
     } else {
         const FastParams& fp = ns.fp;
         const size_t ge = grid_elems(fp);
         DevBuf<double> grid(ge, s), grid2;
         DevBuf<double2> spec(ns.sp.spec_elems, s);
-        const bool fused = chunked_available(fp) && PX.chunked && PY.chunked;
+        // the fused half-steps flush their spread with fp64 atomics: deterministic mode (and
+        // the near-field corrected r = 1 kernel) runs gather, update and spread separately
+        const bool nf = nearfield_needed(fp);  // r = 1: Laplace Gibbs kernel, near-field corrected
+        const bool fused = chunked_available(fp) && PX.chunked && PY.chunked && !fp.deterministic && !nf;
         if (fused) grid2.alloc(ge, s);
+        NearField NX, NY;
+        DevBuf<double> tbx, tby;  // kernel sums in sorted order (gather + near field)
+        if (nf) {
+            build_nearfield(NX, PX, fp, s);
+            build_nearfield(NY, PY, fp, s);
+            tbx.alloc(n, s);
+            tby.alloc(m, s);
+        }
+        // t at the points of P (sorted order) from the grid g' (and, r = 1, the near field
+        // of the other set Q's weights wq), then the epilogue
+        auto half_step = [&](const PointSet& P, const NearField& NP, const NearField& NQ, const double* wq,
+                             double* tb, int64_t np, const double* g, const EpiSinkhorn& e, unsigned long long* dm) {
+            if (!nf) {
+                gather_epi(P, g, fp, e, dm, s);
+                return;
+            }
+            gather_epi(P, g, fp, EpiStore{tb, nullptr}, nullptr, s);
+            nearfield_apply(NQ, wq, NP, fp, nullptr, tb, s);
+            apply_sinkhorn_update(tb, np, e, dm, s);
+        };
         grid.zero();
         spread(PY, wy.p, grid.p, fp, s);  // adjoint NFFT of nu (.) v at y
         auto iterate = [&](int it) {
@@ -434,11 +486,11 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                 chunked_gather_spread(PY, g2, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
             } else {
                 const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
-                gather_epi(PX, g1, fp, ex, last ? dmax.p : nullptr, s);  // (3.3)
+                half_step(PX, NX, NY, wy.p, tbx.p, n, g1, ex, last ? dmax.p : nullptr);  // (3.3)
                 grid.zero();
                 spread(PX, wx.p, grid.p, fp, s);
                 const double* g2 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
-                gather_epi(PY, g2, fp, e2, last ? dmax.p + 1 : nullptr, s);  // (3.4)
+                half_step(PY, NY, NX, wx.p, tby.p, m, g2, e2, last ? dmax.p + 1 : nullptr);  // (3.4)
                 grid.zero();
                 spread(PY, wy.p, grid.p, fp, s);
             }
@@ -458,12 +510,14 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         }
         const double* gx = fft_chain(ns.sp, grid.p, spec.p, s, comm);
         gather_epi(PX, gx, fp, EpiStore{tx.p, nullptr}, nullptr, s);
+        if (nf) nearfield_apply(NY, wy.p, NX, fp, nullptr, tx.p, s);
         if (iters == 0) {
             scaled_mass(mass_x.p, pot_x.p, n, lam, wx.p, s);
             grid.zero();
             spread(PX, wx.p, grid.p, fp, s);
             const double* gy = fft_chain(ns.sp, grid.p, spec.p, s, comm);
             gather_epi(PY, gy, fp, EpiStore{ty.p, nullptr}, nullptr, s);
+            if (nf) nearfield_apply(NX, wx.p, NY, fp, nullptr, ty.p, s);
         }
     }
 
@@ -647,7 +701,7 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
                       const double* b, int kind, double param, double* mmd2, const uotk_opts* opts_in, uotk_info* info,
                       void* comm, cudaStream_t s) {
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
-    need(kind == UOTK_GAUSS || kind == UOTK_IMQ, "unknown kernel kind");
+    need(kind == UOTK_GAUSS || kind == UOTK_IMQ || kind == UOTK_LAP || kind == UOTK_ENERGY, "unknown kernel kind");
     need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");
     need(mmd2 != nullptr, "mmd2 output pointer is null");
     check_points_arg(d, n, x, "x");
@@ -655,6 +709,7 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     check_points_arg(d, m, y, "y");
     check_points_arg(d, m, b, "b");
     const uotk_opts o = resolve(opts_in);
+    check_nearfield_ranks(kind, o, comm);
     ensure_pool();
     InArr X, A, Y, B;
     X.bind(x, (size_t)n * d, s);
@@ -698,6 +753,22 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
         spread(PZ, ws.p, grid.p, ns.fp, s);
         spectrum_energy(ns.sp, grid.p, spec.p, part.p, kParts, s, comm);
         sum_columns(part.p, kParts, 1, sum.p, s);
+        if (nearfield_needed(ns.fp)) {
+            // + sum_i w_i sum_{close j} (K - K_R)(z_i - z_j) w_j
+            NearField NZ;
+            build_nearfield(NZ, PZ, ns.fp, s);
+            DevBuf<double> corr(nz, s), sum2(1, s);
+            corr.zero();
+            nearfield_apply(NZ, ws.p, NZ, ns.fp, nullptr, corr.p, s);
+            multiply(ws.p, corr.p, nz, prod.p, s);
+            sum_columns(prod.p, nz, 1, sum2.p, s);
+            double h2[2];
+            UOTK_CUDA(cudaMemcpyAsync(h2, sum.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+            UOTK_CUDA(cudaMemcpyAsync(h2 + 1, sum2.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+            UOTK_CUDA(cudaStreamSynchronize(s));
+            *mmd2 = h2[0] + h2[1];
+            return;
+        }
     }
     UOTK_CUDA(cudaMemcpyAsync(mmd2, sum.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     UOTK_CUDA(cudaStreamSynchronize(s));

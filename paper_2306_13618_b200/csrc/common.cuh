@@ -115,8 +115,13 @@ struct FastParams {
     double center[kMaxD] = {0, 0, 0};
     double eps_B = 0;      // IMQ boundary band
     int p = 0;             // IMQ boundary order
-    std::vector<double> poly;  // IMQ boundary polynomial in t = (r - r0)/eps_B (torus units), ascending
+    std::vector<double> poly;  // boundary polynomial K_B in t = (r - r0)/eps_B (torus units), ascending
+    // interior regularisation (Laplace, energy; reading R24): K_R = Q(r^2) on r < eps_I,
+    // Q in powers of (r^2 - eps_I^2), torus units; the near-field correction adds K - K_R there
+    double eps_I = 0;
+    std::vector<double> poly_I;
     int flags = 0;         // uotk_opts.flags (kernel family policy)
+    bool deterministic = false;  // uotk_opts.deterministic: spreads by the pull kernel (determ.cu)
     // grid box [box_lo, box_lo + box_w)^d holding every window footprint of the points
     // (both sets): the spread writes only inside it and the gathers read only inside it
     int box_lo = 0, box_w = 0;
@@ -142,6 +147,21 @@ struct PointSet {
     int chunk_kz = 16;        // d = 3: z extent of a group footprint (16 one cell, 24 z-segment)
     double chunk_fill = 0;    // mean occupied fraction of the 32 chunk slots
 };
+
+// Coarse buckets of a point set for the near-field correction (nearfield.cu): the set
+// re-sorted by a coarse key (cells of B >= eps_I n_g grid cells per axis, nc per axis)
+struct NearField {
+    int64_t n = 0;
+    int B = 1, nc = 1;
+    DevBuf<int32_t> perm;   // coarse order -> PointSet order
+    DevBuf<int32_t> key;    // coarse key (sorted)
+    DevBuf<int32_t> start;  // nc^d + 1: first point of each coarse cell
+    DevBuf<double> u;       // d x n grid coordinates in coarse order
+};
+bool nearfield_needed(const FastParams& fp);
+void build_nearfield(NearField& nf, const PointSet& ps, const FastParams& fp, cudaStream_t s);
+void nearfield_apply(const NearField& src, const double* w, const NearField& tgt, const FastParams& fp,
+                     const int32_t* map, double* out, cudaStream_t s);
 
 // Kernel-dependent Fourier-side tables, cached across calls (nfft_plan.cu) by the
 // parameters they depend on; `ready` marks the end of their construction on the stream

@@ -1,5 +1,6 @@
 // Library context: errors, stream-ordered buffers, host/device staging, cuFFT plan cache.
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <map>
@@ -108,6 +109,46 @@ bool capturing(cudaStream_t s) {
 
 size_t round_bytes(size_t b) { return (b + 4095) & ~size_t(4095); }
 
+// ---- guard mode (UOTK_GUARD=1; the memcheck substitute of DESIGN.md §12): every device
+// buffer gets kGuard bytes of a fixed pattern before and after it; when the buffer is
+// freed the stream is synchronised and both bands are checked.  A kernel writing out of
+// bounds into any library buffer is reported (stderr + the next API call fails).
+constexpr size_t kGuard = 64 * 1024;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_mode() {
+    static const bool on = [] {
+        const char* e = getenv("UOTK_GUARD");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+std::atomic<int64_t> g_guard_violations{0};
+
+void* guard_alloc(size_t bytes, cudaStream_t s) {
+    char* base = nullptr;
+    UOTK_CUDA(cudaMallocAsync((void**)&base, bytes + 2 * kGuard, s));
+    UOTK_CUDA(cudaMemsetAsync(base, kGuardByte, kGuard, s));
+    UOTK_CUDA(cudaMemsetAsync(base + kGuard + bytes, kGuardByte, kGuard, s));
+    return base + kGuard;
+}
+
+void guard_free(void* p, size_t bytes, cudaStream_t s) {
+    char* base = static_cast<char*>(p) - kGuard;
+    std::vector<unsigned char> h(2 * kGuard);
+    if (cudaMemcpyAsync(h.data(), base, kGuard, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+        cudaMemcpyAsync(h.data() + kGuard, base + kGuard + bytes, kGuard, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+        cudaStreamSynchronize(s) == cudaSuccess) {
+        size_t bad = 0;
+        for (unsigned char c : h) bad += c != kGuardByte;
+        if (bad) {
+            fprintf(stderr, "[uotk] GUARD VIOLATION: %zu bytes overwritten around a %zu-byte buffer\n", bad, bytes);
+            ++g_guard_violations;
+        }
+    }
+    cudaGetLastError();
+    cudaFreeAsync(base, s);
+}
+
 // Give a cached block back to the pool.  The stream that freed it may no longer exist
 // (a caller's stream), so wait for its event on the host and free on the legacy stream.
 void release_block(const CachedBlock& b) {
@@ -120,6 +161,7 @@ void release_block(const CachedBlock& b) {
 void* cache_alloc(size_t bytes, cudaStream_t s, bool* from_pool) {
     bytes = round_bytes(bytes);
     *from_pool = capturing(s);
+    if (!*from_pool && guard_mode()) return guard_alloc(bytes, s);
     if (*from_pool) {
         void* p = nullptr;
         UOTK_CUDA(cudaMallocAsync(&p, bytes, s));
@@ -159,6 +201,7 @@ void cache_free(void* p, size_t bytes, cudaStream_t s, bool from_pool) {
         return;
     }
     bytes = round_bytes(bytes);
+    if (guard_mode()) return guard_free(p, bytes, s);
     int dev = 0;
     cudaEvent_t ev = nullptr;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -179,6 +222,8 @@ void cache_free(void* p, size_t bytes, cudaStream_t s, bool from_pool) {
     }
 }
 }  // namespace
+
+int64_t guard_violations() { return g_guard_violations.load(); }
 
 // bytes held by the block cache on the current device, and releasing them to the pool
 size_t block_cache_bytes() {

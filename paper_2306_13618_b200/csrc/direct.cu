@@ -40,6 +40,20 @@ __device__ __forceinline__ double pair_sum_tile(const double (*sp)[kTile], const
             }
             acc = fma(r2 * exp(-r2 * inv_or_c2), sw[j], acc);
         }
+    } else if (kind == UOTK_LAP || kind == UOTK_ENERGY) {
+        // Laplace exp(-r/l) (inv_or_c2 = 1/l) and the energy kernel -r (Eq. 4.2; Table 1)
+        const bool lap = kind == UOTK_LAP;
+#pragma unroll 4
+        for (int j = 0; j < cnt; ++j) {
+            double r2 = 0.0;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const double v = xi[t] - sp[t][j];
+                r2 = fma(v, v, r2);
+            }
+            const double r = sqrt(r2);
+            acc = fma(lap ? exp(-r * inv_or_c2) : -r, sw[j], acc);
+        }
     } else {
 #pragma unroll 4
         for (int j = 0; j < cnt; ++j) {
@@ -138,6 +152,8 @@ __global__ void __launch_bounds__(WT) direct_warp_k(int64_t n_src, const double*
             double kv;
             if (kind == UOTK_GAUSS) kv = exp(-r2 * inv_or_c2);
             else if (kind == UOTK_GAUSS_R2) kv = r2 * exp(-r2 * inv_or_c2);
+            else if (kind == UOTK_LAP) kv = exp(-sqrt(r2) * inv_or_c2);
+            else if (kind == UOTK_ENERGY) kv = -sqrt(r2);
             else kv = 1.0 / sqrt(r2);
             part = fma(kv, sw[j], part);
         }

@@ -319,8 +319,15 @@ void gather_dm(const PointSet& ps, const double* grid, const FastParams& fp, con
         }                                                                         \
     } while (0)
 
+void spread_deterministic(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp,
+                          cudaStream_t s);  // determ.cu
+
 void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s) {
     if (ps.n == 0) return;
+    if (fp.deterministic) {
+        spread_deterministic(ps, w_sorted, grid, fp, s);
+        return;
+    }
     if (chunked_available(fp) && ps.chunked) {
         chunked_spread(ps, w_sorted, grid, fp, s);
         return;

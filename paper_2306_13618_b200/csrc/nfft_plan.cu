@@ -55,13 +55,66 @@ std::vector<long double> imq_taylor(long double h, long double c, long double r0
     return y;
 }
 
+// Taylor coefficients y_k = K^(k)(r0)/k! (torus radius r0, physical radius h r0) of the
+// Laplace kernel exp(-h r / l) and of the energy kernel -h r.
+std::vector<long double> lap_taylor(long double h, long double ell, long double r0, int n) {
+    std::vector<long double> y(n);
+    const long double a = -h / ell;
+    long double v = expl(a * r0);
+    for (int k = 0; k < n; ++k) {
+        y[k] = v;
+        v *= a / (k + 1);
+    }
+    return y;
+}
+std::vector<long double> energy_taylor(long double h, long double r0, int n) {
+    std::vector<long double> y(n, 0.0L);
+    y[0] = -h * r0;
+    if (n > 1) y[1] = -h;
+    return y;
+}
+
+// Interior regularisation of the kernels that are not smooth at 0 (Laplace, energy;
+// Rem. 4.2 P:608, reading R24): on ||y|| < eps_I (torus units) K_R(y) = Q(||y||^2) with Q
+// the degree p-1 Taylor polynomial of f(s) = K(h sqrt(s)) at s_I = eps_I^2 — a polynomial
+// in the coordinates inside the ball (smooth at 0) matching K to order p-1 on the sphere.
+// Returns the coefficients of Q in powers of (s - s_I).  Power series: sqrt(s_I + t) by
+// the binomial series, then exp of a series (Laplace) or a multiple (energy).
+std::vector<double> interior_poly(int kind, long double h, long double ell, long double epsI, int p) {
+    const long double sI = epsI * epsI;
+    std::vector<long double> g(p);  // sqrt(s_I + t) = sum g_k t^k
+    long double c = sqrtl(sI);
+    for (int k = 0; k < p; ++k) {
+        g[k] = c;
+        c *= (0.5L - k) / ((k + 1) * sI);
+    }
+    std::vector<long double> f(p);
+    if (kind == UOTK_ENERGY) {
+        for (int k = 0; k < p; ++k) f[k] = -h * g[k];
+    } else {  // exp(A(t)), A = -(h/l) g: E_0 = e^{A_0}, E_k = (1/k) sum_{j=1}^k j A_j E_{k-j}
+        std::vector<long double> A(p);
+        for (int k = 0; k < p; ++k) A[k] = -h / ell * g[k];
+        f[0] = expl(A[0]);
+        for (int k = 1; k < p; ++k) {
+            long double acc = 0;
+            for (int j = 1; j <= k; ++j) acc += j * A[j] * f[k - j];
+            f[k] = acc / k;
+        }
+    }
+    std::vector<double> out(p);
+    for (int k = 0; k < p; ++k) out[k] = (double)f[k];
+    return out;
+}
+
 // Boundary polynomial K_B on t = (r - r0)/eps_B in [0, 1], r0 = 1/2 - eps_B:
 // P^(j)(0) = eps_B^j K^(j)(r0) for j < p (C^{p-1} match with K) and P^(j)(1) = 0 for
 // 1 <= j < p (flat at the torus boundary r = 1/2, so the radial extension by the
 // constant P(1) is smooth across the sphere ||y|| = 1/2 in every dimension; reading R10).
-std::vector<double> imq_boundary_poly(double h, double c, double eps_B, int p) {
+std::vector<double> boundary_poly(int kind, double h, double param, double eps_B, int p) {
     const long double r0 = 0.5L - eps_B;
-    std::vector<long double> y = imq_taylor(h, c, r0, p);
+    std::vector<long double> y = kind == UOTK_IMQ   ? imq_taylor(h, param, r0, p)
+                                 : kind == UOTK_LAP ? lap_taylor(h, param, r0, p)
+                                                    : energy_taylor(h, r0, p);
     std::vector<long double> a(p);
     long double e = 1;
     for (int j = 0; j < p; ++j) { a[j] = y[j] * e; e *= eps_B; }
@@ -117,6 +170,7 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
     fp.m = o.m > 0 ? o.m : 8;
     if (fp.m < 2 || fp.m > 8) fail(UOTK_EINVAL, "opts.m must be in [2, 8]");
     fp.flags = o.flags;
+    fp.deterministic = o.deterministic != 0;
     if ((fp.flags & UOTK_FLAG_CHUNKED) && !(fp.m == 8 || (fp.m == 6 && d == 3)))
         fail(UOTK_EINVAL, "UOTK_FLAG_CHUNKED needs m = 8 (or m = 6 in d = 3)");
     const double sigma = o.sigma > 0 ? o.sigma : 2.0;
@@ -134,7 +188,7 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
         h_min = h_decay;
         fp.eps_B = 0;
         fp.p = 0;
-    } else {
+    } else {  // IMQ, Laplace, energy: boundary polynomial K_B (and for the latter two K_I)
         fp.p = o.p > 0 ? o.p : 12;
         if (fp.p < 2 || fp.p > 16) fail(UOTK_EINVAL, "opts.p must be in [2, 16]");
         fp.eps_B = o.eps_B > 0 ? o.eps_B : 0.1;
@@ -147,7 +201,7 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
         if (o.h < rmax / Rbar_max * (1 - 1e-12)) fail(UOTK_EINVAL, "opts.h too small for the point cloud");
         h = o.h;
     }
-    if (!(h > 0)) h = (kind == UOTK_IMQ) ? std::max(param, 1e-3) : 1.0;
+    if (!(h > 0)) h = (kind == UOTK_IMQ || kind == UOTK_LAP) ? std::max(param, 1e-3) : 1.0;
     fp.h = h;
 
     int N = o.N;
@@ -156,8 +210,10 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
             const double eb = param / (h * h);  // kernel exp(-|y|^2/eb) in torus units
             N = (int)std::ceil(2.0 * std::sqrt(L / (M_PI * M_PI * eb)));
             N = nice_even(std::max(N, 8));
-        } else {
+        } else if (kind == UOTK_IMQ) {
             N = (d == 3) ? 192 : 256;
+        } else {
+            N = 256;  // Laplace / energy: with p = 12, eps_I = p/N (reading R24)
         }
     }
     if (N % 2) fail(UOTK_EINVAL, "opts.N must be even");
@@ -180,7 +236,13 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
         fp.box_lo = lo;
         fp.box_w = hi - lo;
     }
-    if (kind == UOTK_IMQ) fp.poly = imq_boundary_poly(h, param, fp.eps_B, fp.p);
+    if (kind == UOTK_IMQ || kind == UOTK_LAP || kind == UOTK_ENERGY)
+        fp.poly = boundary_poly(kind, h, param, fp.eps_B, fp.p);
+    if (kind == UOTK_LAP || kind == UOTK_ENERGY) {
+        fp.eps_I = (double)fp.p / N;
+        if (fp.eps_I >= 0.5 - fp.eps_B) fail(UOTK_EINVAL, "eps_I = p/N must stay below 1/2 - eps_B");
+        fp.poly_I = interior_poly(kind, h, param, fp.eps_I, fp.p);
+    }
     return fp;
 }
 
@@ -192,6 +254,9 @@ struct KernelCoef {
     double r0, eps_B;
     int npoly;
     double poly[32];
+    double sI;      // eps_I^2 (interior regularisation, Laplace / energy)
+    int npolyI;
+    double polyI[16];
 };
 
 // Samples of the regularised kernel K_R on the N^d grid j/N, j in I_N (stored at j mod N).
@@ -217,8 +282,15 @@ __global__ void sample_kernel_k(double* out, int N, KernelCoef kc) {
         v = kc.h2 * r2 * exp(-kc.h2 * r2 / kc.param);  // physical r^2 = h^2 r^2 (torus units)
     } else {
         double r = sqrt(r2);
-        if (r <= kc.r0) {
-            v = 1.0 / sqrt(kc.h2 * r2 + kc.param * kc.param);
+        if (kc.npolyI > 0 && r2 < kc.sI) {  // interior K_I: Q(r^2) (Laplace, energy)
+            const double ds = r2 - kc.sI;
+            double acc = 0;
+            for (int k = kc.npolyI - 1; k >= 0; --k) acc = acc * ds + kc.polyI[k];
+            v = acc;
+        } else if (r <= kc.r0) {
+            const double hr = sqrt(kc.h2) * r;
+            v = kc.kind == UOTK_IMQ ? 1.0 / sqrt(kc.h2 * r2 + kc.param * kc.param)
+                                    : (kc.kind == UOTK_LAP ? exp(-hr / kc.param) : -hr);
         } else {
             double tt = r >= 0.5 ? 1.0 : (r - kc.r0) / kc.eps_B;
             double acc = 0;
@@ -385,6 +457,10 @@ void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s) {
     kc.npoly = (int)fp.poly.size();
     if (kc.npoly > 32) fail(UOTK_EINVAL, "boundary polynomial too long");
     for (int k = 0; k < kc.npoly; ++k) kc.poly[k] = fp.poly[k];
+    kc.sI = fp.eps_I * fp.eps_I;
+    kc.npolyI = (int)fp.poly_I.size();
+    if (kc.npolyI > 16) fail(UOTK_EINVAL, "interior polynomial too long");
+    for (int k = 0; k < kc.npolyI; ++k) kc.polyI[k] = fp.poly_I[k];
     const int tb = 256;
     int gb = (int)((nsamp + tb - 1) / tb);
     if (d == 1) sample_kernel_k<1><<<gb, tb, 0, s>>>(samp.p, N, kc);

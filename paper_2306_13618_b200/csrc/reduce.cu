@@ -76,6 +76,12 @@ __global__ void check_finite_k(const double* __restrict__ a, int64_t n, int* __r
     if (i < n && !isfinite(a[i])) atomicOr(flag, bit);
 }
 
+__global__ void multiply_k(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                           double* __restrict__ prod) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) prod[i] = a[i] * b[i];
+}
+
 __global__ void split_bits_k(const int* __restrict__ flag, int32_t* __restrict__ bits) {
     if (threadIdx.x < 4) bits[threadIdx.x] = (*flag >> threadIdx.x) & 1;
 }
@@ -163,6 +169,12 @@ void check_mass(const double* a, int64_t n, int* flag, cudaStream_t s) {
 void check_finite(const double* a, int64_t n, int* flag, int bit, cudaStream_t s) {
     if (n == 0) return;
     check_finite_k<<<blocks_for(n, 256), 256, 0, s>>>(a, n, flag, bit);
+    UOTK_LAUNCHED();
+}
+
+void multiply(const double* a, const double* b, int64_t n, double* prod, cudaStream_t s) {
+    if (n == 0) return;
+    multiply_k<<<blocks_for(n, 256), 256, 0, s>>>(a, b, n, prod);
     UOTK_LAUNCHED();
 }
 

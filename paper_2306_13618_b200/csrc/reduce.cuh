@@ -19,6 +19,8 @@ void join_bits(const int32_t* bits, int* flag, cudaStream_t s);
 void scaled_mass(const double* mass, const double* pot, int64_t n, double lam, double* w, cudaStream_t s);
 // cols (n x (2 + d), column-major): a, a ||x - c||^2, a (x - c)  (c: d device values or NULL)
 void moment_cols(const double* x, const double* a, int64_t n, int d, const double* c, double* cols, cudaStream_t s);
+// prod[i] = a[i] * b[i]
+void multiply(const double* a, const double* b, int64_t n, double* prod, cudaStream_t s);
 void signed_concat(const double* a, int64_t n, const double* b, int64_t m, double* w, cudaStream_t s);
 
 }  // namespace uotk

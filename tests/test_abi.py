@@ -84,7 +84,7 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     with pytest.raises(uk.UotkError) as e:
         uk.mmd2(x, np.ones(4), x, np.ones(4), "imq", 0.0)
     assert e.value.code == -1
-    for bad in (16, uk.FLAG_GENERIC | uk.FLAG_CHUNKED):
+    for bad in (32, uk.FLAG_GENERIC | uk.FLAG_CHUNKED):
         with pytest.raises(uk.UotkError) as e:
             uk.kernel_sum(x, np.ones(4), x, "gauss", 0.1, opts={"flags": bad})
         assert e.value.code == -1
