@@ -3,13 +3,15 @@ r = 1 Sinkhorn iteration (Laplace Gibbs kernel), each against the CPU oracle.
 
 Tolerances (reading R24): the kernels are not smooth at 0, so the NFFT path
 regularises them inside eps_I = p/N and adds the exact near-field correction; the
-remaining error is that of the trigonometric approximation of the regularised kernel,
-~5e-10 of max|K| at the defaults (N = 256, p = 12; the paper's own Laplace / energy
-residuals are ~1e-6, Table 4).  Bars:
-  * kernel sums: max_i |ds_i| <= 1e-8 * max|K| * sum_j |alpha_j|  (max|K| over the cloud);
+remaining error is that of the trigonometric approximation of the regularised kernel:
+measured <= 7e-13 of max|K| sum|alpha| and <= 5e-12 per entry (positive weights) at the
+defaults N = 256, p = 12 in d = 1..3 (profiles/r02/f2_accuracy.jsonl; the paper's own
+Laplace / energy residuals are ~1e-6, Table 4).  The bars are the north
+star's:
+  * kernel sums: max_i |ds_i| <= 1e-9 * max|K| * sum_j |alpha_j| (signed weights; max|K|
+    over the cloud, reading R14's normalisation), per entry 1e-9 for positive weights;
   * MMD^2: |d| / max(|MMD^2|, 1e-3 * sum of |quadratic terms|) <= 1e-8 (reading R13);
-  * r = 1 UOT: potentials element by element and objective values within 1e-8 at the
-    workload of reading R24 (eps = 0.2 on the radius-0.2 cloud).
+  * r = 1 UOT: potentials element by element and objective values within 1e-8.
 The DIRECT path must match the oracle to 1e-12 in every case.
 """
 
@@ -52,7 +54,7 @@ def test_kernel_sum_f2(uk, method, kind, param, d):
                               return_info=True)
     assert info["method"] == method
     err = np.max(np.abs(got.cpu().numpy() - ref)) / (kmax(kind, 0.2) * np.sum(np.abs(pr.alpha)))
-    assert err <= (1e-12 if method == "direct" else 1e-8), (err, info)
+    assert err <= (1e-12 if method == "direct" else 1e-9), (err, info)
 
 
 @pytest.mark.parametrize("kind,param", [(LAP, 0.05), (ENERGY, 1.0)])
@@ -68,7 +70,9 @@ def test_kernel_sum_f2_chunked_ragged_and_coincident(uk, kind, param):
     for flags in (2, 1):
         got = uk.kernel_sum(cuda(src), cuda(al), cuda(tgt), kind, param, opts={"method": "nfft", "flags": flags})
         err = np.max(np.abs(got.cpu().numpy() - ref)) / (kmax(kind, 0.2) * al.sum())
-        assert err <= 1e-8, (flags, err)
+        assert err <= 1e-9, (flags, err)
+        if kind == LAP:  # positive weights, positive kernel: per entry
+            assert np.max(np.abs(got.cpu().numpy() - ref) / ref) <= 1e-9
     p = np.array([[0.01, -0.02, 0.03]])
     one = uk.kernel_sum(cuda(p), cuda(np.array([2.0])), cuda(p), kind, param, opts={"method": "nfft"})
     assert abs(one.item() - (2.0 if kind == LAP else 0.0)) <= 1e-8 * 2.0
@@ -101,11 +105,13 @@ def _pot_err(got, ref, c):
 
 @pytest.mark.parametrize("method", ["direct", "nfft"])
 @pytest.mark.parametrize("d", [1, 2, 3])
-def test_uot_r1_laplace_gibbs(uk, method, d):
+@pytest.mark.parametrize("eps", [0.05, 0.2])
+def test_uot_r1_laplace_gibbs(uk, method, d, eps):
     """Algorithm 2 with r = 1 (UOTK_FLAG_COST_R1): t_i = sum_j e^{-lambda ||x_i - y_j||} ...
-    against the oracle's r = 1 iteration, C1's distributions with eps = 0.2 (reading R24)."""
+    against the oracle's r = 1 iteration: C1's distributions and lambda = 20 (eps = 0.05,
+    the paper's Table 2 parameters) and a wider kernel."""
     pr = W.c1_uot(n=1200, m=1000, d=d)
-    eps, lam, iters = 0.2, 1.0, 15
+    lam, iters = 1.0, 15
     ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, eps, lam, lam, iters, r=1)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), eps, lam, iters=iters,
                                        opts={"method": method, "flags": uk.FLAG_COST_R1})
