@@ -54,7 +54,7 @@ def build(verbose=False, force=False):
         objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
     if os.path.exists(LIB) and os.path.getmtime(LIB) > max(os.path.getmtime(o) for o in objs):
         return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-lcublas", "-ldl", "-Xlinker",
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-ldl", "-Xlinker",
            "-rpath,/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -448,7 +448,10 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         // the near-field corrected r = 1 kernel) runs gather, update and spread separately
         const bool nf = nearfield_needed(fp);  // r = 1: Laplace Gibbs kernel, near-field corrected
         const bool fused = chunked_available(fp) && PX.chunked && PY.chunked && !fp.deterministic && !nf;
-        if (fused) grid2.alloc(ge, s);
+        if (fused) {
+            grid2.alloc(ge, s);
+            grid2.zero();
+        }
         NearField NX, NY;
         DevBuf<double> tbx, tby;  // kernel sums in sorted order (gather + near field)
         if (nf) {
@@ -476,22 +479,25 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
             if (last) dmax.zero();
             EpiSinkhorn e2 = ey;
             if (last) e2.t_store = ty.p;
+            // the separable chain zeroes the footprint box of the next spread's target grid
+            // as a side job (both grids are zero outside the box); else a full memset
+            bool zd = false;
             if (fused) {
                 // beta-step at x: gather t from g', update, spread mu (.) u into the other grid
-                const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
-                grid2.zero();
+                const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm, grid2.p, &zd);
+                if (!zd) grid2.zero();
                 chunked_gather_spread(PX, g1, grid2.p, fp, ex, last ? dmax.p : nullptr, s);
-                const double* g2 = fft_chain(ns.sp, grid2.p, spec.p, s, comm);
-                grid.zero();
+                const double* g2 = fft_chain(ns.sp, grid2.p, spec.p, s, comm, grid.p, &zd);
+                if (!zd) grid.zero();
                 chunked_gather_spread(PY, g2, grid.p, fp, e2, last ? dmax.p + 1 : nullptr, s);
             } else {
-                const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                const double* g1 = fft_chain(ns.sp, grid.p, spec.p, s, comm, grid.p, &zd);
                 half_step(PX, NX, NY, wy.p, tbx.p, n, g1, ex, last ? dmax.p : nullptr);  // (3.3)
-                grid.zero();
+                if (!zd) grid.zero();
                 spread(PX, wx.p, grid.p, fp, s);
-                const double* g2 = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+                const double* g2 = fft_chain(ns.sp, grid.p, spec.p, s, comm, grid.p, &zd);
                 half_step(PY, NY, NX, wx.p, tby.p, m, g2, e2, last ? dmax.p + 1 : nullptr);  // (3.4)
-                grid.zero();
+                if (!zd) grid.zero();
                 spread(PY, wy.p, grid.p, fp, s);
             }
         };

@@ -192,6 +192,7 @@ struct SpectralPlan {
     size_t grid_elems = 0;   // ng^d
     size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
     cudaStream_t use_stream = nullptr;  // the call's stream (build_spectral_plan)
+    DevBuf<double> work;                // the separable chain's compact intermediate (w^d)
     ~SpectralPlan() {
         if (pd) pd->note_use(use_stream);
     }
@@ -224,8 +225,10 @@ void unpermute_values(double* dst, const double* src, const int32_t* perm, int64
 void spread(const PointSet& ps, const double* w_sorted, double* grid, const FastParams& fp, cudaStream_t s);
 // g' = F^-1 (D .* F g): returns the buffer holding g' (grid itself, or spec's storage
 // reinterpreted as n_g^d doubles on the separable path)
-double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
-void get_cublas(void** handle);  // per-device cuBLAS handle (context.cu)
+// zero_next (optional): a grid that is zero outside the footprint box; the separable chain
+// zeroes its box as a side job (then *zeroed = true: the caller's memset is not needed)
+double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm,
+                  double* zero_next = nullptr, bool* zeroed = nullptr);
 // cuFFT plans of the pruned 3-D forward transform (box width w, kept modes |k| <= H)
 void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cufftHandle* px, cufftHandle* pzi);
 void gather(const PointSet& ps, const double* grid, double* out_sorted, const FastParams& fp, cudaStream_t s);

@@ -8,7 +8,6 @@
 #include <mutex>
 #include <tuple>
 
-#include <cublas_v2.h>
 
 #include "common.cuh"
 
@@ -337,7 +336,6 @@ struct Context {
     // (device, slot, d, n) -> (r2c, c2r)
     std::map<std::tuple<int, int, int, int>, std::pair<cufftHandle, cufftHandle>> fft;
     bool pool_configured[64] = {};
-    std::map<std::pair<int, int>, cublasHandle_t> blas;  // (device, slot)
     // (device, slot, n, w, H) -> pruned-transform plans (pass z R2C, pass y C2C, pass x C2C)
     std::map<std::tuple<int, int, int, int, int>, std::array<cufftHandle, 4>> pruned;
     std::map<int, cudaStream_t> streams;
@@ -427,20 +425,6 @@ void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cuf
     *py = it->second[1];
     *px = it->second[2];
     *pzi = it->second[3];
-}
-
-void get_cublas(void** handle) {
-    int dev = 0;
-    UOTK_CUDA(cudaGetDevice(&dev));
-    Context& c = ctx();
-    std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.blas.find({dev, g_slot});
-    if (it == c.blas.end()) {
-        cublasHandle_t h;
-        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cublasCreate failed");
-        it = c.blas.emplace(std::make_pair(dev, g_slot), h).first;
-    }
-    *handle = it->second;
 }
 
 cudaStream_t private_stream() {

@@ -2,7 +2,6 @@
 // (4.6)), the FFT chain with the fused D_k multiplication, and interpolation
 // (forward NFFT, outer sum of (4.6)) — P:590-592.  These are the simple
 // thread-per-point kernels; the tuned cell-group kernels live in fused3d.cu / fused12d.cu.
-#include <cublas_v2.h>
 #include <cstdlib>
 
 #include <string>
@@ -372,71 +371,25 @@ void gather(const PointSet& ps, const double* grid, double* out_sorted, const Fa
 
 int comm_nranks(void* comm);  // comm.cu
 
-// Separable chain (Gaussian kernel, one rank): one GEMM pass per axis with the circulant
-// Csep on the FP64 tensor cores (cuBLAS DGEMM), restricted to the box [o, o + w)^d that
-// holds every footprint (outside it the spread grid is zero and no gather reads): pass t
-// maps the box of the input to the box of the output along axis t, so the work is
-// d w^(d+1) instead of d n^(d+1) (C3: w = 44 of n = 96).  The grid is row-major
-// (last axis contiguous); cuBLAS is column-major.  Csep is symmetric, so any square
-// sub-block C[o.., o..] read column-major with ld n is the same sub-block.
-// Returns the buffer holding g' in grid layout (valid inside the box only).
+// Separable chain (Gaussian kernel): circgemm.cu, hand-written DMMA GEMM passes on the box
+double* separable_chain_dmma(const FastParams& fp, const double* Csep, double* grid, double* spare, double* work,
+                             double* zero_next, cudaStream_t s, void* comm);
 void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);  // comm.cu
-
-// With several ranks every rank spread its own sources: the chain is linear, so the
-// first pass's compact output (w^d doubles — the size of the truncated spectrum the FFT
-// path would all-reduce) is summed over ranks (NCCL) before the remaining passes.
-static double* separable_chain(SpectralPlan& sp, double* grid, double* spare, cudaStream_t s, void* comm) {
-    const FastParams& fp = sp.fp;
-    const int n = fp.ng;
-    const int o = fp.box_lo, w = fp.box_w;
-    const long long n2 = (long long)n * n, w2 = (long long)w * w;
-    void* hv = nullptr;
-    get_cublas(&hv);
-    cublasHandle_t h = (cublasHandle_t)hv;
-    if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cublasSetStream failed");
-    const double one = 1.0, zero = 0.0;
-    const double* Cb = sp.pd->Csep.p + (size_t)o * n + o;  // the box block of Csep
-    auto ok = [](cublasStatus_t st) {
-        if (st != CUBLAS_STATUS_SUCCESS) fail(UOTK_ECUDA, "cuBLAS DGEMM failed (" + std::to_string((int)st) + ")");
-    };
-    if (fp.d == 1) {  // out[z] = sum_z' C[z][z'] g[z']
-        ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, w, 1, w, &one, Cb, n, grid + o, w, &zero, spare + o, w));
-        add_launches(1);
-        if (comm) comm_allreduce(spare + o, (size_t)w, 0, comm, s);  // sum
-        return spare;
-    }
-    if (fp.d == 2) {
-        // y: T1(y, x) = sum_y' C[y][y'] g[x][y']                      (compact w x w in spare)
-        ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, Cb, n, grid + (size_t)o * n + o, n, &zero, spare,
-                       w));
-        if (comm) comm_allreduce(spare, (size_t)w2, 0, comm, s);  // sum
-        // x: out[x][y] = sum_x' T1(y, x') C[x'][x]                    (into grid, box positions)
-        ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, spare, w, Cb, n, &zero, grid + (size_t)o * n + o,
-                       n));
-        add_launches(2);
-        return grid;
-    }
-    // d = 3.  z, per x: T1[x][y][z] = sum_z' C[z][z'] g[x][y][z']   (compact w^3 in spare)
-    ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, Cb, n, 0,
-                                 grid + (size_t)o * n2 + (size_t)o * n + o, n, n2, &zero, spare, w, w2, w));
-    if (comm) comm_allreduce(spare, (size_t)w2 * w, 0, comm, s);  // sum
-    // y, per x: T2[x][y][z] = sum_y' T1[x][y'][z] C[y'][y]          (compact w^3 in grid)
-    ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, spare, w, w2, Cb, n, 0, &zero, grid, w,
-                                 w2, w));
-    // x, per y: out[x][y][z] = sum_x' T2[x'][y][z] C[x'][x]         (into spare, box positions)
-    ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, w, w, w, &one, grid, (int)w2, w, Cb, n, 0, &zero,
-                                 spare + (size_t)o * n2 + (size_t)o * n + o, (int)n2, n, w));
-    add_launches(3);
-    return spare;
-}
 
 static double* fft_chain_pruned(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm);
 
-double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm) {
+double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s, void* comm, double* zero_next,
+                  bool* zeroed) {
     const FastParams& fp = sp.fp;
+    if (zeroed) *zeroed = false;
     if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT)) {
-        ProfScope ps_(kProfFft, s);
-        return separable_chain(sp, grid, reinterpret_cast<double*>(spec), s, comm);
+        size_t wd = 1;
+        for (int t = 0; t < fp.d; ++t) wd *= fp.box_w;
+        if (sp.work.n < wd) sp.work.alloc(wd, s);
+        if (fp.d == 1 && zero_next == grid) zero_next = nullptr;  // d = 1: one pass, still reading it
+        if (zeroed) *zeroed = zero_next != nullptr;
+        return separable_chain_dmma(fp, sp.pd->Csep.p, grid, reinterpret_cast<double*>(spec), sp.work.p, zero_next, s,
+                                    comm);
     }
     ProfScope ps_(kProfFft, s);
     {
