@@ -151,6 +151,7 @@ struct NfftSetup {
 
 void setup_nfft(NfftSetup& ns, int d, int kind, double param, const double* p1, int64_t n1, const double* p2,
                 int64_t n2, const uotk_opts& o, void* comm, cudaStream_t s) {
+    NvtxRange nvtx_("setup");
     trace_mark("setup_nfft: start");
     Geometry g = compute_geometry(d, p1, n1, p2, n2, s, comm);
     trace_mark("geometry");
@@ -188,6 +189,7 @@ constexpr int kGraphIters = 16;  // iterations per captured graph
 template <class F>
 int run_iterations(int iters, F&& iterate, bool use_graph, cudaStream_t s, int check_every = 0,
                    double stop_tol = 0.0, unsigned long long* dmax = nullptr, void* comm = nullptr) {
+    NvtxRange nvtx_("iterations");
     if (check_every > 0) {
         // stopping rule: after every check_every-th iteration read the two sup-norm
         // changes (non-negative doubles stored as their bit patterns) and stop if both
@@ -264,6 +266,7 @@ template struct DevBuf<int>;
 static void kernel_sum_impl(int d, int64_t n_src, const double* src, const double* alpha, int64_t n_tgt,
                             const double* tgt, int kind, double param, double* out, const uotk_opts* opts_in,
                             uotk_info* info, void* comm, cudaStream_t s) {
+    NvtxRange nvtx_call("uotk_kernel_sum");
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
     need(kind >= UOTK_GAUSS && kind <= UOTK_ENERGY, "unknown kernel kind");
     need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");
@@ -328,6 +331,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
                      double eps, double lam1, double lam2, int iters, const double* gamma_init, double* beta_out,
                      double* gamma_out, uotk_uot_result* res, const uotk_opts* opts_in, void* comm, cudaStream_t s,
                      double* p_out = nullptr, double* q_out = nullptr) {
+    NvtxRange nvtx_call("uotk_uot_sinkhorn");
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
     // a rank's local shard may be empty (it still takes part in every collective)
     if (comm_nranks(comm) > 1) need(n >= 0 && m >= 0, "n and m must be >= 0");
@@ -527,6 +531,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
         }
     }
 
+    NvtxRange nvtx_obj("objectives");
     // objective terms and their global sums
     DevBuf<double> cols(5 * (size_t)std::max(n, m), s), sums(13, s);
     sums.zero();
@@ -596,6 +601,7 @@ static void uot_impl(int d, int64_t n, const double* x, const double* a, int64_t
 static void sd_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
                     const double* b, double eps, double lam1, double lam2, int iters, double* sd, double* terms,
                     const uotk_opts* opts, void* comm, cudaStream_t s) {
+    NvtxRange nvtx_call("uotk_sinkhorn_divergence");
     need(sd != nullptr, "sd output pointer is null");
     need(n >= 1 && m >= 1, "n and m must be >= 1");
     ensure_pool();
@@ -648,6 +654,7 @@ void on_capturable_stream(cudaStream_t cs, bool graphable, F&& f) {
 static void cstar_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
                        const double* b, double eps, double lam1, double lam2, double* cstar, void* comm,
                        cudaStream_t s) {
+    NvtxRange nvtx_call("uotk_uot_cstar");
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
     if (comm_nranks(comm) > 1) need(n >= 0 && m >= 0, "n and m must be >= 0");  // empty shards take part
     else need(n >= 1 && m >= 1, "n and m must be >= 1");
@@ -706,6 +713,7 @@ static void cstar_impl(int d, int64_t n, const double* x, const double* a, int64
 static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_t m, const double* y,
                       const double* b, int kind, double param, double* mmd2, const uotk_opts* opts_in, uotk_info* info,
                       void* comm, cudaStream_t s) {
+    NvtxRange nvtx_call("uotk_mmd2");
     need(d >= 1 && d <= 3, "d must be 1, 2 or 3");
     need(kind == UOTK_GAUSS || kind == UOTK_IMQ || kind == UOTK_LAP || kind == UOTK_ENERGY, "unknown kernel kind");
     need(param > 0 && std::isfinite(param), "kernel parameter must be positive and finite");

@@ -6,6 +6,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "profile.cuh"
 
 namespace uotk {
 
@@ -204,6 +205,7 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
 
 void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
                    PointUse use) {
+    NvtxRange nvtx_("pointset");
     const int d = fp.d;
     ps.d = d;
     ps.n = n;

@@ -44,6 +44,7 @@ bool profiling_enabled() {
 }
 
 ProfScope::ProfScope(int tag, cudaStream_t s) : tag_(tag), s_(s) {
+    nvtxRangePushA(kTagNames[tag]);
     Prof& p = prof();
     if (!p.on) return;
     std::lock_guard<std::mutex> lk(p.mu);
@@ -54,6 +55,7 @@ ProfScope::ProfScope(int tag, cudaStream_t s) : tag_(tag), s_(s) {
 }
 
 ProfScope::~ProfScope() {
+    nvtxRangePop();
     if (!active_) return;
     Prof& p = prof();
     std::lock_guard<std::mutex> lk(p.mu);
