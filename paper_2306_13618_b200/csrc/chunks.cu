@@ -226,7 +226,13 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     // a gather-only set this sparse is gathered by the generic kernel anyway (nfft.cu)
     if (!forced && use == kUseGatherOnly && d == 3 && (double)n < kGatherMinFill3 * kChunk * (double)nchunks) return;
     const int wd = d == 3 ? chunk_win3_doubles(kz) : chunk_win_doubles(d);
-    const size_t win_bytes = (size_t)nchunks * wd * sizeof(double);
+    // spread-only d = 3 one-cell sets: the spread evaluates the windows itself
+    static const bool fly_env = [] {
+        const char* e = getenv("UOTK_SPREAD_FLY");
+        return !(e && e[0] == '0');
+    }();
+    const bool fly = fly_env && d == 3 && kz == 16 && fp.m == kChunkM && use == kUseSpreadOnly;
+    const size_t win_bytes = fly ? 0 : (size_t)nchunks * wd * sizeof(double);
     // cudaMemGetInfo can stall the host (milliseconds, and seconds when the stream-ordered
     // pool caches tens of GB): ask it only for blocks that are a noticeable fraction of the
     // device and that the pool's cached (reserved but unused) memory cannot hold already
@@ -269,7 +275,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
         return;
     }
     ps.chunk_desc.alloc(nchunks, s);
-    ps.chunk_win.alloc((size_t)nchunks * wd, s);
+    if (!fly) ps.chunk_win.alloc((size_t)nchunks * wd, s);
     chunk_desc_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, chunk_off.p, cnt.p,
                                                         ps.chunk_desc.p);
     UOTK_LAUNCHED();
@@ -290,7 +296,9 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
             fits.push_back({{fp.b, fp.m}, win});
         }
     }
-    {
+    ps.win_fly = fly;
+    if (fly) ps.win_coef = win;
+    if (!fly) {
         ProfScope prof(kProfSetup, s);
         const unsigned wb = (unsigned)((nchunks * d + kWinWarps - 1) / kWinWarps);
         if (d == 3 && kz == 12)

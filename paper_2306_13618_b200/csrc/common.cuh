@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/uotk.h"
+#include "window_fit.h"
 
 namespace uotk {
 
@@ -145,6 +146,10 @@ struct PointSet {
     DevBuf<int32_t> chunk_bounds_ws;  // d = 2: partition for the warp-specialised half-step
     int chunk_units_ws = 0;
     int chunk_kz = 16;        // d = 3: z extent of a group footprint (16 one cell, 24 z-segment)
+    // d = 3 spread-only one-cell sets: no window blocks, the spread evaluates them on the
+    // fly from the per-tap polynomials (fused3d.cu spread3d_fly_k)
+    bool win_fly = false;
+    KBHorner win_coef;
     double chunk_fill = 0;    // mean occupied fraction of the 32 chunk slots
 };
 

@@ -32,6 +32,7 @@
 #include "profile.cuh"
 #include "ptx.cuh"
 #include "window.cuh"
+#include "window_fit.h"
 
 namespace uotk {
 
@@ -599,6 +600,150 @@ spread3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
     if (cur_key >= 0) flush();
 }
 
+// ---------------------------------------------------------------- spread only, windows on the fly
+// For a set that is only ever spread (kernel sums' sources, MMD^2's z = x u y) the window
+// block of a chunk is used once: instead of precomputing it (a 15 KB HBM write and read
+// per chunk) the CTA evaluates it in shared memory two chunks ahead of the DMMAs — every
+// thread 6 of the 1536 taps (degree-14 polynomial per tap, window_fit.h; coefficients in
+// shared memory), released by an mbarrier all 256 threads arrive on; the eight warps
+// release a slot after their DMMAs (mbarrier, 8 arrivals) and the threads refill it.
+constexpr int kRingF = 4, kLeadF = 2;
+struct __align__(128) SmemF {
+    double win[kRingF][3][kChunk][kStride];
+    unsigned long long full[kRingF];
+    unsigned long long empty[kRingF];
+};
+
+__global__ void __launch_bounds__(kThreads, kBlocksPerSM)
+spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
+               const int32_t* __restrict__ bounds, int ng, double* __restrict__ grid_out,
+               const double* __restrict__ w_in, KBHorner hcoef) {
+    extern __shared__ __align__(128) unsigned char f_raw[];
+    SmemF& sm = *reinterpret_cast<SmemF*>(f_raw);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int gq = lane >> 2;
+    const int tq = lane & 3;
+    const int a0 = 2 * warp;
+    const int64_t cbeg = bounds[blockIdx.x];
+    const int64_t nck = bounds[blockIdx.x + 1] - cbeg;
+    const int64_t ng2 = (int64_t)ng * ng;
+    if (tid == 0) {
+        for (int r = 0; r < kRingF; ++r) {
+            mbar_init(&sm.full[r], kThreads);
+            mbar_init(&sm.empty[r], kThreads / 32);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+    // this thread's taps of a block: tap a = tid & 15 of the 6 rows r = (tid >> 4) + 16 i of
+    // [axis 3 x slot 32]; the tap's 15 polynomial coefficients stay in registers
+    const int fa = tid & 15, frow = tid >> 4;
+    double hcr[kHornerDeg + 1];
+#pragma unroll
+    for (int q = 0; q <= kHornerDeg; ++q) hcr[q] = hcoef.c[fa][q];
+    // the coordinates of the next block to fill are loaded one fill ahead (their L2 latency
+    // then overlaps a chunk of DMMAs instead of stalling the fill)
+    double uf[6];
+    int cntf = 0;
+    auto load_rows = [&](int64_t j) {
+        const int4 dj = j < nck ? desc[cbeg + j] : make_int4(0, 0, 0, 0);
+        cntf = dj.y;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int r = frow + 16 * i;
+            const int ax = r >> 5, p = r & 31;
+            uf[i] = p < dj.y ? u[(int64_t)ax * n + dj.x + p] : 0.0;
+        }
+    };
+    auto fill = [&](int64_t j) {
+        const int slot = (int)(j % kRingF);
+        double t[6];
+        int cnt = cntf;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) t[i] = uf[i] - floor(uf[i]) - 0.5;
+        load_rows(j + 1);
+        if (j >= kRingF) mbar_wait(&sm.empty[slot], (uint32_t)(((j - kRingF) / kRingF) & 1));
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int r = frow + 16 * i;
+            const int ax = r >> 5, p = r & 31;
+            double v = 0.0;
+            if (p < cnt) {
+                v = hcr[kHornerDeg];
+#pragma unroll
+                for (int q = kHornerDeg - 1; q >= 0; --q) v = fma(v, t[i], hcr[q]);
+            }
+            sm.win[slot][ax][p][fa] = v;
+        }
+        mbar_arrive(&sm.full[slot]);
+    };
+    load_rows(0);
+    for (int64_t j = 0; j < kLeadF && j < nck; ++j) fill(j);
+
+    double S[4][2][2];
+    int32_t cur_key = -1;
+    int64_t gorg = 0;
+    auto origin = [&](int32_t kk) -> int64_t {
+        const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
+        return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
+    };
+    auto flush = [&]() {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
+#pragma unroll
+            for (int nz = 0; nz < 2; ++nz)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (S[mt][nz][i] != 0.0) atomicAdd(grid_out + row + 8 * nz + 2 * tq + i, S[mt][nz][i]);
+        }
+    };
+    int4 d0 = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
+    double w_cur = lane < d0.y ? w_in[d0.x + lane] : 0.0;
+    for (int64_t k = 0; k < nck; ++k) {
+        const int slot = (int)(k % kRingF);
+        const int4 dsc = d0;
+        if (k + 1 < nck) d0 = desc[cbeg + k + 1];
+        const double w_nxt = (k + 1 < nck && lane < d0.y) ? w_in[d0.x + lane] : 0.0;
+        if (k + kLeadF < nck) fill(k + kLeadF);  // windows of a later chunk while this one's are ready
+        if (dsc.z != cur_key) {
+            if (cur_key >= 0) flush();
+            cur_key = dsc.z;
+            gorg = origin(cur_key);
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nz = 0; nz < 2; ++nz) S[mt][nz][0] = S[mt][nz][1] = 0.0;
+        }
+        mbar_wait(&sm.full[slot], (uint32_t)((k / kRingF) & 1));
+        const double(*wx)[kStride] = sm.win[slot][0];
+        const double(*wy)[kStride] = sm.win[slot][1];
+        const double(*wz)[kStride] = sm.win[slot][2];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            if (4 * ks >= dsc.y) break;  // k-steps past the chunk's points add zero windows
+            const int p = 4 * ks + tq;
+            const double wp = __shfl_sync(0xffffffffu, w_cur, p);
+            const double bz0 = wp * wz[p][gq], bz1 = wp * wz[p][8 + gq];
+            const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+            const double xv[2] = {xa.x, xa.y};
+            const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
+                dmma(S[mt][0][0], S[mt][0][1], am, bz0);
+                dmma(S[mt][1][0], S[mt][1][1], am, bz1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[slot]);  // this warp is done with the slot
+        w_cur = w_nxt;
+    }
+    if (cur_key >= 0) flush();
+}
+
 // ---------------------------------------------------------------- gather only, ring
 // The forward NFFT alone (kernel sums' targets): per chunk every warp contracts its
 // a-pair and writes 32 partial sums; the warp k mod 8 waits for all eight (mbarrier),
@@ -801,12 +946,20 @@ void fused3d_spread(const PointSet& ps, const double* w, double* grid, const Fas
         const char* e = getenv("UOTK_SPREAD_RING");
         return !(e && e[0] == '0');
     }();
-    if (!ring) {
+    if (!ring && !ps.win_fly) {
         launch<1, EpiNone>(ps, nullptr, grid, w, fp, EpiNone{}, nullptr, s, kProfSpread);
         return;
     }
     if (ps.n == 0 || ps.nchunks == 0) return;
     ProfScope prof(kProfSpread, s);
+    if (ps.win_fly) {  // spread-only set without precomputed window blocks (KZ = 16)
+        set_smem_attr((const void*)spread3d_fly_k, (int)sizeof(SmemF));
+        spread3d_fly_k<<<ps.chunk_blocks, kThreads, sizeof(SmemF), s>>>(ps.chunk_desc.p, ps.u.p, ps.n,
+                                                                        ps.chunk_bounds.p, fp.ng, grid, w,
+                                                                        ps.win_coef);
+        UOTK_LAUNCHED();
+        return;
+    }
     if (ps.chunk_kz == 40) {
         set_smem_attr((const void*)spread3d_k<40>, (int)sizeof(SmemS<40>));
         spread3d_k<40><<<ps.chunk_blocks, kThreads, sizeof(SmemS<40>), s>>>(ps.chunk_desc.p, ps.chunk_win.p,

@@ -774,3 +774,26 @@ def test_auto_method_crossover(uk):
     ref_b = uk.kernel_sum(cuda(big.src), cuda(big.alpha), cuda(big.tgt), "gauss", big.param,
                           opts={"method": "direct"})
     assert rel_err(got_b.cpu().numpy(), ref_b.cpu().numpy(), False) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+def test_spread_only_windows_on_the_fly(uk, kind):
+    """Spread-only d = 3 one-cell sets (kernel-sum sources, MMD^2's z) evaluate their window
+    blocks inside the spread kernel (spread3d_fly_k): dense sources (C3 per-cell density)
+    against the oracle for a kernel sum and an MMD^2, and against the precomputed-window
+    spread (UOTK_SPREAD_FLY=0 in a subprocess is the A/B; here: the generic kernels)."""
+    pr = W.c3_dense_uot(n=20000, m=3001)
+    param = 0.02 if kind == W.GAUSS else 0.05
+    got, info = uk.kernel_sum(cuda(pr.x), cuda(pr.a), cuda(pr.y), kind, param, opts={"method": "nfft"},
+                              return_info=True)
+    if kind == W.GAUSS:  # (the IMQ's torus scaling follows the cloud: a sparser grid, generic kernels)
+        assert info["groups"][0] == 16, info
+    ref = oracle.kernel_sum_direct(pr.x, pr.a, pr.y, kind, param)
+    assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9
+    gen = uk.kernel_sum(cuda(pr.x), cuda(pr.a), cuda(pr.y), kind, param, opts={"method": "nfft", "flags": uk.FLAG_GENERIC})
+    assert rel_err(got.cpu().numpy(), gen.cpu().numpy(), False) <= 1e-13
+    v, minfo = uk.mmd2(cuda(pr.x), cuda(pr.a), cuda(pr.y[:2500]), cuda(pr.b[:2500]), kind, param,
+                       opts={"method": "nfft"}, return_info=True)
+    mref = oracle.mmd2_direct(pr.x, pr.a, pr.y[:2500], pr.b[:2500], kind, param)
+    denom = max(abs(mref), 1e-3 * _mmd_tol(pr.x, pr.a, pr.y[:2500], pr.b[:2500], kind, param))
+    assert abs(v - mref) / denom <= 1e-8, (v, mref, minfo)
