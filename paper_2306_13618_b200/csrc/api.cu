@@ -28,6 +28,8 @@ int64_t guard_violations();     // context.cu (UOTK_GUARD=1)
 
 void spectrum_energy(SpectralPlan& sp, double* grid, double2* spec, double* part, int nparts, cudaStream_t s,
                      void* comm);  // nfft.cu
+void box_dot(const double* g, const double* gp, const FastParams& fp, double* part, int nparts,
+             cudaStream_t s);  // circgemm.cu
 
 void apply_sinkhorn_update(const double* t, int64_t n, const EpiSinkhorn& epi, unsigned long long* dmax,
                            cudaStream_t s);  // nearfield.cu
@@ -765,8 +767,17 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
         permute_values(ws.p, w.p, PZ.perm.p, nz, s);
         grid.zero();
         spread(PZ, ws.p, grid.p, ns.fp, s);
-        spectrum_energy(ns.sp, grid.p, spec.p, part.p, kParts, s, comm);
-        sum_columns(part.p, kParts, 1, sum.p, s);
+        if (ns.sp.pd->separable && !(ns.fp.flags & UOTK_FLAG_FFT)) {
+            // Gaussian: <g, g'> with g' the separable chain's output (no FFT, no cuFFT plan);
+            // with a communicator g' is global and <g_rank, g'> is summed over ranks
+            const double* gp = fft_chain(ns.sp, grid.p, spec.p, s, comm);
+            box_dot(grid.p, gp, ns.fp, part.p, kParts, s);
+            sum_columns(part.p, kParts, 1, sum.p, s);
+            if (comm) comm_allreduce(sum.p, 1, 0, comm, s);
+        } else {
+            spectrum_energy(ns.sp, grid.p, spec.p, part.p, kParts, s, comm);
+            sum_columns(part.p, kParts, 1, sum.p, s);
+        }
         if (nearfield_needed(ns.fp)) {
             // + sum_i w_i sum_{close j} (K - K_R)(z_i - z_j) w_j
             NearField NZ;

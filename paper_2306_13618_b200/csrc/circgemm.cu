@@ -222,4 +222,39 @@ double* separable_chain_dmma(const FastParams& fp, const double* Csep, double* g
     return spare;
 }
 
+// MMD^2 for the Gaussian without an FFT: sum_k D_k |G_k|^2 = <g, F^-1 (D . F g)> = <g, g'>
+// with g' the separable chain's output — the grid g is zero outside the footprint box, so
+// the inner product runs over the box only.  part[b] = this block's partial sum (fixed
+// order), reduced afterwards.
+namespace {
+__global__ void box_dot_k(const double* __restrict__ g, const double* __restrict__ gp, int d, int n, int o, int w,
+                          int64_t total, double* __restrict__ part) {
+    __shared__ double sm[256];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rem = i, off = 0, stride = 1;
+        for (int t = 0; t < d; ++t) {
+            off += (o + rem % w) * stride;
+            rem /= w;
+            stride *= n;
+        }
+        acc = fma(g[off], gp[off], acc);
+    }
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int k = 128; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sm[threadIdx.x] += sm[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+}  // namespace
+
+void box_dot(const double* g, const double* gp, const FastParams& fp, double* part, int nparts, cudaStream_t s) {
+    int64_t total = 1;
+    for (int t = 0; t < fp.d; ++t) total *= fp.box_w;
+    box_dot_k<<<nparts, 256, 0, s>>>(g, gp, fp.d, fp.ng, fp.box_lo, fp.box_w, total, part);
+    UOTK_LAUNCHED();
+}
+
 }  // namespace uotk

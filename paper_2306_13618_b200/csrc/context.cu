@@ -396,6 +396,7 @@ void get_fft_plans(int d, int n, cufftHandle* r2c, cufftHandle* c2r) {
         UOTK_CUFFT(cufftPlan3d(&b, n, n, n, CUFFT_Z2D));
     }
     c.fft[key] = {a, b};
+    trace_mark("full cuFFT plans created");
     *r2c = a;
     *c2r = b;
 }
@@ -420,6 +421,7 @@ void get_pruned_plans(int n, int w, int H, cufftHandle* pz, cufftHandle* py, cuf
         // z inverse (kernel-sum chain): C2R of the w * n rows back into the box slab
         UOTK_CUFFT(cufftPlanMany(&h[3], 1, &len, nullptr, 1, half, nullptr, 1, n, CUFFT_Z2D, w * n));
         it = c.pruned.emplace(key, h).first;
+        trace_mark("pruned cuFFT plans created");
     }
     *pz = it->second[0];
     *py = it->second[1];

@@ -353,6 +353,26 @@ void PlanData::note_use(cudaStream_t s) {
     cudaGetLastError();
 }
 
+// Separable Gaussian: D_k = prod_t d1(|k_t|) on k in [-N/2, N/2]^(d-1) x [0, N/2] (the same
+// values dk_kernel forms from the N^d samples' DFT: b_k factors over the axes)
+template <int D>
+__global__ void dk_separable_k(double* Dk, const double* __restrict__ d1, int N) {
+    const int nh = N / 2 + 1, nf = N + 1;
+    int64_t total = nh;
+    for (int t = 0; t < D - 1; ++t) total *= nf;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t rem = i;
+    double f = d1[rem % nh];
+    rem /= nh;
+    for (int t = D - 2; t >= 0; --t) {
+        const int k = (int)(rem % nf) - N / 2;
+        rem /= nf;
+        f *= d1[k < 0 ? -k : k];
+    }
+    Dk[i] = f;
+}
+
 PlanData::~PlanData() {
     // evicted tables may still be read by kernels queued on the streams that used them:
     // wait for those uses only (not the whole device: unrelated streams, NCCL's included,
@@ -422,6 +442,7 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
     } else {
         auto pd = std::make_shared<PlanData>();
         build_plan_data(*pd, fp, s);
+        trace_mark("plan: tables built");
         UOTK_CUDA(cudaEventCreateWithFlags(&pd->ready, cudaEventDisableTiming));
         UOTK_CUDA(cudaEventRecord(pd->ready, s));
         sp.pd = pd;
@@ -440,7 +461,15 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
 
 namespace {
 
+void build_plan_data_separable(PlanData& pd, const FastParams& fp, cudaStream_t s);
+std::vector<double> deconv_psi(const FastParams& fp);
+
 void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s) {
+    static const bool sep_env0 = [] {
+        const char* e = getenv("UOTK_SEPARABLE");
+        return !(e && e[0] == '0');
+    }();
+    if (fp.kind == UOTK_GAUSS && sep_env0) return build_plan_data_separable(pd, fp, s);
     const int d = fp.d, N = fp.N, ng = fp.ng;
     // 1) samples of K_R and their DFT -> b_k (real: K_R is real and even)
     size_t nsamp = 1;
@@ -472,18 +501,8 @@ void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s) {
     UOTK_CUFFT(cufftSetStream(r2c, s));
     UOTK_CUFFT(cufftExecD2Z(r2c, samp.p, (cufftDoubleComplex*)bspec.p));
 
-    // 2) per-axis deconvolution psi(k) = 1/(n_g^2 phihat(k)^2), k = 0..N/2, with the
-    //    Kaiser-Bessel pair  phi(v) = sinh(b sqrt(m^2 - v^2))/sqrt(m^2 - v^2) * m/sinh(b m)
-    //    (v in grid units) and phihat(k) = (pi m / n_g) I0(m sqrt(b^2 - (2 pi k/n_g)^2)) / sinh(b m).
-    std::vector<double> psi(N / 2 + 1);
-    const long double m = fp.m, b = fp.b;
-    const long double sinh_bm = sinhl(b * m);
-    for (int k = 0; k <= N / 2; ++k) {
-        long double w = 2.0L * M_PI * k / ng;
-        long double z = m * sqrtl(b * b - w * w);
-        long double ph = (long double)M_PI * m / ng * bessel_i0(z) / sinh_bm;
-        psi[k] = (double)(1.0L / ((long double)ng * ng * ph * ph));
-    }
+    // 2) per-axis deconvolution psi(k) = 1/(n_g^2 phihat(k)^2), k = 0..N/2 (deconv_psi)
+    const std::vector<double> psi = deconv_psi(fp);
     DevBuf<double> psi_d(psi.size(), s);
     UOTK_CUDA(cudaMemcpyAsync(psi_d.p, psi.data(), psi.size() * sizeof(double), cudaMemcpyHostToDevice, s));
 
@@ -498,40 +517,68 @@ void build_plan_data(PlanData& pd, const FastParams& fp, cudaStream_t s) {
     UOTK_LAUNCHED();
     // psi_d / samp / bspec are freed stream-ordered after the kernels that use them
 
-    // 4) Gaussian: the samples exp(-h^2 |j/N|^2 / eps) factor over the axes, hence so do b_k
-    //    and D_k = prod_t d1(k_t), d1(k) = psi(k) w(k) b1(k) / N (the same factors dk_kernel
-    //    multiplies).  The chain F^-1 (D .* F g) is then (Csep x ... x Csep) g with the real
-    //    symmetric circulant Csep[l][l'] = c(l - l'),  c(D) = d1(0) + 2 sum_{k=1}^{N/2} d1(k)
-    //    cos(2 pi k D / n_g)  (k = +-N/2 carry weight 1/2 each, as in the FFT path).
     pd.separable = false;
-    static const bool sep_env = [] {
-        const char* e = getenv("UOTK_SEPARABLE");
-        return !(e && e[0] == '0');
-    }();
-    if (fp.kind == UOTK_GAUSS && sep_env) {
-        std::vector<long double> d1(N / 2 + 1);
-        const long double h2e = (long double)fp.h * fp.h / fp.param;
-        for (int k = 0; k <= N / 2; ++k) {
-            long double b1 = 0;
-            for (int j = -N / 2; j < N / 2; ++j) {
-                const long double y = (long double)j / N;
-                b1 += expl(-h2e * y * y) * cosl(2.0L * M_PI * k * j / N);
-            }
-            d1[k] = (long double)psi[k] * (k == N / 2 ? 0.5L : 1.0L) * b1 / N;
-        }
-        std::vector<double> cvec(ng), C((size_t)ng * ng);
-        for (int D = 0; D < ng; ++D) {
-            long double c = d1[0];
-            for (int k = 1; k <= N / 2; ++k) c += 2.0L * d1[k] * cosl(2.0L * M_PI * k * D / ng);
-            cvec[D] = (double)c;
-        }
-        for (int l = 0; l < ng; ++l)
-            for (int lp = 0; lp < ng; ++lp) C[(size_t)l * ng + lp] = cvec[((l - lp) % ng + ng) % ng];
-        pd.Csep.alloc(C.size(), s);
-        UOTK_CUDA(cudaMemcpyAsync(pd.Csep.p, C.data(), C.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-        UOTK_CUDA(cudaStreamSynchronize(s));  // C lives on the host stack frame
-        pd.separable = true;
+}
+
+// Kaiser-Bessel pair  phi(v) = sinh(b sqrt(m^2 - v^2))/sqrt(m^2 - v^2) * m/sinh(b m) (v in grid
+// units) and phihat(k) = (pi m / n_g) I0(m sqrt(b^2 - (2 pi k/n_g)^2)) / sinh(b m):
+// psi(k) = 1/(n_g^2 phihat(k)^2), k = 0..N/2
+std::vector<double> deconv_psi(const FastParams& fp) {
+    const int N = fp.N, ng = fp.ng;
+    std::vector<double> psi(N / 2 + 1);
+    const long double m = fp.m, b = fp.b;
+    const long double sinh_bm = sinhl(b * m);
+    for (int k = 0; k <= N / 2; ++k) {
+        long double w = 2.0L * M_PI * k / ng;
+        long double z = m * sqrtl(b * b - w * w);
+        long double ph = (long double)M_PI * m / ng * bessel_i0(z) / sinh_bm;
+        psi[k] = (double)(1.0L / ((long double)ng * ng * ph * ph));
     }
+    return psi;
+}
+
+// The Gaussian's tables without the N^d samples and their DFT (no cuFFT plan): the samples
+// exp(-h^2 |j/N|^2 / eps) factor over the axes, hence so do b_k and D_k = prod_t d1(k_t),
+// d1(k) = psi(k) w(k) b1(k) / N with b1 the 1-D DFT of the samples (the same factors
+// dk_kernel multiplies).  The chain F^-1 (D .* F g) is then (Csep x ... x Csep) g with the
+// real symmetric circulant Csep[l][l'] = c(l - l'),  c(D) = d1(0) + 2 sum_{k=1}^{N/2} d1(k)
+// cos(2 pi k D / n_g)  (k = +-N/2 carry weight 1/2 each, as in the FFT path).
+void build_plan_data_separable(PlanData& pd, const FastParams& fp, cudaStream_t s) {
+    const int d = fp.d, N = fp.N, ng = fp.ng;
+    const std::vector<double> psi = deconv_psi(fp);
+    std::vector<long double> d1(N / 2 + 1);
+    const long double h2e = (long double)fp.h * fp.h / fp.param;
+    for (int k = 0; k <= N / 2; ++k) {
+        long double b1 = 0;
+        for (int j = -N / 2; j < N / 2; ++j) {
+            const long double y = (long double)j / N;
+            b1 += expl(-h2e * y * y) * cosl(2.0L * M_PI * k * j / N);
+        }
+        d1[k] = (long double)psi[k] * (k == N / 2 ? 0.5L : 1.0L) * b1 / N;
+    }
+    std::vector<double> d1d(N / 2 + 1), cvec(ng), C((size_t)ng * ng);
+    for (int k = 0; k <= N / 2; ++k) d1d[k] = (double)d1[k];
+    for (int D = 0; D < ng; ++D) {
+        long double c = d1[0];
+        for (int k = 1; k <= N / 2; ++k) c += 2.0L * d1[k] * cosl(2.0L * M_PI * k * D / ng);
+        cvec[D] = (double)c;
+    }
+    for (int l = 0; l < ng; ++l)
+        for (int lp = 0; lp < ng; ++lp) C[(size_t)l * ng + lp] = cvec[((l - lp) % ng + ng) % ng];
+    pd.Csep.alloc(C.size(), s);
+    UOTK_CUDA(cudaMemcpyAsync(pd.Csep.p, C.data(), C.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    DevBuf<double> d1_dev(d1d.size(), s);
+    UOTK_CUDA(cudaMemcpyAsync(d1_dev.p, d1d.data(), d1d.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    size_t ndk = (size_t)(N / 2 + 1);
+    for (int t = 0; t < d - 1; ++t) ndk *= (N + 1);
+    pd.Dk.alloc(ndk, s);
+    const int gb = (int)((ndk + 255) / 256);
+    if (d == 1) dk_separable_k<1><<<gb, 256, 0, s>>>(pd.Dk.p, d1_dev.p, N);
+    else if (d == 2) dk_separable_k<2><<<gb, 256, 0, s>>>(pd.Dk.p, d1_dev.p, N);
+    else dk_separable_k<3><<<gb, 256, 0, s>>>(pd.Dk.p, d1_dev.p, N);
+    UOTK_LAUNCHED();
+    UOTK_CUDA(cudaStreamSynchronize(s));  // C, d1d live on the host stack frame
+    pd.separable = true;
 }
 
 }  // namespace
