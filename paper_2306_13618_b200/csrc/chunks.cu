@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(kWinWarps * 32)
 chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u, const int32_t* __restrict__ key,
                     int64_t n, int64_t nchunks, KBHorner hc, double* __restrict__ out) {
     __shared__ double stage[kWinWarps][kChunk * kMaxRow];
-    constexpr int kW = D == 3 ? chunk_win3_doubles(KZ) : chunk_win_doubles(D);
+    constexpr int kW = D == 3 ? chunk_win3_doubles(KZ) : (D == 2 ? chunk_win2_doubles(KZ) : chunk_win_doubles(D));
+    constexpr bool YSEG = D == 2 && KZ == 24;  // d = 2 y-segment rows (chunks.cuh)
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t job = blockIdx.x * (int64_t)kWinWarps + warp;  // (chunk, axis)
@@ -59,7 +60,8 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
     const int ax = (int)(job - c * D);
     const int4 dsc = desc[c];
     // row stride and offset of this axis' matrix inside the chunk block
-    const int stride = D == 3 ? (ax == 2 ? chunk_zstride3(KZ) : chunk_xstride3(KZ)) : kChunkT;
+    const int stride = D == 3 ? (ax == 2 ? chunk_zstride3(KZ) : chunk_xstride3(KZ))
+                              : (D == 2 && ax == 1 ? chunk_ystride2(KZ) : kChunkT);
     const int64_t base = c * kW + (int64_t)ax * kChunk * (D == 3 ? chunk_xstride3(KZ) : kChunkT);
     double* st = stage[warp];
     const int p = lane;
@@ -70,6 +72,7 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
         const double ut = u[ax * n + dsc.x + p];
         f = ut - floor(ut);
         if (D == 3 && ax == 2 && (KZ == 24 || KZ == 40)) off = key[dsc.x + p] - dsc.z;
+        if (YSEG && ax == 1) off = key[dsc.x + p] - dsc.z;
     }
     // the row: zeros (empty slots, padding columns), then the 2m taps of a live point,
     // each a degree-14 polynomial in f - 1/2 (window_fit.h)
@@ -82,7 +85,7 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
             double v = hc.c[a][kHornerDeg];
 #pragma unroll
             for (int j = kHornerDeg - 1; j >= 0; --j) v = fma(v, t, hc.c[a][j]);
-            st[p * stride + (D == 2 ? swz2(p, a) : a + off)] = v;
+            st[p * stride + ((D == 2 && !(YSEG && ax == 1)) ? swz2(p, a) : a + off)] = v;
         }
     }
     __syncwarp();
@@ -217,6 +220,26 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
         }
         trace_mark("chunks: z-segments");
     }
+    // d = 2 sparse clouds: y-segments of kSegY cells (one 16 x 24 footprint) when that needs
+    // sufficiently fewer chunks; the footprint flushes (fp64 RED) bind those sets
+    static const bool yseg_env = [] {
+        const char* e = getenv("UOTK_YSEG");
+        return !(e && e[0] == '0');
+    }();
+    if (d == 2 && fp.m == kChunkM && yseg_env && (double)n < 0.5 * kChunk * (double)nchunks) {
+        gk.alloc(n, s);
+        segment_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, ps.n, fp.ng, kSegY, gk.p);
+        UOTK_LAUNCHED();
+        const int64_t nseg = encode(gk.p);
+        if (1.5 * (double)nseg < (double)nchunks) {
+            kz = 24;
+            chunk_cost = 1.5;
+            nchunks = nseg;
+        } else {
+            nchunks = encode(ps.key.p);  // back to one-cell groups
+        }
+        trace_mark("chunks: y-segments");
+    }
     // minimum mean fill of the 32-slot chunks (per unit of chunk cost): below it the padded
     // GEMM work and the per-group footprint flush cost more than the generic kernels'
     // per-tap atomics (d = 3: ~3 points per chunk, measured on C5/C2 clouds; d = 2: ~2;
@@ -225,7 +248,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     if (!forced && (double)n < min_fill * chunk_cost * kChunk * (double)nchunks) return;
     // a gather-only set this sparse is gathered by the generic kernel anyway (nfft.cu)
     if (!forced && use == kUseGatherOnly && d == 3 && (double)n < kGatherMinFill3 * kChunk * (double)nchunks) return;
-    const int wd = d == 3 ? chunk_win3_doubles(kz) : chunk_win_doubles(d);
+    const int wd = d == 3 ? chunk_win3_doubles(kz) : (d == 2 ? chunk_win2_doubles(kz) : chunk_win_doubles(d));
     // spread-only d = 3 one-cell sets: the spread evaluates the windows itself
     static const bool fly_env = [] {
         const char* e = getenv("UOTK_SPREAD_FLY");
@@ -312,6 +335,9 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
                                                                       win, ps.chunk_win.p);
         else if (d == 3)
             chunk_window_rows_k<3, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
+                                                                      win, ps.chunk_win.p);
+        else if (d == 2 && kz == 24)
+            chunk_window_rows_k<2, 24><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,
                                                                       win, ps.chunk_win.p);
         else if (d == 2)
             chunk_window_rows_k<2, 16><<<wb, kWinWarps * 32, 0, s>>>(ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, nchunks,

@@ -54,6 +54,14 @@ __host__ __device__ constexpr int chunk_win_doubles(int d) {
     return d == 3 ? chunk_win3_doubles(16) : d * kChunk * kChunkT;
 }
 
+// d = 2 y-segments (sparse clouds, e.g. C4's literal 4096^2 grid at ~5 points per cell):
+// kSegY cells along y share one 16 x 24 footprint; X rows as for one cell (16 swizzled
+// taps), Y rows 24 columns wide at stride 28 (conflict-free fragments), the 16 taps at the
+// point's cell offset in the segment
+constexpr int kSegY = 9;
+__host__ __device__ constexpr int chunk_ystride2(int ky) { return ky == 16 ? kChunkT : 28; }
+__host__ __device__ constexpr int chunk_win2_doubles(int ky) { return kChunk * (kChunkT + chunk_ystride2(ky)); }
+
 // d = 3 stand-alone gathers on sets whose chunks are filled below this fraction use the
 // generic per-point kernel (its per-point loads beat the padded GEMMs there; nfft.cu), and
 // gather-only sets that sparse get no chunk list at all (chunks.cu)

@@ -43,15 +43,30 @@ void fused3d_gather_spread(const PointSet& ps, const double* grid_in, double* gr
 namespace {
 
 constexpr int kM = kChunkM;
-constexpr int kW2 = chunk_win_doubles(2);  // 1024 doubles = 8 KB per chunk
-constexpr uint32_t kW2Bytes = kW2 * sizeof(double);
+// d = 2 window blocks: X [slot 32][16 taps, swizzled], then Y: one-cell groups (KY = 16)
+// [slot 32][16 taps, swizzled]; y-segment groups of sparse clouds (KY = 24: kSegY cells
+// along y share one 16 x 24 footprint) [slot 32][24 columns, stride 28], the 16 taps at
+// the point's cell offset in the segment (chunks.cuh)
+template <int KY>
+struct Lay2 {
+    static constexpr int NT = KY / 8;                           // 8-wide column tiles along y
+    static constexpr int YS = KY == 16 ? kChunkT : chunk_ystride2(KY);
+    static constexpr int W = chunk_win2_doubles(KY);            // doubles per chunk block
+    static constexpr uint32_t Bytes = W * sizeof(double);
+    // column c of slot p's Y row
+    __device__ static __forceinline__ int y(int p, int c) { return KY == 16 ? p * kChunkT + swz2(p, c) : p * YS + c; }
+};
 constexpr int kW1 = chunk_win_doubles(1);  // 512 doubles per chunk
-constexpr int kRing2 = 3;  // window blocks in flight per warp
+template <int KY>
+struct Ring2 {
+    static constexpr int N = KY == 16 ? 3 : 2;  // window blocks in flight per warp (3 CTAs per SM)
+};
 
+template <int KY>
 struct __align__(128) Smem2 {
-    double win[kWarps2][kRing2][kW2];  // per-warp TMA ring of window blocks
-    double red[kWarps2][kChunk];       // per-warp gathered t of the current chunk
-    unsigned long long bar[kWarps2][kRing2];
+    double win[kWarps2][Ring2<KY>::N][Lay2<KY>::W];  // per-warp TMA ring of window blocks
+    double red[kWarps2][kChunk];                       // per-warp gathered t of the current chunk
+    unsigned long long bar[kWarps2][Ring2<KY>::N];
 };
 
 // chunk descriptors of a warp's range, batched: lane L holds the descriptor of chunk
@@ -91,7 +106,7 @@ struct DescBatch {
 };
 
 // MODE: 0 = gather -> epilogue -> spread (Sinkhorn half-step), 1 = spread only, 2 = gather only
-template <int MODE, class Epi>
+template <int MODE, class Epi, int KY>
 __global__ void __launch_bounds__(kWarps2 * 32, kCtas2)
 chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
             int nunits, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
@@ -100,7 +115,10 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     constexpr bool SPREAD = MODE != 2;
     using In = typename Epi::In;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem2& sm = *reinterpret_cast<Smem2*>(smem_raw);
+    using L = Lay2<KY>;
+    constexpr int NT = L::NT;
+    constexpr int R = Ring2<KY>::N;
+    Smem2<KY>& sm = *reinterpret_cast<Smem2<KY>*>(smem_raw);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int gq = lane >> 2;  // fragment group: row of A / D, column of B
@@ -113,21 +131,21 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     double* swin = &sm.win[warp][0][0];
     unsigned long long* bar = sm.bar[warp];
     if (lane == 0) {
-        for (int r = 0; r < kRing2; ++r) mbar_init(&bar[r], 1);
+        for (int r = 0; r < R; ++r) mbar_init(&bar[r], 1);
         mbar_init_fence();
     }
     __syncwarp();
     if (lane == 0) {
-        for (int k = 0; k < kRing2 && k < nck; ++k) {
-            mbar_expect_tx(&bar[k], kW2Bytes);
-            bulk_g2s(swin + k * kW2, win + (cbeg + k) * kW2, kW2Bytes, &bar[k]);
+        for (int k = 0; k < R && k < nck; ++k) {
+            mbar_expect_tx(&bar[k], L::Bytes);
+            bulk_g2s(swin + k * L::W, win + (cbeg + k) * L::W, L::Bytes, &bar[k]);
         }
     }
     DescBatch db;
     db.init(desc, cbeg, cbeg + nck, lane);
 
-    double Fb[2][4];     // Fb[nt][ks] = F[4ks + tq][8nt + gq]          (gather B operand)
-    double S[2][2][2];   // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]  (spread accumulators)
+    double Fb[NT][4];     // Fb[nt][ks] = F[4ks + tq][8nt + gq]          (gather B operand)
+    double S[2][NT][2];   // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]  (spread accumulators)
     int32_t cur_key = -1;
     int64_t org = 0;  // grid index of footprint (0, 0) of the current group
     double ddmax = 0.0;
@@ -137,7 +155,7 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
         for (int mt = 0; mt < 2; ++mt) {
             double* row = grid_out + org + (int64_t)(8 * mt + gq) * ng + 2 * tq;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
+            for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
                     if (S[mt][nt][i] != 0.0) atomicAdd(row + 8 * nt + i, S[mt][nt][i]);
@@ -151,7 +169,7 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
     if (!GATHER && lane < dsc.y) w_cur = w_in[dsc.x + lane];
     for (int64_t k = 0; k < nck; ++k) {
         const int64_t c = cbeg + k;
-        const int slot = (int)(k % kRing2);
+        const int slot = (int)(k % R);
         const int64_t p0 = dsc.x;
         const int cnt = dsc.y;
         // next chunk's descriptor and per-point inputs, in flight during this chunk
@@ -170,23 +188,23 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double* row = grid_in + org + (int64_t)(4 * ks + tq) * ng + gq;
-                    Fb[0][ks] = __ldg(row);
-                    Fb[1][ks] = __ldg(row + 8);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) Fb[nt][ks] = __ldg(row + 8 * nt);
                 }
             }
             if (SPREAD) {
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
+                    for (int nt = 0; nt < NT; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
         }
         if (GATHER && k + 1 < nck && dnext.z != cur_key && lane < 16) {
             // warm L1 with the next group's footprint rows
             asm volatile("prefetch.global.L1 [%0];" ::"l"(grid_in + origin(dnext.z) + (int64_t)lane * ng));
         }
-        mbar_wait(&bar[slot], (uint32_t)((k / kRing2) & 1));
-        const double* X = swin + slot * kW2;
+        mbar_wait(&bar[slot], (uint32_t)((k / R) & 1));
+        const double* X = swin + slot * L::W;
         const double* Y = X + kChunk * kChunkT;
 
         double wn = 0.0;  // spread weight of slot `lane`
@@ -195,19 +213,20 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
             for (int mt = 0; mt < 4; ++mt) {
                 const int p = 8 * mt + gq;
                 const double* xr = X + p * kChunkT;
-                const double* yr = Y + p * kChunkT;
-                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                double acc[NT][2];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double a = xr[swz2(p, 4 * ks + tq)];
-                    dmma(acc[0][0], acc[0][1], a, Fb[0][ks]);
-                    dmma(acc[1][0], acc[1][1], a, Fb[1][ks]);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a, Fb[nt][ks]);
                 }
                 // acc[nt][i] = G[p][8nt + 2tq + i]
                 double part = 0.0;
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    const double2 y = *reinterpret_cast<const double2*>(yr + swz2(p, 8 * nt + 2 * tq));
+                for (int nt = 0; nt < NT; ++nt) {
+                    const double2 y = *reinterpret_cast<const double2*>(Y + L::y(p, 8 * nt + 2 * tq));
                     part = fma(acc[nt][0], y.x, part);
                     part = fma(acc[nt][1], y.y, part);
                 }
@@ -228,22 +247,21 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
                 const int p = 4 * ks + tq;
                 const double wp = __shfl_sync(0xffffffffu, wn, p);
                 const double* xr = X + p * kChunkT;
-                const double* yr = Y + p * kChunkT;
                 const double xa0 = wp * xr[swz2(p, gq)];
                 const double xa1 = wp * xr[swz2(p, 8 + gq)];
-                const double yb0 = yr[swz2(p, gq)];
-                const double yb1 = yr[swz2(p, 8 + gq)];
-                dmma(S[0][0][0], S[0][0][1], xa0, yb0);
-                dmma(S[0][1][0], S[0][1][1], xa0, yb1);
-                dmma(S[1][0][0], S[1][0][1], xa1, yb0);
-                dmma(S[1][1][0], S[1][1][1], xa1, yb1);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const double yb = Y[L::y(p, 8 * nt + gq)];
+                    dmma(S[0][nt][0], S[0][nt][1], xa0, yb);
+                    dmma(S[1][nt][0], S[1][nt][1], xa1, yb);
+                }
             }
         }
         __syncwarp();  // the warp is done with window slot `slot` and red
-        if (lane == 0 && k + kRing2 < nck) {
+        if (lane == 0 && k + R < nck) {
             fence_proxy_async();
-            mbar_expect_tx(&bar[slot], kW2Bytes);
-            bulk_g2s(swin + slot * kW2, win + (c + kRing2) * kW2, kW2Bytes, &bar[slot]);
+            mbar_expect_tx(&bar[slot], L::Bytes);
+            bulk_g2s(swin + slot * L::W, win + (c + R) * L::W, L::Bytes, &bar[slot]);
         }
         if (k + 1 < nck) dsc = db.get(k + 1, lane);
         in_cur = in_next;
@@ -261,22 +279,30 @@ chunked2d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 // spread side (the update's log/exp), hence two G warps per S warp.  The window ring
 // (TMA, refilled by S when it releases a slot) and the weight hand-offs are per-unit
 // mbarriers: the units of a CTA never synchronise after the start.
-constexpr int kRingWS2 = 5;
+template <int KY>
+struct RingWS2 {
+    static constexpr int N = KY == 16 ? 5 : 4;  // 2 CTAs per SM: 2 x 2 units x N x (8 | 11) KB
+};
+template <int KY>
 struct __align__(128) Smem2WS {
-    double win[kUnitsWS2][kRingWS2][kW2];
+    double win[kUnitsWS2][RingWS2<KY>::N][Lay2<KY>::W];
     double w[kUnitsWS2][2][kChunk];  // published weights of the even / odd chunk
-    unsigned long long win_full[kUnitsWS2][kRingWS2];
+    unsigned long long win_full[kUnitsWS2][RingWS2<KY>::N];
     unsigned long long w_full[kUnitsWS2][2];
     unsigned long long w_empty[kUnitsWS2][2];
 };
 
+template <int KY>
 __global__ void __launch_bounds__(3 * kUnitsWS2 * 32, kCtasWS2)
 sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, const int32_t* __restrict__ bounds,
                 int nunits, int ng, const double* __restrict__ grid_in, double* __restrict__ grid_out,
                 EpiSinkhorn epi, unsigned long long* dmax) {
     using In = EpiSinkhorn::In;
+    using L = Lay2<KY>;
+    constexpr int NT = L::NT;
+    constexpr int kRingWS2 = RingWS2<KY>::N;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem2WS& sm = *reinterpret_cast<Smem2WS*>(smem_raw);
+    Smem2WS<KY>& sm = *reinterpret_cast<Smem2WS<KY>*>(smem_raw);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int u = warp / 3;     // unit within the CTA
@@ -303,14 +329,14 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     if (nck <= 0) return;
     if (role == 2 && lane == 0) {
         for (int k = 0; k < kRingWS2 && k < nck; ++k) {
-            mbar_expect_tx(&win_full[k], kW2Bytes);
-            bulk_g2s(swin + k * kW2, win + (cbeg + k) * kW2, kW2Bytes, &win_full[k]);
+            mbar_expect_tx(&win_full[k], L::Bytes);
+            bulk_g2s(swin + k * L::W, win + (cbeg + k) * L::W, L::Bytes, &win_full[k]);
         }
     }
     auto origin = [&](int32_t kk) -> int64_t { return (int64_t)(kk / ng - kM + 1) * ng + (kk % ng - kM + 1); };
 
     if (role < 2) {
-        double Fb[2][4];  // Fb[nt][ks] = F[4ks + tq][8nt + gq]
+        double Fb[NT][4];  // Fb[nt][ks] = F[4ks + tq][8nt + gq]
         int32_t cur_key = -1;
         double ddmax = 0.0;
         int64_t k = role;
@@ -331,30 +357,31 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double* row = grid_in + org + (int64_t)(4 * ks + tq) * ng + gq;
-                    Fb[0][ks] = __ldg(row);
-                    Fb[1][ks] = __ldg(row + 8);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) Fb[nt][ks] = __ldg(row + 8 * nt);
                 }
             }
             mbar_wait(&win_full[slot], (uint32_t)((k / kRingWS2) & 1));
-            const double* X = swin + slot * kW2;
+            const double* X = swin + slot * L::W;
             const double* Y = X + kChunk * kChunkT;
             double t = 0.0;  // t of slot `lane`, assembled from the 4 m-tiles
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int p = 8 * mt + gq;
                 const double* xr = X + p * kChunkT;
-                const double* yr = Y + p * kChunkT;
-                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                double acc[NT][2];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const double a = xr[swz2(p, 4 * ks + tq)];
-                    dmma(acc[0][0], acc[0][1], a, Fb[0][ks]);
-                    dmma(acc[1][0], acc[1][1], a, Fb[1][ks]);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a, Fb[nt][ks]);
                 }
                 double part = 0.0;
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    const double2 y = *reinterpret_cast<const double2*>(yr + swz2(p, 8 * nt + 2 * tq));
+                for (int nt = 0; nt < NT; ++nt) {
+                    const double2 y = *reinterpret_cast<const double2*>(Y + L::y(p, 8 * nt + 2 * tq));
                     part = fma(acc[nt][0], y.x, part);
                     part = fma(acc[nt][1], y.y, part);
                 }
@@ -381,7 +408,7 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
         }
         warp_max_atomic(dmax, ddmax);
     } else {
-        double S[2][2][2];  // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]
+        double S[2][NT][2];  // S[mt][nt][i] = S[8mt + gq][8nt + 2tq + i]
         int32_t cur_key = -1;
         int64_t org = 0;
         auto flush = [&]() {
@@ -389,7 +416,7 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             for (int mt = 0; mt < 2; ++mt) {
                 double* row = grid_out + org + (int64_t)(8 * mt + gq) * ng + 2 * tq;
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
+                for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
                         if (S[mt][nt][i] != 0.0) atomicAdd(row + 8 * nt + i, S[mt][nt][i]);
@@ -409,11 +436,11 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
+                    for (int nt = 0; nt < NT; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
             mbar_wait(&w_full[b], (uint32_t)((k >> 1) & 1));
             mbar_wait(&win_full[slot], (uint32_t)((k / kRingWS2) & 1));
-            const double* X = swin + slot * kW2;
+            const double* X = swin + slot * L::W;
             const double* Y = X + kChunk * kChunkT;
             const double wl = sm.w[u][b][lane];
 #pragma unroll
@@ -421,23 +448,22 @@ sinkhorn2d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 const int p = 4 * ks + tq;
                 const double wp = __shfl_sync(0xffffffffu, wl, p);
                 const double* xr = X + p * kChunkT;
-                const double* yr = Y + p * kChunkT;
                 const double xa0 = wp * xr[swz2(p, gq)];
                 const double xa1 = wp * xr[swz2(p, 8 + gq)];
-                const double yb0 = yr[swz2(p, gq)];
-                const double yb1 = yr[swz2(p, 8 + gq)];
-                dmma(S[0][0][0], S[0][0][1], xa0, yb0);
-                dmma(S[0][1][0], S[0][1][1], xa0, yb1);
-                dmma(S[1][0][0], S[1][0][1], xa1, yb0);
-                dmma(S[1][1][0], S[1][1][1], xa1, yb1);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const double yb = Y[L::y(p, 8 * nt + gq)];
+                    dmma(S[0][nt][0], S[0][nt][1], xa0, yb);
+                    dmma(S[1][nt][0], S[1][nt][1], xa1, yb);
+                }
             }
             __syncwarp();  // S is done with window slot `slot` and w[b]
             if (lane == 0) {
                 mbar_arrive(&w_empty[b]);
                 if (k + kRingWS2 < nck) {
                     fence_proxy_async();
-                    mbar_expect_tx(&win_full[slot], kW2Bytes);
-                    bulk_g2s(swin + slot * kW2, win + (c + kRingWS2) * kW2, kW2Bytes, &win_full[slot]);
+                    mbar_expect_tx(&win_full[slot], L::Bytes);
+                    bulk_g2s(swin + slot * L::W, win + (c + kRingWS2) * L::W, L::Bytes, &win_full[slot]);
                 }
             }
         }
@@ -546,10 +572,16 @@ void launch12(const PointSet& ps, const double* gin, double* gout, const double*
     const int nunits = ps.chunk_blocks;
     ProfScope prof(tag, s);
     if (fp.d == 2) {
-        set_smem_attr((const void*)chunked2d_k<MODE, Epi>, (int)sizeof(Smem2));
         const int blocks = (nunits + kWarps2 - 1) / kWarps2;
-        chunked2d_k<MODE, Epi><<<blocks, kWarps2 * 32, sizeof(Smem2), s>>>(
-            ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, gin, gout, w, epi, dmax);
+        if (ps.chunk_kz == 24) {
+            set_smem_attr((const void*)chunked2d_k<MODE, Epi, 24>, (int)sizeof(Smem2<24>));
+            chunked2d_k<MODE, Epi, 24><<<blocks, kWarps2 * 32, sizeof(Smem2<24>), s>>>(
+                ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, gin, gout, w, epi, dmax);
+        } else {
+            set_smem_attr((const void*)chunked2d_k<MODE, Epi, 16>, (int)sizeof(Smem2<16>));
+            chunked2d_k<MODE, Epi, 16><<<blocks, kWarps2 * 32, sizeof(Smem2<16>), s>>>(
+                ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p, nunits, fp.ng, gin, gout, w, epi, dmax);
+        }
     } else {
         const int blocks = (nunits + kWarps1 - 1) / kWarps1;
         chunked1d_k<MODE, Epi><<<blocks, kWarps1 * 32, 0, s>>>(ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds.p,
@@ -593,12 +625,18 @@ void chunked_gather_spread(const PointSet& ps, const double* grid_in, double* gr
     }();
     if (fp.d == 2 && ws) {
         if (ps.n == 0 || ps.nchunks == 0) return;
-        set_smem_attr((const void*)sinkhorn2d_ws_k, (int)sizeof(Smem2WS));
         const int nunits = ps.chunk_units_ws;
         const int blocks = (nunits + kUnitsWS2 - 1) / kUnitsWS2;
         ProfScope prof(kProfFused, s);
-        sinkhorn2d_ws_k<<<blocks, 3 * kUnitsWS2 * 32, sizeof(Smem2WS), s>>>(
-            ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds_ws.p, nunits, fp.ng, grid_in, grid_out, epi, dmax);
+        if (ps.chunk_kz == 24) {
+            set_smem_attr((const void*)sinkhorn2d_ws_k<24>, (int)sizeof(Smem2WS<24>));
+            sinkhorn2d_ws_k<24><<<blocks, 3 * kUnitsWS2 * 32, sizeof(Smem2WS<24>), s>>>(
+                ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds_ws.p, nunits, fp.ng, grid_in, grid_out, epi, dmax);
+        } else {
+            set_smem_attr((const void*)sinkhorn2d_ws_k<16>, (int)sizeof(Smem2WS<16>));
+            sinkhorn2d_ws_k<16><<<blocks, 3 * kUnitsWS2 * 32, sizeof(Smem2WS<16>), s>>>(
+                ps.chunk_desc.p, ps.chunk_win.p, ps.chunk_bounds_ws.p, nunits, fp.ng, grid_in, grid_out, epi, dmax);
+        }
         UOTK_LAUNCHED();
         return;
     }

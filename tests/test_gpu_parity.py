@@ -401,7 +401,8 @@ def test_uot_c4_full_size_grid4096_sampled(uk):
     pr = W.c4_uot(iters=3)
     beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam,
                                        iters=pr.iters, opts={"method": "nfft", "N": 2048})
-    assert res.info["n_grid"] == 4096 and res.info["groups"] == (16, 16), res.info
+    # ~5 points per cell at 4096^2: y-segment groups (9 cells along y, 16 x 24 footprints)
+    assert res.info["n_grid"] == 4096 and res.info["groups"] == (24, 24), res.info
     b = beta.cpu().numpy()
     g = gamma.cpu().numpy()
     lam = 1.0 / pr.eps
@@ -797,3 +798,28 @@ def test_spread_only_windows_on_the_fly(uk, kind):
     mref = oracle.mmd2_direct(pr.x, pr.a, pr.y[:2500], pr.b[:2500], kind, param)
     denom = max(abs(mref), 1e-3 * _mmd_tol(pr.x, pr.a, pr.y[:2500], pr.b[:2500], kind, param))
     assert abs(v - mref) / denom <= 1e-8, (v, mref, minfo)
+
+
+@pytest.mark.parametrize("n,m", [(500, 450), (1201, 999)])
+def test_uot_d2_y_segments(uk, n, m):
+    """d = 2 clouds of a few points per cell take y-segment groups (kSegY cells along y share
+    one 16 x 24 footprint; the y-windows sit at the cell's offset in the segment) in the
+    warp-specialised half-step: against the oracle element by element."""
+    pr = W.c1_uot(n=n, m=m)
+    ref = oracle.uot_sinkhorn_direct(pr.x, pr.a, pr.y, pr.b, pr.eps, pr.lam, pr.lam, 12)
+    beta, gamma, res = uk.uot_sinkhorn(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), pr.eps, pr.lam, iters=12,
+                                       opts={"method": "nfft"})
+    assert res.info["groups"] == (24, 24), res.info
+    _uot_check(res, beta.cpu().numpy(), gamma.cpu().numpy(), ref, pr.eps, pr.lam)
+
+
+@pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
+def test_kernel_sum_d2_y_segments(uk, kind):
+    """Stand-alone d = 2 spread and gather on y-segment groups (forced cell-group kernels)."""
+    n = 3001 if kind == W.GAUSS else 30001  # ~1 point per cell (the IMQ's grid is 512^2)
+    pr = W.random_sum(2, n, 2003, kind=kind, param=(0.0025 if kind == W.GAUSS else 0.05), seed=77, signed=True)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    got, info = uk.kernel_sum(cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt), kind, pr.param,
+                              opts={"method": "nfft", "flags": uk.FLAG_CHUNKED}, return_info=True)
+    assert info["groups"][0] == 24, info
+    assert rel_err(got.cpu().numpy(), ref, True) <= 1e-9
