@@ -7,11 +7,15 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 h = [i for i, r in enumerate(rows) if "Source" in r and "Address" in r][0]
 hdr = rows[h]
+# newer ncu: one section per profiled launch ("Kernel Name" row, header row, instructions);
+# keep the first launch's instructions only
+end = next((i for i in range(h + 1, len(rows)) if rows[i] and rows[i][0] == "Kernel Name"), len(rows))
+rows = rows[:end]
 si = hdr.index("Source"); wi = hdr.index("Warp Stall Sampling (All Samples)")
 stall_cols = [i for i, c in enumerate(hdr) if c.startswith("stall_") and "Not Issued" not in c]
 ins = []
 for r in rows[h+1:]:
-    if len(r) <= wi: break
+    if len(r) <= max(stall_cols + [wi]): continue
     try: ins.append((r[si].strip(), int(r[wi] or 0), [int(r[i] or 0) for i in stall_cols], int(r[hdr.index("Instructions Executed")] or 0)))
     except ValueError: pass
 tot = sum(x[1] for x in ins)
