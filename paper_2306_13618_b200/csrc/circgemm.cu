@@ -179,6 +179,43 @@ void gemm(int M, int N, int K, const double* A, int64_t lda, int64_t sA, const d
 }  // namespace
 
 void comm_allreduce(double* buf, size_t count, int op_max_min_sum, void* comm, cudaStream_t s);  // comm.cu
+void comm_reduce_scatter(const double* in, double* out, size_t count, void* comm, cudaStream_t s);
+void comm_all_gather(const double* in, double* out, size_t count, void* comm, cudaStream_t s);
+int comm_nranks(void* comm);
+int comm_rank(void* comm);
+
+namespace {
+// d = 2, distributed pass: spare[(o + x) n + o + y] = all[(y / wb) w wb + x wb + y % wb]
+__global__ void unpack_cols_k(const double* __restrict__ all, int w, int wb, int n, int o,
+                              double* __restrict__ spare) {
+    const int64_t total = (int64_t)w * w;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(i / w), y = (int)(i % w);
+        spare[(int64_t)(o + x) * n + o + y] = all[(int64_t)(y / wb) * w * wb + (int64_t)x * wb + y % wb];
+    }
+}
+}  // namespace
+
+// doubles of the chain's work buffer for a (P-rank) chain
+size_t separable_work_elems(const FastParams& fp, int P) {
+    const size_t w = fp.box_w;
+    if (fp.d == 1) return w;
+    if (P <= 1) return fp.d == 2 ? w * w : w * w * w;
+    if (fp.d == 2) {
+        const size_t wb = (w + P - 1) / P;
+        return (2 * (size_t)P + 2) * w * wb;
+    }
+    const size_t xb = (w + P - 1) / P;
+    return ((size_t)P + 2) * xb * w * w;
+}
+
+static bool dist_chain_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("UOTK_DIST_CHAIN");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 // g' = (Csep x ... x Csep) g on the footprint box (spread grid g: zero outside the box).
 // Returns the buffer holding g' at the box positions (`spare`, n_g^d doubles).  `work`
@@ -204,6 +241,53 @@ double* separable_chain_dmma(const FastParams& fp, const double* Csep, double* g
     if (d == 1) {  // out[z] = sum_z' C[z][z'] g[z']   (N = 1 column)
         gemm(w, 1, w, Cb, n, 0, grid + o, 1, 0, spare + o, 1, 0, 1, s, z);
         if (comm) comm_allreduce(spare + o, (size_t)w, 0, comm, s);
+        return spare;
+    }
+    const int P = comm_nranks(comm);
+    if (d == 2 && P > 1 && dist_chain_enabled()) {
+        // slab-distributed: the y-pass of each rank's own spread, written as
+        // P column blocks of width wb; a reduce-scatter gives rank r the global block r; the
+        // x-pass of that block only (1/P of the work); an all-gather of the output blocks
+        const int r = comm_rank(comm);
+        const int wb = (w + P - 1) / P;
+        const int64_t blk = (int64_t)w * wb;
+        double* t1 = work;                 // P x (w x wb)
+        double* t1r = t1 + P * blk;        // w x wb
+        double* orr = t1r + blk;           // w x wb
+        double* oall = orr + blk;          // P x (w x wb)
+        UOTK_CUDA(cudaMemsetAsync(t1, 0, P * blk * sizeof(double), s));
+        for (int b = 0; b < P; ++b) {
+            const int nb = std::min(wb, w - b * wb);
+            if (nb > 0) gemm(w, nb, w, grid + (int64_t)o * n + o, n, 0, Cb + b * wb, n, 0, t1 + b * blk, wb, 0, 1, s);
+        }
+        comm_reduce_scatter(t1, t1r, (size_t)blk, comm, s);
+        const int nr = std::min(wb, w - r * wb);
+        if (nr > 0) gemm(w, nr, w, Cb, n, 0, t1r, wb, 0, orr, wb, 0, 1, s, z);
+        else if (zero_next) gemm(1, 1, 1, Cb, n, 0, Cb, n, 0, orr, wb, 0, 1, s, z);  // the side job alone
+        comm_all_gather(orr, oall, (size_t)blk, comm, s);
+        unpack_cols_k<<<(int)std::min<int64_t>(1184, ((int64_t)w * w + 255) / 256), 256, 0, s>>>(oall, w, wb, n, o,
+                                                                                               spare);
+        UOTK_LAUNCHED();
+        return spare;
+    }
+    if (d == 3 && P > 1 && dist_chain_enabled() && (int64_t)P * ((w + P - 1) / P) * w2 <= n2 * n) {
+        // slab-distributed: the z-pass of each rank's own spread (all x-planes), a
+        // reduce-scatter of x-plane blocks, the y-pass of rank r's planes only, an all-gather
+        // of those planes, the x-pass (replicated).  T1 (P xb planes) sits compact in spare (its
+        // capacity is >= n^3 doubles, checked above)
+        const int r = comm_rank(comm);
+        const int xb = (w + P - 1) / P;
+        const int64_t blk = (int64_t)xb * w2;
+        double* t1r = work;               // xb planes
+        double* t2r = t1r + blk;          // xb planes
+        double* t2 = t2r + blk;           // P xb planes
+        if ((int64_t)P * xb > w) UOTK_CUDA(cudaMemsetAsync(spare + w * w2, 0, ((int64_t)P * xb - w) * w2 * sizeof(double), s));
+        gemm(w, w, w, grid + o * n2 + (int64_t)o * n + o, n, n2, Cb, n, 0, spare, w, w2, w, s);
+        comm_reduce_scatter(spare, t1r, (size_t)blk, comm, s);
+        const int nx = std::max(0, std::min(xb, w - r * xb));
+        if (nx > 0) gemm(w, w, w, Cb, n, 0, t1r, w, w2, t2r, w, w2, nx, s);
+        comm_all_gather(t2r, t2, (size_t)blk, comm, s);
+        gemm(w, w, w, Cb, n, 0, t2, w2, w, spare + o * n2 + (int64_t)o * n + o, n2, n, w, s, z);
         return spare;
     }
     if (d == 2) {

@@ -34,6 +34,9 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     ncclResult_t (*GetVersion)(int*) = nullptr;
 };
@@ -52,10 +55,12 @@ NcclApi& nccl() {
         api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.lib, "ncclCommInitRank");
         api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.lib, "ncclCommDestroy");
         api.AllReduce = (decltype(api.AllReduce))dlsym(api.lib, "ncclAllReduce");
+        api.ReduceScatter = (decltype(api.ReduceScatter))dlsym(api.lib, "ncclReduceScatter");
+        api.AllGather = (decltype(api.AllGather))dlsym(api.lib, "ncclAllGather");
         api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.lib, "ncclGetErrorString");
         api.GetVersion = (decltype(api.GetVersion))dlsym(api.lib, "ncclGetVersion");
     });
-    if (!api.lib || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce)
+    if (!api.lib || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.ReduceScatter || !api.AllGather)
         fail(UOTK_ENCCL, "NCCL (libnccl.so.2) could not be loaded");
     return api;
 }
@@ -139,6 +144,12 @@ __global__ void loop_reduce_k(LoopPtrs in, int P, size_t n, int op, T* __restric
     }
 }
 
+// all-gather: out[k * n + i] = in_k[i]
+__global__ void loop_gather_k(LoopPtrs in, int P, size_t n, double* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n * P; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = static_cast<const double*>(in.p[i / n])[i % n];
+}
+
 }  // namespace
 
 struct Comm {
@@ -211,43 +222,64 @@ void comm_destroy(void* comm) {
 
 namespace {
 
-void loop_allreduce(Comm* c, void* buf, size_t count, int type, int op, cudaStream_t s) {
+// kind 0: all-reduce of `count` elements in place (buf); 1: reduce-scatter (fp64 sum): rank r
+// receives the sum of the ranks' buf[r count .. (r + 1) count) in out; 2: all-gather (fp64):
+// out[k count ..] = rank k's buf[0 .. count)
+void loop_collective(Comm* c, int kind, void* buf, void* out, size_t count, int type, int op, cudaStream_t s) {
     LoopGroup& g = *c->group;
     const int r = c->rank;
     try {
         UOTK_CUDA(cudaEventRecord(g.ready[r], s));
         g.buf[r] = buf;
         g.count[r] = count;
-        g.op[r] = op;
+        g.op[r] = op + 16 * kind;
         g.type[r] = type;
         g.barrier();  // (1) every rank's buffer and event are published
         for (int k = 0; k < g.P; ++k)
-            if (g.count[k] != count || g.op[k] != op || g.type[k] != type)
-                fail(UOTK_ENCCL, "loopback all-reduce: ranks disagree on count / op / type (rank " +
+            if (g.count[k] != count || g.op[k] != op + 16 * kind || g.type[k] != type)
+                fail(UOTK_ENCCL, "loopback collective: ranks disagree on kind / count / op / type (rank " +
                                      std::to_string(k) + ": " + std::to_string(g.count[k]) + " vs " +
                                      std::to_string(count) + ")");
         LoopPtrs ptrs{};
         for (int k = 0; k < g.P; ++k) {
             ptrs.p[k] = g.buf[k];
+            if (kind == 1) ptrs.p[k] = static_cast<const double*>(g.buf[k]) + (size_t)r * count;
             if (k != r) UOTK_CUDA(cudaStreamWaitEvent(s, g.ready[k], 0));
         }
         const size_t esz = type == kF64 ? sizeof(double) : sizeof(int32_t);
-        DevBuf<double> tmp((count * esz + 7) / 8, s);
-        if (count) {
-            const int blocks = (int)std::min<size_t>(1184, (count + 255) / 256);
-            if (type == kF64) loop_reduce_k<double><<<blocks, 256, 0, s>>>(ptrs, g.P, count, op, tmp.p);
-            else loop_reduce_k<int32_t><<<blocks, 256, 0, s>>>(ptrs, g.P, count, op, reinterpret_cast<int32_t*>(tmp.p));
-            UOTK_LAUNCHED();
+        DevBuf<double> tmp;
+        const int blocks = (int)std::min<size_t>(1184, (count * (kind == 2 ? g.P : 1) + 255) / 256);
+        if (kind == 0) {
+            tmp.alloc((count * esz + 7) / 8, s);
+            if (count) {
+                if (type == kF64) loop_reduce_k<double><<<blocks, 256, 0, s>>>(ptrs, g.P, count, op, tmp.p);
+                else loop_reduce_k<int32_t><<<blocks, 256, 0, s>>>(ptrs, g.P, count, op, reinterpret_cast<int32_t*>(tmp.p));
+                UOTK_LAUNCHED();
+            }
+        } else if (kind == 1) {  // into `out` (not a published buffer): no copy-back needed
+            if (count) {
+                loop_reduce_k<double><<<blocks, 256, 0, s>>>(ptrs, g.P, count, kSum, static_cast<double*>(out));
+                UOTK_LAUNCHED();
+            }
+        } else {
+            if (count) {
+                loop_gather_k<<<blocks, 256, 0, s>>>(ptrs, g.P, count, static_cast<double*>(out));
+                UOTK_LAUNCHED();
+            }
         }
         UOTK_CUDA(cudaEventRecord(g.done[r], s));
-        g.barrier();  // (2) every rank's reduction is enqueued: no buffer is overwritten before all read it
+        g.barrier();  // (2) every rank's reads are enqueued: no buffer is overwritten before all read it
         for (int k = 0; k < g.P; ++k)
             if (k != r) UOTK_CUDA(cudaStreamWaitEvent(s, g.done[k], 0));
-        if (count) UOTK_CUDA(cudaMemcpyAsync(buf, tmp.p, count * esz, cudaMemcpyDeviceToDevice, s));
+        if (kind == 0 && count) UOTK_CUDA(cudaMemcpyAsync(buf, tmp.p, count * esz, cudaMemcpyDeviceToDevice, s));
     } catch (const Error& e) {
         g.abort(e.msg);
         throw;
     }
+}
+
+void loop_allreduce(Comm* c, void* buf, size_t count, int type, int op, cudaStream_t s) {
+    loop_collective(c, 0, buf, nullptr, count, type, op, s);
 }
 
 }  // namespace
@@ -269,6 +301,26 @@ void comm_allreduce_i32(int32_t* buf, size_t count, int op_max_min_sum, void* co
     ncclRedOp_t op = op_max_min_sum == 1 ? ncclMax : (op_max_min_sum == 2 ? ncclMin : ncclSum);
     check_nccl(nccl().AllReduce(buf, buf, count, ncclInt32, op, c->comm, s), "ncclAllReduce");
 }
+
+// rank r receives out[0 .. count) = sum over ranks of their in[r count .. (r + 1) count)
+void comm_reduce_scatter(const double* in, double* out, size_t count, void* comm, cudaStream_t s) {
+    Comm* c = static_cast<Comm*>(comm);
+    if (!c) fail(UOTK_EINVAL, "internal: reduce-scatter without a communicator");
+    if (c->loopback) return loop_collective(c, 1, const_cast<double*>(in), out, count, kF64, kSum, s);
+    if (count == 0) return;
+    check_nccl(nccl().ReduceScatter(in, out, count, ncclDouble, ncclSum, c->comm, s), "ncclReduceScatter");
+}
+
+// out[k count .. (k + 1) count) = rank k's in[0 .. count)
+void comm_all_gather(const double* in, double* out, size_t count, void* comm, cudaStream_t s) {
+    Comm* c = static_cast<Comm*>(comm);
+    if (!c) fail(UOTK_EINVAL, "internal: all-gather without a communicator");
+    if (c->loopback) return loop_collective(c, 2, const_cast<double*>(in), out, count, kF64, kSum, s);
+    if (count == 0) return;
+    check_nccl(nccl().AllGather(in, out, count, ncclDouble, c->comm, s), "ncclAllGather");
+}
+
+int comm_rank(void* comm) { return comm ? static_cast<Comm*>(comm)->rank : 0; }
 
 void comm_allreduce_minmax(double* dmin, int nmin, double* dmax, int nmax, void* comm, cudaStream_t s) {
     if (dmin) comm_allreduce(dmin, nmin, 2, comm, s);

@@ -85,8 +85,9 @@ def _np(t):
                                           (2, W.GAUSS, 0), (1, W.GAUSS, 8)])
 def test_kernel_sum_sharded(uk, P, d, kind, flags):
     """Sources and targets sharded over P ranks: each rank obtains, at its own targets,
-    the sum over ALL ranks' sources.  Gaussian on the separable chain (all-reduce of the
-    first pass's box) and on the cuFFT chain (flags 8: truncated-spectrum all-reduce);
+    the sum over ALL ranks' sources.  Gaussian on the separable chain (slab-distributed:
+    reduce-scatter of the first pass's column / plane blocks, 1/P of the next pass per
+    rank, all-gather) and on the cuFFT chain (flags 8: truncated-spectrum all-reduce);
     IMQ on the pruned d = 3 chain and the full d = 2 chain."""
     param = 0.0025 if kind == W.GAUSS else 0.05
     pr = W.random_sum(d, 4001, 3001, kind=kind, param=param, seed=100 + d + P, signed=True)
@@ -104,6 +105,26 @@ def test_kernel_sum_sharded(uk, P, d, kind, flags):
     got = np.concatenate([o for o, _ in res])
     assert all(info["nranks"] == P for _, info in res)
     assert len({info["h"] for _, info in res}) == 1 and len({info["N"] for _, info in res}) == 1
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-9
+
+
+@pytest.mark.parametrize("P", [3, 8])
+@pytest.mark.parametrize("d", [2, 3])
+def test_kernel_sum_sharded_small_box(uk, P, d):
+    """A wide Gaussian (small grid, footprint box of a few cells): the slab split of the
+    separable chain leaves some ranks with no column / plane block (w < P * ceil(w/P) or
+    w < P); they still take part in every collective.  P = 3 gives ragged blocks."""
+    pr = W.random_sum(d, 2001, 1501, kind=W.GAUSS, param=0.08, seed=300 + d + P, signed=True)
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, pr.kind, pr.param)
+    sb, tb = shard_bounds(2001, P), shard_bounds(1501, P)
+    src, alpha, tgt = cuda(pr.src), cuda(pr.alpha), cuda(pr.tgt)
+
+    def fn(r, comm, st):
+        (s0, s1), (t0, t1) = sb[r], tb[r]
+        return _np(uk.kernel_sum(src[s0:s1], alpha[s0:s1], tgt[t0:t1], W.GAUSS, 0.08,
+                                 opts={"method": "nfft"}, comm=comm, stream=st))
+
+    got = np.concatenate(run_ranks(uk, P, fn))
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-9
 
 
