@@ -34,7 +34,8 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
     const int len = run_len[r];
     const int nc = (len + kChunk - 1) / kChunk;
     for (int k = 0; k < nc; ++k)
-        desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r], 0);
+        desc[chunk_off[r] + k] = make_int4(run_start[r] + k * kChunk, min(kChunk, len - k * kChunk), run_key[r],
+                                           r + 1 < *nruns ? run_key[r + 1] : -1);  // .w: the next group's key
 }
 
 // Window blocks (layout per d: chunks.cuh).  One warp per (chunk, axis): lane p loads

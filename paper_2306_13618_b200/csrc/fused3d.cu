@@ -264,21 +264,30 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 
 // ---------------------------------------------------------------- warp-specialised half-step
 // The Sinkhorn half-step with the gather and the spread on different warps of the CTA:
-//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions), sum the 4
-//                    warp partials, run the update (3.3)/(3.4), and publish the weighted
-//                    rows xw[p][a] = w_p X_p[a] of chunk k;
-//   warps 4-7 ("S"): spread chunk k from xw (A = xw Y, B = Z on DMMA) while G already
-//                    gathers chunk k+1.
+//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions); one of them
+//                    (k mod 4) sums the 4 warp partials, runs the update (3.3)/(3.4) and
+//                    publishes the weights w_p of chunk k while the other three already
+//                    gather chunk k+1;
+//   warps 4-7 ("S"): spread chunk k (A = w_p X_p Y_p, B = Z on DMMA) while G gathers
+//                    chunk k+1.
 // Each group's scalar phases (contractions, log/exp of the update, fragment products) then
 // overlap the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
 // mbarriers: win_full[3] (TMA ring of window blocks, refilled by S when it releases a
-// slot), xw_full[2] / xw_empty[2] (the weighted rows); each group synchronises
-// internally with its own named barrier (ids 1 and 2), never with __syncthreads.
+// slot), xw_full[2] / xw_empty[2] (the weights); the epilogue warp waits for the
+// partials on a per-slot named barrier (ids 3..6, the others bar.arrive), S synchronises
+// on named barrier 2, never with __syncthreads.
 constexpr int kRing = 3;
+// Gather footprint staging: each G warp copies its 4 a-planes x 16 rows of the NEXT group's
+// footprint (key = desc.w) into shared memory with 16-byte cp.async while the current group
+// runs, and loads its B fragments from there at the group change (no global-latency stall
+// at the first DMMAs of a group).  Rows start at the even double at or before the row
+// (16-byte alignment): 18 doubles per row, the row's parity is the offset.
+constexpr int kFootRow = 18;
 struct __align__(128) SmemWS {
+    double foot[4][4][16][kFootRow];
     double win[kRing][3][kChunk][kStride];
-    double xw[2][kChunk][kStride];
-    double red[2][4][kChunk];
+    double wsc[2][kChunk];     // the chunk's next weights w_p (the spread's A = w_p X_p Y_p)
+    double red[4][4][kChunk];  // per-warp partial sums, 4 chunks in flight
     unsigned long long win_full[kRing];
     unsigned long long xw_full[2];
     unsigned long long xw_empty[2];
@@ -306,7 +315,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     if (tid == 0) {
         for (int i = 0; i < kRing; ++i) mbar_init(&sm.win_full[i], 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&sm.xw_full[i], 128);
+            mbar_init(&sm.xw_full[i], 32);
             mbar_init(&sm.xw_empty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -328,7 +337,23 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
         double Fb[8][4];  // Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
         int32_t cur_key = -1;
         double ddmax = 0.0;
-        int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
+        int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, -1);
+        double(*foot)[16][kFootRow] = sm.foot[gw];
+        // stage this warp's 64 footprint rows of group `key` (576 16-byte pieces, 18 per lane)
+        auto stage = [&](int32_t key) {
+            const int64_t org = origin(key);
+#pragma unroll 6
+            for (int t = 0; t < 18; ++t) {
+                const int i = lane + 32 * t;
+                const int row = i / 9, j = i - 9 * row;
+                const int64_t rs = org + (int64_t)(a0 + (row >> 4)) * ng2 + (int64_t)(row & 15) * ng;
+                const int sh = (int)(rs & 1);
+                const uint32_t nb = j < 8 ? 16u : (sh ? 8u : 0u);
+                cp_async16(&foot[row >> 4][row & 15][2 * j], grid_in + (rs - sh) + 2 * j, nb);
+            }
+            cp_async_commit();
+        };
+        if (nck > 0) stage(dsc_next.z);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
@@ -339,28 +364,25 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             if (dsc.z != cur_key) {
                 cur_key = dsc.z;
                 const int64_t org = origin(cur_key);
+                cp_async_wait_all();
+                __syncwarp();
 #pragma unroll
                 for (int nt = 0; nt < 8; ++nt) {
-                    const double* row = grid_in + org + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+                    const int64_t rs = org + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
+                    const double* row = &foot[nt >> 1][8 * (nt & 1) + gq][rs & 1];
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) Fb[nt][ks] = __ldg(row + 4 * ks + tq);
+                    for (int ks = 0; ks < 4; ++ks) Fb[nt][ks] = row[4 * ks + tq];
                 }
+                __syncwarp();
+                if (dsc.w >= 0) stage(dsc.w);  // the next group's rows, one group ahead
             }
-            if (lane < cnt) epi.prefetch(p0 + lane);
-            if (k + 1 < nck && dsc_next.z != cur_key) {
-                const int64_t norg = origin(dsc_next.z);
-#pragma unroll
-                for (int nt = 0; nt < 8; ++nt) {
-                    const double* rowp =
-                        grid_in + norg + (int64_t)(a0 + (nt >> 1)) * ng2 + (int64_t)(8 * (nt & 1) + gq) * ng;
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(rowp + 4 * tq));
-                }
-            }
+            const int duty = (int)(k & 3);  // this chunk's epilogue warp
+            if (gw == duty && lane < cnt) epi.prefetch(p0 + lane);
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
             const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
-            double(*red)[kChunk] = sm.red[k & 1];
+            double(*red)[kChunk] = sm.red[k & 3];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 if (8 * mt >= cnt) break;  // m-tiles past the chunk's points hold no point
@@ -392,29 +414,27 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 part += __shfl_xor_sync(0xffffffffu, part, 2);
                 if (tq == 0) red[gw][p] = part;
             }
-            group_sync(1);
-            // lane p: t_p; warp 0 writes the potentials, all G warps form w_p
-            double wp = 0.0;
-            if (lane < cnt) {
-                const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
-                if (gw == 0) {  // one update evaluation returning both the change and the weight
+            // The epilogue of chunk k runs on ONE warp (k mod 4): the other three arrive on
+            // the chunk's named barrier (ids 3..6) and go on to chunk k+1's DMMAs.  Four
+            // partial-sum slots suffice: a warp reaches chunk k+4 only after S released
+            // chunk k+1 (window ring of 3), i.e. after chunk k's epilogue.
+            if (gw != duty) {
+                group_arrive(3 + duty, 128);
+            } else {
+                group_sync(3 + duty, 128);
+                double wp = 0.0;
+                if (lane < cnt) {
+                    const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
                     ddmax = fmax(ddmax, epi.apply(p0 + lane, t, epi.load(p0 + lane), wp));
-                } else {
-                    wp = epi.weight(p0 + lane, t);
                 }
+                // publish w_p for chunk k (S forms w_p X_p[a] from the window block)
+                if (k >= 2) mbar_wait(&sm.xw_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
+                sm.wsc[k & 1][lane] = wp;
+                mbar_arrive(&sm.xw_full[k & 1]);
             }
-            // publish xw[p][a0..a0+3] = w_p X_p[a] for chunk k
-            if (k >= 2) mbar_wait(&sm.xw_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
-            {
-                const double2 xa = *reinterpret_cast<const double2*>(&wx[lane][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&wx[lane][a0 + 2]);
-                double2* dst = reinterpret_cast<double2*>(&sm.xw[k & 1][lane][a0]);
-                dst[0] = make_double2(wp * xa.x, wp * xa.y);
-                dst[1] = make_double2(wp * xb.x, wp * xb.y);
-            }
-            mbar_arrive(&sm.xw_full[k & 1]);
         }
-        if (gw == 0) warp_max_atomic(dmax, ddmax);
+        cp_async_wait_all();  // a staged next group past this block's range
+        warp_max_atomic(dmax, ddmax);
     } else {
         // ------------------------------------------------------------ spread
         double S[8][2][2];  // S[mt][nt] = S[a0 + (mt>>1)][8(mt&1) + gq][8nt + 2tq + i]
@@ -448,18 +468,20 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             }
             mbar_wait(&sm.xw_full[k & 1], (uint32_t)((k >> 1) & 1));
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
+            const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
-            const double(*xw)[kStride] = sm.xw[k & 1];
+            const double* wsc = sm.wsc[k & 1];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 if (4 * ks >= cnt) break;  // k-steps past the chunk's points add zero windows
                 const int p = 4 * ks + tq;
                 const double b0 = wz[p][gq];
                 const double b1 = wz[p][8 + gq];
-                const double2 xa = *reinterpret_cast<const double2*>(&xw[p][a0]);
-                const double2 xb = *reinterpret_cast<const double2*>(&xw[p][a0 + 2]);
-                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                const double wv = wsc[p];
+                const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
+                const double xv[4] = {wv * xa.x, wv * xa.y, wv * xb.x, wv * xb.y};
                 const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
@@ -468,7 +490,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     dmma(S[mt][1][0], S[mt][1][1], am, b1);
                 }
             }
-            group_sync(2);  // all S warps are done with xw[k&1] and window slot
+            group_sync(2);  // all S warps are done with wsc[k&1] and the window slot
             if (warp == 4 && lane == 0) {
                 mbar_arrive(&sm.xw_empty[k & 1]);
                 if (k + kRing < nck) {

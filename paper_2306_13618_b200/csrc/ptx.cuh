@@ -49,6 +49,9 @@ __device__ __forceinline__ void group_sync(int id) {  // named barrier over one 
     asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
 
+__device__ __forceinline__ void group_arrive(int id, int nthreads) {  // arrive without waiting
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void group_sync(int id, int nthreads) {  // named barrier over nthreads
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -59,5 +62,15 @@ __device__ __forceinline__ void mbar_init_fence() {
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+
+
+// 16-byte cp.async (L2 -> shared, bypassing L1) copying `src_bytes` (0, 8 or 16) bytes and
+// zero-filling the rest; completion tracked per thread with commit / wait groups.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 }  // namespace uotk
