@@ -7,7 +7,7 @@
 // chunked_prepare) — points do not move between Sinkhorn iterations.  A 256-thread CTA
 // walks a contiguous, cost-balanced range of chunks, streaming each chunk's window block
 // into shared memory with a TMA bulk copy (cp.async.bulk + mbarrier, double buffered in
-// chunked3d_k, a ring of 3 in the warp-specialised sinkhorn3d_ws_k).  Sparse clouds use
+// chunked3d_k, a ring of 4 in the warp-specialised sinkhorn3d_ws_k).  Sparse clouds use
 // z-segment groups (KZ = 24: 9 cells along z share one 16 x 16 x 24 footprint).
 //
 // Per chunk, with X_p, Y_p, Z_p the windows of point p along the three axes and F the
@@ -272,11 +272,11 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 //                    chunk k+1.
 // Each group's scalar phases (contractions, log/exp of the update, fragment products) then
 // overlap the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
-// mbarriers: win_full[3] (TMA ring of window blocks, refilled by S when it releases a
-// slot), xw_full[2] / xw_empty[2] (the weights); the epilogue warp waits for the
+// mbarriers: win_full[4] (TMA ring of window blocks, refilled by S when it releases a
+// slot), xw_full[4] / xw_empty[4] (the weights); the epilogue warp waits for the
 // partials on a per-slot named barrier (ids 3..6, the others bar.arrive), S synchronises
 // on named barrier 2, never with __syncthreads.
-constexpr int kRing = 3;
+constexpr int kRing = 4;
 // Gather footprint staging: each G warp copies its 4 a-planes x 16 rows of the NEXT group's
 // footprint (key = desc.w) into shared memory with 16-byte cp.async while the current group
 // runs, and loads its B fragments from there at the group change (no global-latency stall
@@ -286,11 +286,11 @@ constexpr int kFootRow = 18;
 struct __align__(128) SmemWS {
     double foot[4][4][16][kFootRow];
     double win[kRing][3][kChunk][kStride];
-    double wsc[2][kChunk];     // the chunk's next weights w_p (the spread's A = w_p X_p Y_p)
+    double wsc[4][kChunk];     // the chunk's next weights w_p (the spread's A = w_p X_p Y_p)
     double red[4][4][kChunk];  // per-warp partial sums, 4 chunks in flight
     unsigned long long win_full[kRing];
-    unsigned long long xw_full[2];
-    unsigned long long xw_empty[2];
+    unsigned long long xw_full[4];
+    unsigned long long xw_empty[4];
 };
 
 __global__ void __launch_bounds__(256, kBlocksPerSM)
@@ -314,7 +314,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 
     if (tid == 0) {
         for (int i = 0; i < kRing; ++i) mbar_init(&sm.win_full[i], 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(&sm.xw_full[i], 32);
             mbar_init(&sm.xw_empty[i], 1);
         }
@@ -417,7 +417,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             // The epilogue of chunk k runs on ONE warp (k mod 4): the other three arrive on
             // the chunk's named barrier (ids 3..6) and go on to chunk k+1's DMMAs.  Four
             // partial-sum slots suffice: a warp reaches chunk k+4 only after S released
-            // chunk k+1 (window ring of 3), i.e. after chunk k's epilogue.
+            // chunk k (window ring of 4), i.e. after chunk k's epilogue.
             if (gw != duty) {
                 group_arrive(3 + duty, 128);
             } else {
@@ -428,9 +428,9 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     ddmax = fmax(ddmax, epi.apply(p0 + lane, t, epi.load(p0 + lane), wp));
                 }
                 // publish w_p for chunk k (S forms w_p X_p[a] from the window block)
-                if (k >= 2) mbar_wait(&sm.xw_empty[k & 1], (uint32_t)(((k >> 1) - 1) & 1));
-                sm.wsc[k & 1][lane] = wp;
-                mbar_arrive(&sm.xw_full[k & 1]);
+                if (k >= 4) mbar_wait(&sm.xw_empty[k & 3], (uint32_t)(((k >> 2) - 1) & 1));
+                sm.wsc[k & 3][lane] = wp;
+                mbar_arrive(&sm.xw_full[k & 3]);
             }
         }
         cp_async_wait_all();  // a staged next group past this block's range
@@ -466,12 +466,12 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
-            mbar_wait(&sm.xw_full[k & 1], (uint32_t)((k >> 1) & 1));
+            mbar_wait(&sm.xw_full[k & 3], (uint32_t)((k >> 2) & 1));
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
             const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
-            const double* wsc = sm.wsc[k & 1];
+            const double* wsc = sm.wsc[k & 3];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 if (4 * ks >= cnt) break;  // k-steps past the chunk's points add zero windows
@@ -490,9 +490,9 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     dmma(S[mt][1][0], S[mt][1][1], am, b1);
                 }
             }
-            group_sync(2);  // all S warps are done with wsc[k&1] and the window slot
+            group_sync(2);  // all S warps are done with wsc[k&3] and the window slot
             if (warp == 4 && lane == 0) {
-                mbar_arrive(&sm.xw_empty[k & 1]);
+                mbar_arrive(&sm.xw_empty[k & 3]);
                 if (k + kRing < nck) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(&sm.win_full[slot], kWinBytes);
