@@ -383,9 +383,11 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             const double(*wy)[kStride] = sm.win[slot][1];
             const double(*wz)[kStride] = sm.win[slot][2];
             double(*red)[kChunk] = sm.red[k & 3];
+            double part[4];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
-                if (8 * mt >= cnt) break;  // m-tiles past the chunk's points hold no point
+                part[mt] = 0.0;
+                if (8 * mt >= cnt) continue;  // m-tiles past the chunk's points hold no point
                 const int p = 8 * mt + gq;
                 double acc[8][2];
 #pragma unroll
@@ -401,18 +403,23 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
                 const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
                 const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
-                double part = 0.0;
 #pragma unroll
                 for (int al = 0; al < 4; ++al) {
                     double q = acc[2 * al][0] * ylo.x;
                     q = fma(acc[2 * al][1], ylo.y, q);
                     q = fma(acc[2 * al + 1][0], yhi.x, q);
                     q = fma(acc[2 * al + 1][1], yhi.y, q);
-                    part = fma(q, xv[al], part);
+                    part[mt] = fma(q, xv[al], part[mt]);
                 }
-                part += __shfl_xor_sync(0xffffffffu, part, 1);
-                part += __shfl_xor_sync(0xffffffffu, part, 2);
-                if (tq == 0) red[gw][p] = part;
+            }
+            // the four tiles' reductions over tq together (independent shuffles)
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) part[mt] += __shfl_xor_sync(0xffffffffu, part[mt], 1);
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) part[mt] += __shfl_xor_sync(0xffffffffu, part[mt], 2);
+            if (tq == 0) {
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) red[gw][8 * mt + gq] = part[mt];
             }
             // The epilogue of chunk k runs on ONE warp (k mod 4): the other three arrive on
             // the chunk's named barrier (ids 3..6) and go on to chunk k+1's DMMAs.  Four
