@@ -31,8 +31,10 @@
  *  - `comm` is a uotk_comm created by uotk_comm_create, or NULL for one GPU.
  *    With a communicator every rank passes its LOCAL shard of the points; the
  *    oversampled Fourier coefficients of each kernel sum are summed over ranks
- *    (NCCL all-reduce) so each rank obtains the sums at its own targets from
- *    all ranks' sources.  Scalar results (uot result, mmd2) are global and
+ *    (NCCL all-reduce of the truncated I_N spectrum; for the Gaussian's separable
+ *    chain a reduce-scatter of the first pass's blocks, the middle pass on 1/P of
+ *    the box per rank and an all-gather: UOTK_DIST_CHAIN=0 keeps one all-reduce)
+ *    so each rank obtains the sums at its own targets from all ranks' sources.  Scalar results (uot result, mmd2) are global and
  *    identical on all ranks.
  *    A rank's local shard may be empty (n = 0 or m = 0) with a multi-rank
  *    communicator: it still takes part in every collective.  Input and numeric
@@ -124,8 +126,8 @@ typedef struct {
 #define UOTK_FLAG_CHUNKED 2  /* cell-group kernels at any density (m = 8; d = 3: or 6) */
 #define UOTK_FLAG_TRANSPORT 4 /* uot: also evaluate the transport term <pi, d^2>    */
 #define UOTK_FLAG_FFT 8       /* always the cuFFT chain (D2Z, D_k, Z2D), never the separable
-                                 circulant GEMMs of the Gaussian (with a communicator their
-                                 first pass's box is the all-reduced quantity)             */
+                                 circulant GEMMs of the Gaussian (with a communicator those
+                                 are slab-distributed: reduce-scatter / all-gather)        */
 #define UOTK_FLAG_COST_R1 16  /* uot: cost d^1 instead of d^2, i.e. the Laplace Gibbs kernel
                                  exp(-||x - y|| / eps) (Algorithm 2's r = 1);
                                  not combinable with UOTK_FLAG_TRANSPORT                     */
@@ -287,10 +289,10 @@ int uotk_comm_destroy(void* comm);
  * to comms_out[0..nranks-1] (handle k = rank k).  It stands in for nranks processes (the
  * multi-rank path tested with a single device): each handle is used by one host thread,
  * all nranks threads call the same entry point concurrently with their own shards and
- * streams.  Every all-reduce of the exchange step (Fourier coefficients, bounding box,
- * scalars) is performed by a library kernel that sums (or maxes) the nranks device
- * buffers in rank order, ordered by CUDA events and host barriers — no kernel waits on
- * another.  A rank whose call fails aborts the group (the others fail with UOTK_ENCCL at
+ * streams.  Every collective of the exchange step (all-reduce of Fourier coefficients,
+ * bounding box and scalars; reduce-scatter / all-gather of the slab-distributed chain) is
+ * performed by a library kernel that sums (or maxes, or copies) the nranks device buffers
+ * in rank order, ordered by CUDA events and host barriers — no kernel waits on another.  A rank whose call fails aborts the group (the others fail with UOTK_ENCCL at
  * their next collective; a rank that never arrives times out after 120 s).  Results equal
  * NCCL's up to the summation order; timings are not representative.  Destroy each
  * handle with uotk_comm_destroy. */
