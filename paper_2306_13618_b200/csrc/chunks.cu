@@ -20,10 +20,24 @@ namespace {
 
 inline int blocks_for(int64_t n, int tb) { return (int)std::max<int64_t>(1, (n + tb - 1) / tb); }
 
-__global__ void chunk_count_k(const int32_t* __restrict__ run_len, const int32_t* __restrict__ nruns,
-                              int32_t* __restrict__ nchunk) {
+// over all n run slots: chunks per run, zero (run length and chunks) past the last run, so
+// the scans can run over n items without the host knowing the run count
+__global__ void chunk_count_k(int32_t* __restrict__ run_len, const int32_t* __restrict__ nruns,
+                              int32_t* __restrict__ nchunk, int n) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < *nruns) nchunk[r] = (run_len[r] + kChunk - 1) / kChunk;
+    if (r >= n) return;
+    if (r < *nruns) {
+        nchunk[r] = (run_len[r] + kChunk - 1) / kChunk;
+    } else {
+        run_len[r] = 0;
+        nchunk[r] = 0;
+    }
+}
+
+// cnt[1] = total number of chunks (chunk_off is the exclusive sum of nchunk over n slots)
+__global__ void chunk_total_k(const int32_t* __restrict__ chunk_off, const int32_t* __restrict__ nchunk, int n,
+                              int32_t* __restrict__ cnt) {
+    cnt[1] = chunk_off[n - 1] + nchunk[n - 1];
 }
 
 __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t* __restrict__ run_len,
@@ -159,26 +173,29 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     DevBuf<uint8_t> tmp(tmp_bytes, s);
     trace_mark("chunks: temp allocation");
     int32_t nruns = 0;
-    // runs of equal group keys -> chunks of <= 32 points; returns the number of chunks
+    // runs of equal group keys -> chunks of <= 32 points; returns the number of chunks.
+    // One host synchronisation per encode: the scans run over all n run slots (the slots
+    // past the last run zeroed on the device), and the run and chunk counts come back
+    // together.
     auto encode = [&](const int32_t* keys) -> int64_t {
         size_t t = tmp_bytes;
         UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, t, keys, run_key.p, run_len.p, cnt.p, n, s));
         add_launches(2);
-        UOTK_CUDA(cudaMemcpyAsync(&nruns, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        UOTK_CUDA(cudaStreamSynchronize(s));
-        trace_mark("chunks: run-length encode");
-        t = tmp_bytes;
-        UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, run_len.p, run_start.p, nruns, s));
-        chunk_count_k<<<blocks_for(nruns, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p);
+        chunk_count_k<<<blocks_for(n, 256), 256, 0, s>>>(run_len.p, cnt.p, nchunk.p, n);
         UOTK_LAUNCHED();
         t = tmp_bytes;
-        UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, nchunk.p, chunk_off.p, nruns, s));
-        add_launches(2);
-        int32_t last[2];
-        UOTK_CUDA(cudaMemcpyAsync(&last[0], chunk_off.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        UOTK_CUDA(cudaMemcpyAsync(&last[1], nchunk.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, run_len.p, run_start.p, n, s));
+        t = tmp_bytes;
+        UOTK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, nchunk.p, chunk_off.p, n, s));
+        add_launches(4);
+        chunk_total_k<<<1, 1, 0, s>>>(chunk_off.p, nchunk.p, n, cnt.p);
+        UOTK_LAUNCHED();
+        int32_t h[2];
+        UOTK_CUDA(cudaMemcpyAsync(h, cnt.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         UOTK_CUDA(cudaStreamSynchronize(s));
-        return (int64_t)last[0] + last[1];
+        trace_mark("chunks: run-length encode + scans");
+        nruns = h[0];
+        return (int64_t)h[1];
     };
     int64_t nchunks = encode(ps.key.p);
     trace_mark("chunks: encode");
