@@ -264,18 +264,16 @@ chunked3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const
 
 // ---------------------------------------------------------------- warp-specialised half-step
 // The Sinkhorn half-step with the gather and the spread on different warps of the CTA:
-//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions); one of them
-//                    (k mod 4) sums the 4 warp partials, runs the update (3.3)/(3.4) and
-//                    publishes the weights w_p of chunk k while the other three already
-//                    gather chunk k+1;
-//   warps 4-7 ("S"): spread chunk k (A = w_p X_p Y_p, B = Z on DMMA) while G gathers
-//                    chunk k+1.
-// Each group's scalar phases (contractions, log/exp of the update, fragment products) then
-// overlap the other group's DMMA stream instead of idling the FP64 pipe.  Hand-offs use
-// mbarriers: win_full[4] (TMA ring of window blocks, refilled by S when it releases a
-// slot), xw_full[4] / xw_empty[4] (the weights); the epilogue warp waits for the
-// partials on a per-slot named barrier (ids 3..6, the others bar.arrive), S synchronises
-// on named barrier 2, never with __syncthreads.
+//   warps 0-3 ("G"): gather chunk k (DMMA GEMM over c + b/a contractions) and publish the
+//                    four warp partials of t_p (red_full); no update, no barrier: G runs up
+//                    to a window ring ahead of S;
+//   warps 4-7 ("S"): the update (3.3)/(3.4) of chunk k+1 on ONE S warp (rotating, one chunk
+//                    ahead: its log/exp chain overlaps the other S warps' DMMAs), then the
+//                    spread of chunk k (A = w_p X_p Y_p, B = Z on DMMA).
+// Each group's scalar phases then overlap DMMA streams instead of idling the FP64 pipe.
+// Hand-offs are mbarriers: win_full[4] (TMA ring of window blocks, refilled by the last S
+// warp to release a slot), red_full[4] (G partials), w_full / w_empty[4] (the weights);
+// never __syncthreads.
 constexpr int kRing = 4;
 // Gather footprint staging: each G warp copies its 4 a-planes x 16 rows of the NEXT group's
 // footprint (key = desc.w) into shared memory with 16-byte cp.async while the current group
@@ -287,10 +285,12 @@ struct __align__(128) SmemWS {
     double foot[4][4][16][kFootRow];
     double win[kRing][3][kChunk][kStride];
     double wsc[4][kChunk];     // the chunk's next weights w_p (the spread's A = w_p X_p Y_p)
-    double red[4][4][kChunk];  // per-warp partial sums, 4 chunks in flight
+    double red[4][4][kChunk];  // per-G-warp partial sums of t_p, 4 chunks in flight
     unsigned long long win_full[kRing];
-    unsigned long long xw_full[4];
-    unsigned long long xw_empty[4];
+    unsigned long long red_full[4];  // the four G partials of a chunk are in red[]
+    unsigned long long w_full[4];    // a chunk's weights are in wsc[]
+    unsigned long long w_empty[4];   // the four S warps are done with wsc[] of a chunk
+    unsigned int slot_done[kRing];   // S warps done with a window slot (running count)
 };
 
 __global__ void __launch_bounds__(256, kBlocksPerSM)
@@ -315,9 +315,11 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
     if (tid == 0) {
         for (int i = 0; i < kRing; ++i) mbar_init(&sm.win_full[i], 1);
         for (int i = 0; i < 4; ++i) {
-            mbar_init(&sm.xw_full[i], 32);
-            mbar_init(&sm.xw_empty[i], 1);
+            mbar_init(&sm.red_full[i], 4);
+            mbar_init(&sm.w_full[i], 1);
+            mbar_init(&sm.w_empty[i], 4);
         }
+        for (int i = 0; i < kRing; ++i) sm.slot_done[i] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -336,7 +338,6 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
         // ------------------------------------------------------------ gather + update
         double Fb[8][4];  // Fb[nt][ks] = F[a0 + (nt>>1)][8(nt&1) + gq][4ks + tq]
         int32_t cur_key = -1;
-        double ddmax = 0.0;
         int4 dsc_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, -1);
         double(*foot)[16][kFootRow] = sm.foot[gw];
         // stage this warp's 64 footprint rows of group `key` (576 16-byte pieces, 18 per lane)
@@ -359,7 +360,6 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             const int slot = (int)(k % kRing);
             const int4 dsc = dsc_next;
             if (k + 1 < nck) dsc_next = desc[c + 1];
-            const int64_t p0 = dsc.x;
             const int cnt = dsc.y;
             if (dsc.z != cur_key) {
                 cur_key = dsc.z;
@@ -376,8 +376,6 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 __syncwarp();
                 if (dsc.w >= 0) stage(dsc.w);  // the next group's rows, one group ahead
             }
-            const int duty = (int)(k & 3);  // this chunk's epilogue warp
-            if (gw == duty && lane < cnt) epi.prefetch(p0 + lane);
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
             const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
@@ -421,27 +419,14 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) red[gw][8 * mt + gq] = part[mt];
             }
-            // The epilogue of chunk k runs on ONE warp (k mod 4): the other three arrive on
-            // the chunk's named barrier (ids 3..6) and go on to chunk k+1's DMMAs.  Four
-            // partial-sum slots suffice: a warp reaches chunk k+4 only after S released
-            // chunk k (window ring of 4), i.e. after chunk k's epilogue.
-            if (gw != duty) {
-                group_arrive(3 + duty, 128);
-            } else {
-                group_sync(3 + duty, 128);
-                double wp = 0.0;
-                if (lane < cnt) {
-                    const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
-                    ddmax = fmax(ddmax, epi.apply(p0 + lane, t, epi.load(p0 + lane), wp));
-                }
-                // publish w_p for chunk k (S forms w_p X_p[a] from the window block)
-                if (k >= 4) mbar_wait(&sm.xw_empty[k & 3], (uint32_t)(((k >> 2) - 1) & 1));
-                sm.wsc[k & 3][lane] = wp;
-                mbar_arrive(&sm.xw_full[k & 3]);
-            }
+            // publish this warp's partials of chunk k; the update runs on the spread side.
+            // Four partial-sum slots suffice: a G warp reaches chunk k+4 only after every S
+            // warp released chunk k's window slot (ring of 4), i.e. after chunk k's update
+            // (run by an S warp during chunk k-1) read them.
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.red_full[k & 3]);
         }
         cp_async_wait_all();  // a staged next group past this block's range
-        warp_max_atomic(dmax, ddmax);
     } else {
         // ------------------------------------------------------------ spread
         double S[8][2][2];  // S[mt][nt] = S[a0 + (mt>>1)][8(mt&1) + gq][8nt + 2tq + i]
@@ -458,10 +443,32 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                         if (S[mt][nt][i] != 0.0) atomicAdd(grid_out + row + 8 * nt + 2 * tq + i, S[mt][nt][i]);
             }
         };
+        // the update (3.3)/(3.4) of chunk j by one S warp (j mod 4), one chunk AHEAD of the
+        // spread: lane p sums the four G partials, writes the potential, the next weight,
+        // the sup-norm change, and publishes w_p in wsc[j & 3]
+        double ddmax = 0.0;
+        auto update = [&](int64_t j, const int4& dj) {
+            if (lane < dj.y) epi.prefetch(dj.x + lane);
+            mbar_wait(&sm.red_full[j & 3], (uint32_t)((j >> 2) & 1));
+            double wp = 0.0;
+            if (lane < dj.y) {
+                const double(*red)[kChunk] = sm.red[j & 3];
+                const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
+                ddmax = fmax(ddmax, epi.apply(dj.x + lane, t, epi.load(dj.x + lane), wp));
+            }
+            if (j >= 4) mbar_wait(&sm.w_empty[j & 3], (uint32_t)(((j >> 2) - 1) & 1));
+            sm.wsc[j & 3][lane] = wp;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.w_full[j & 3]);
+        };
+        int4 dk_next = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, -1);
+        if (nck > 0 && gw == 0) update(0, dk_next);
         for (int64_t k = 0; k < nck; ++k) {
             const int64_t c = cbeg + k;
             const int slot = (int)(k % kRing);
-            const int4 dk = desc[c];
+            const int4 dk = dk_next;
+            if (k + 1 < nck) dk_next = desc[c + 1];
+            if (k + 1 < nck && gw == (int)((k + 1) & 3)) update(k + 1, dk_next);
             const int32_t key = dk.z;
             const int cnt = dk.y;
             if (key != cur_key) {
@@ -473,7 +480,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) S[mt][nt][0] = S[mt][nt][1] = 0.0;
             }
-            mbar_wait(&sm.xw_full[k & 3], (uint32_t)((k >> 2) & 1));
+            mbar_wait(&sm.w_full[k & 3], (uint32_t)((k >> 2) & 1));
             mbar_wait(&sm.win_full[slot], (uint32_t)((k / kRing) & 1));
             const double(*wx)[kStride] = sm.win[slot][0];
             const double(*wy)[kStride] = sm.win[slot][1];
@@ -497,10 +504,14 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                     dmma(S[mt][1][0], S[mt][1][1], am, b1);
                 }
             }
-            group_sync(2);  // all S warps are done with wsc[k&3] and the window slot
-            if (warp == 4 && lane == 0) {
-                mbar_arrive(&sm.xw_empty[k & 3]);
-                if (k + kRing < nck) {
+            // release wsc[k & 3] (w_empty) and the window slot: no barrier among the S
+            // warps (the update rotates over them); the last of the four refills the slot
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                mbar_arrive(&sm.w_empty[k & 3]);
+                if ((atomicAdd(&sm.slot_done[slot], 1u) & 3u) == 3u && k + kRing < nck) {
+                    __threadfence_block();
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(&sm.win_full[slot], kWinBytes);
                     bulk_g2s(&sm.win[slot][0][0][0], win + (c + kRing) * kWinDoubles, kWinBytes, &sm.win_full[slot]);
@@ -508,6 +519,7 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
             }
         }
         if (cur_key >= 0) flush();
+        warp_max_atomic(dmax, ddmax);
     }
 }
 
