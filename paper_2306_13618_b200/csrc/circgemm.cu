@@ -5,8 +5,9 @@
 //
 // The passes are batched row-major fp64 GEMMs  Out_b = A_b B_b  (M = N = K = w) on the FP64
 // tensor cores: mma.sync m8n8k4 f64 (SASS DMMA), 64 x 64 output tiles per 128-thread CTA
-// (2 x 2 warps of 32 x 32), K in steps of 16 through a double-buffered cp.async pipeline,
-// zero-filled at the ragged edges.  The last pass also zeroes the footprint box of the
+// (2 x 2 warps of 32 x 32), K in steps of 16 through a double-buffered cp.async pipeline
+// (8-byte copies; a 3-stage ring of 16-byte copies when the rows are 16-byte aligned, as
+// they are on the even-aligned footprint box), zero-filled at the ragged edges.  The last pass also zeroes the footprint box of the
 // grid the next spread writes into (a disjoint buffer), which replaces a full-grid memset
 // per half-step.
 #include "common.cuh"
@@ -142,6 +143,111 @@ __global__ void __launch_bounds__(WM * WN * 32) dgemm_rm_k(GemmArgs g) {
     }
 }
 
+// Large boxes with 16-byte-aligned rows (even box origin, leading dimensions and sizes —
+// the box is even-aligned by choose_params): the same warp tiling, operands streamed by
+// 16-byte cp.async through a 3-stage ring (two tiles in flight while one is computed).
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, bool valid) {
+    const uint32_t d = smem_u32(dst);
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(valid ? src : nullptr), "r"(sz)
+                 : "memory");
+}
+template <int BM, int BN, int BK, int WM = 2, int WN = 2>
+__global__ void __launch_bounds__(WM * WN * 32) dgemm_v16_k(GemmArgs g) {
+    constexpr int NTH = WM * WN * 32;
+    constexpr int ST = 3;
+    constexpr int SA = BK + 4;
+    constexpr int SB = BN + 4;
+    constexpr int TM = BM / WM / 8, TN = BN / WN / 8;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                  // [ST][BM * SA]
+    double* Bs = smem + ST * BM * SA;   // [ST][BK * SB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int per_batch = g.tiles_m * g.tiles_n;
+    const int b = blockIdx.x / per_batch;
+    const int t = blockIdx.x % per_batch;
+    const int m0 = (t / g.tiles_n) * BM, n0 = (t % g.tiles_n) * BN;
+    const double* A = g.A + b * g.sA;
+    const double* B = g.B + b * g.sB;
+    const int nk = (g.K + BK - 1) / BK;
+    auto load = [&](int stage, int kt) {
+        if (kt < nk) {
+            const int k0 = kt * BK;
+            double* as = As + stage * BM * SA;
+            double* bs = Bs + stage * BK * SB;
+            for (int e = tid; e < BM * BK / 2; e += NTH) {
+                const int r = e / (BK / 2), c = 2 * (e % (BK / 2));
+                const bool v = m0 + r < g.M && k0 + c < g.K;
+                cp_async16(&as[r * SA + c], A + (int64_t)(m0 + r) * g.lda + (k0 + c), v);
+            }
+            for (int e = tid; e < BK * BN / 2; e += NTH) {
+                const int r = e / (BN / 2), c = 2 * (e % (BN / 2));
+                const bool v = k0 + r < g.K && n0 + c < g.N;
+                cp_async16(&bs[r * SB + c], B + (int64_t)(k0 + r) * g.ldb + (n0 + c), v);
+            }
+        }
+        cp_async_commit();  // (an empty group past the last tile keeps the wait counts uniform)
+    };
+    load(0, 0);
+    load(1, 1);
+    if (g.zbase) {
+        const int64_t nblk = (int64_t)gridDim.x;
+        const int64_t r0 = g.zrows * blockIdx.x / nblk, r1 = g.zrows * (blockIdx.x + 1) / nblk;
+        for (int64_t r = r0; r < r1; ++r) {
+            double* row = g.zbase + (r / g.zdiv) * g.zs1 + (r % g.zdiv) * g.zs0;
+            for (int64_t c = tid; c < g.zlen; c += NTH) row[c] = 0.0;
+        }
+    }
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<1>();  // tile kt has landed (tile kt+1 may still be in flight)
+        __syncthreads();     // ... for every thread; and everyone is done with tile kt-1's stage
+        load((kt + 2) % ST, kt + 2);
+        const double* as = As + (kt % ST) * BM * SA;
+        const double* bs = Bs + (kt % ST) * BK * SB;
+        const int kmax = min(BK, g.K - kt * BK);
+        for (int kk = 0; kk < kmax; kk += 4) {
+            double a[TM], bf[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = as[(wm * (BM / WM) + i * 8 + (lane >> 2)) * SA + kk + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bf[j] = bs[(kk + (lane & 3)) * SB + wn * (BN / WN) + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
+        }
+    }
+    double* O = g.O + b * g.sO;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int r = m0 + wm * (BM / WM) + i * 8 + (lane >> 2);
+        if (r >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int c = n0 + wn * (BN / WN) + j * 8 + 2 * (lane & 3);
+            if (c < g.N) O[(int64_t)r * g.ldo + c] = acc[i][j][0];
+            if (c + 1 < g.N) O[(int64_t)r * g.ldo + c + 1] = acc[i][j][1];
+        }
+    }
+}
+
+template <int BM, int BN, int BK, int WM = 2, int WN = 2>
+void launch_gemm_v16(GemmArgs g, int batch, cudaStream_t s) {
+    g.tiles_m = (g.M + BM - 1) / BM;
+    g.tiles_n = (g.N + BN - 1) / BN;
+    const int64_t blocks = (int64_t)g.tiles_m * g.tiles_n * batch;
+    const int smem = 3 * (BM * (BK + 4) + BK * (BN + 4)) * (int)sizeof(double);
+    set_smem_attr((const void*)dgemm_v16_k<BM, BN, BK, WM, WN>, smem);
+    dgemm_v16_k<BM, BN, BK, WM, WN><<<(unsigned)blocks, WM * WN * 32, smem, s>>>(g);
+    UOTK_LAUNCHED();
+}
+
 template <int BM, int BN, int BK, int STAGES, int WM = 2, int WN = 2>
 void launch_gemm(GemmArgs g, int batch, cudaStream_t s) {
     g.tiles_m = (g.M + BM - 1) / BM;
@@ -172,8 +278,20 @@ void gemm(int M, int N, int K, const double* A, int64_t lda, int64_t sA, const d
     const int64_t tiles64 = (int64_t)((M + 63) / 64) * ((N + 63) / 64) * batch;
     if (K <= 64 && M <= 64) launch_gemm<32, 32, 64, 1>(g, batch, s);       // C3 (w = 44)
     else if (tiles64 < 2 * 148) launch_gemm<32, 32, 32, 2>(g, batch, s);  // few tiles (C4 auto, w = 164)
-    else launch_gemm<64, 64, 16, 2>(g, batch, s);  // large boxes (C4 at 4096^2, w = 1982; 128 x 128
-                                                      // tiles with 8 warps measured 1.44 vs 1.24 ms per chain)
+    else {
+        // large boxes (C4 at 4096^2, w = 1982): 16-byte 3-stage operand ring when every row
+        // start is 16-byte aligned, else the 8-byte 2-stage kernel (128 x 128 tiles with 8
+        // warps measured 1.44 vs 1.24 ms per chain)
+        const bool even = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+                          ((lda | sA | ldb | sB | (int64_t)M | (int64_t)N | (int64_t)K) & 1) == 0;
+        static const bool v16_env = [] {
+            const char* e = getenv("UOTK_GEMM_V16");
+            return !(e && e[0] == '0');
+        }();
+        // (64 x 64 x 32 and 128 x 64 x 16 three-stage variants measured 1.38 / 1.35 ms)
+        if (even && v16_env) launch_gemm_v16<64, 64, 16>(g, batch, s);
+        else launch_gemm<64, 64, 16, 2>(g, batch, s);
+    }
 }
 
 }  // namespace

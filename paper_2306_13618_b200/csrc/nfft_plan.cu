@@ -231,8 +231,10 @@ FastParams choose_params(int d, int kind, double param, const Geometry& g, const
     {
         // grid coordinates u in [-Rc, Rc] around index n_g/2; taps floor(u) - m + 1 .. floor(u) + m
         const int Rc = (int)std::ceil(Rbar * ng) + 1;
-        const int lo = std::max(0, ng / 2 - Rc - fp.m);
-        const int hi = std::min(ng, ng / 2 + Rc + fp.m + 1);
+        // even origin and width (ng is even): every box row starts 16-byte aligned, for the
+        // chain's 16-byte operand loads (circgemm.cu)
+        const int lo = std::max(0, ng / 2 - Rc - fp.m) & ~1;
+        const int hi = std::min(ng, (ng / 2 + Rc + fp.m + 1 + 1) & ~1);
         fp.box_lo = lo;
         fp.box_w = hi - lo;
     }
