@@ -7,9 +7,9 @@
 // tensor cores: mma.sync m8n8k4 f64 (SASS DMMA), 64 x 64 output tiles per 128-thread CTA
 // (2 x 2 warps of 32 x 32), K in steps of 16 through a double-buffered cp.async pipeline
 // (8-byte copies; a 3-stage ring of 16-byte copies when the rows are 16-byte aligned, as
-// they are on the even-aligned footprint box), zero-filled at the ragged edges.  The last pass also zeroes the footprint box of the
-// grid the next spread writes into (a disjoint buffer), which replaces a full-grid memset
-// per half-step.
+// they are on the even-aligned footprint box), zero-filled at the ragged edges.  The last
+// pass also zeroes the footprint box of the grid the next spread writes into (a disjoint
+// buffer), which replaces a full-grid memset per half-step.
 #include "common.cuh"
 #include "profile.cuh"
 #include "ptx.cuh"
