@@ -314,11 +314,19 @@ __global__ void unpack_cols_k(const double* __restrict__ all, int w, int wb, int
 }
 }  // namespace
 
-// doubles of the chain's work buffer for a (P-rank) chain
-size_t separable_work_elems(const FastParams& fp, int P) {
+static bool dist_chain_enabled();
+static int dist_chain_mode();
+// the chain runs slab-distributed (reduce-scatter / middle pass on 1/P / all-gather)
+static bool chain_distributed(void* comm) {
+    return comm && dist_chain_enabled() && (comm_nranks(comm) > 1 || dist_chain_mode() == 2);
+}
+
+// doubles of the chain's work buffer
+size_t separable_work_elems(const FastParams& fp, void* comm) {
     const size_t w = fp.box_w;
+    const int P = comm_nranks(comm);
     if (fp.d == 1) return w;
-    if (P <= 1) return fp.d == 2 ? w * w : w * w * w;
+    if (!chain_distributed(comm)) return fp.d == 2 ? w * w : w * w * w;
     if (fp.d == 2) {
         const size_t wb = (w + P - 1) / P;
         return (2 * (size_t)P + 2) * w * wb;
@@ -327,13 +335,17 @@ size_t separable_work_elems(const FastParams& fp, int P) {
     return ((size_t)P + 2) * xb * w * w;
 }
 
-static bool dist_chain_enabled() {
-    static const bool on = [] {
+// UOTK_DIST_CHAIN: 0 = one all-reduce of the first pass's box instead of the slab split;
+// 2 = the slab split even on a 1-rank communicator (tests the reduce-scatter / all-gather
+// calls of a real NCCL communicator on one GPU)
+static int dist_chain_mode() {
+    static const int mode = [] {
         const char* e = getenv("UOTK_DIST_CHAIN");
-        return !(e && e[0] == '0');
+        return e ? atoi(e) : 1;
     }();
-    return on;
+    return mode;
 }
+static bool dist_chain_enabled() { return dist_chain_mode() != 0; }
 
 // g' = (Csep x ... x Csep) g on the footprint box (spread grid g: zero outside the box).
 // Returns the buffer holding g' at the box positions (`spare`, n_g^d doubles).  `work`
@@ -362,7 +374,8 @@ double* separable_chain_dmma(const FastParams& fp, const double* Csep, double* g
         return spare;
     }
     const int P = comm_nranks(comm);
-    if (d == 2 && P > 1 && dist_chain_enabled()) {
+    const bool dist = chain_distributed(comm);
+    if (d == 2 && dist) {
         // slab-distributed: the y-pass of each rank's own spread, written as
         // P column blocks of width wb; a reduce-scatter gives rank r the global block r; the
         // x-pass of that block only (1/P of the work); an all-gather of the output blocks
@@ -388,7 +401,7 @@ double* separable_chain_dmma(const FastParams& fp, const double* Csep, double* g
         UOTK_LAUNCHED();
         return spare;
     }
-    if (d == 3 && P > 1 && dist_chain_enabled() && (int64_t)P * ((w + P - 1) / P) * w2 <= n2 * n) {
+    if (d == 3 && dist && (int64_t)P * ((w + P - 1) / P) * w2 <= n2 * n) {
         // slab-distributed: the z-pass of each rank's own spread (all x-planes), a
         // reduce-scatter of x-plane blocks, the y-pass of rank r's planes only, an all-gather
         // of those planes, the x-pass (replicated).  T1 (P xb planes) sits compact in spare (its

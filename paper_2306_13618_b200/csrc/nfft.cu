@@ -371,7 +371,7 @@ void gather(const PointSet& ps, const double* grid, double* out_sorted, const Fa
 
 int comm_nranks(void* comm);  // comm.cu
 
-size_t separable_work_elems(const FastParams& fp, int P);  // circgemm.cu
+size_t separable_work_elems(const FastParams& fp, void* comm);  // circgemm.cu
 // Separable chain (Gaussian kernel): circgemm.cu, hand-written DMMA GEMM passes on the box
 double* separable_chain_dmma(const FastParams& fp, const double* Csep, double* grid, double* spare, double* work,
                              double* zero_next, cudaStream_t s, void* comm);
@@ -384,7 +384,7 @@ double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s,
     const FastParams& fp = sp.fp;
     if (zeroed) *zeroed = false;
     if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT)) {
-        const size_t wd = separable_work_elems(fp, comm_nranks(comm));
+        const size_t wd = separable_work_elems(fp, comm);
         if (sp.work.n < wd) sp.work.alloc(wd, s);
         if (fp.d == 1 && zero_next == grid) zero_next = nullptr;  // d = 1: one pass, still reading it
         if (zeroed) *zeroed = zero_next != nullptr;

@@ -286,6 +286,41 @@ def test_one_rank_nccl_communicator_matches(uk):
         comm.close()
 
 
+def test_one_rank_nccl_slab_chain_collectives():
+    """The slab-distributed separable chain's NCCL reduce-scatter and all-gather on a real
+    (1-rank) NCCL communicator: UOTK_DIST_CHAIN=2 takes the slab path even with one rank
+    (the collectives are copies then), in a subprocess because the switch is read once.
+    Kernel sums d = 2, 3 and a short C3-like solve must equal the communicator-free run."""
+    import subprocess, sys, os, textwrap
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    code = textwrap.dedent("""
+        import numpy as np, torch, paper_2306_13618_b200 as uk, workloads as W
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        comm = uk.Comm(uk.Comm.unique_id(), 1, 0)
+        worst = 0.0
+        for d in (2, 3):
+            pr = W.random_sum(d, 3001, 1999, kind=W.GAUSS, param=0.0025, seed=40 + d)
+            a = uk.kernel_sum(t(pr.src), t(pr.alpha), t(pr.tgt), "gauss", pr.param, opts={"method": "nfft"})
+            b = uk.kernel_sum(t(pr.src), t(pr.alpha), t(pr.tgt), "gauss", pr.param, opts={"method": "nfft"}, comm=comm)
+            worst = max(worst, float(torch.max(torch.abs(a - b)) / torch.max(torch.abs(a))))
+        u = W.c3_uot(n=1500, m=1300, iters=5)
+        r1 = uk.uot_sinkhorn(t(u.x), t(u.a), t(u.y), t(u.b), u.eps, u.lam, iters=5, opts={"method": "nfft"})
+        r2 = uk.uot_sinkhorn(t(u.x), t(u.a), t(u.y), t(u.b), u.eps, u.lam, iters=5, opts={"method": "nfft"}, comm=comm)
+        worst = max(worst, float(torch.max(torch.abs(r1[0] - r2[0])) / torch.max(torch.abs(r1[0]))))
+        worst = max(worst, abs(r1[2].primal - r2[2].primal) / abs(r1[2].primal))
+        comm.close()
+        print("WORST", worst)
+    """)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, UOTK_DIST_CHAIN="2", PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    worst = float(out.stdout.split("WORST")[-1])
+    assert worst <= 1e-13, worst
+
+
 # ------------------------------------------------------------------ full-size cross-checks
 def test_uot_c3_full_size_nfft_vs_direct(uk):
     """C3 at full size (n = m = 1e6): the NFFT path as bench.py runs it against the GPU
