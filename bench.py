@@ -430,7 +430,9 @@ def main_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
+    # UOTK_BENCH_COMM=1: the NCCL communicator path also at one rank (a check of the
+    # multi-GPU code path on a one-GPU box; with UOTK_DIST_CHAIN=2 including the slab chain)
+    if world > 1 or os.environ.get("UOTK_BENCH_COMM") == "1":
         os.environ.setdefault("UOTK_COMM_VERBOSE", "1")  # one stderr line per rank: rank / nranks / device
         dist.init_process_group("nccl", device_id=dev)
         comm = uk.Comm.from_torch_distributed()
@@ -505,7 +507,7 @@ def main_ours(args):
                                            "h": res.info["h"], "groups": res.info["groups"],
                                            "parallelism": f"points sharded x{world} (cell-ordered blocks)",
                                            "comm": {"nranks": res.info["nranks"],
-                                                    "backend": "nccl" if world > 1 else None},
+                                                    "backend": "nccl" if comm is not None else None},
                                            "l2": "flushed between steps (256 MB write outside the events)"}),
             "gpu_launches": launches,
             "step_ms": [round(v, 3) for v in step_ms],
@@ -520,7 +522,7 @@ def main_ours(args):
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
