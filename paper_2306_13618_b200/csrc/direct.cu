@@ -132,6 +132,9 @@ __global__ void __launch_bounds__(WT) direct_warp_k(int64_t n_src, const double*
     const int64_t i = blockIdx.x * (int64_t)(WT / 32) + (threadIdx.x >> 5);
     double xi[D];
     for (int t = 0; t < D; ++t) xi[t] = i < n_tgt ? tgt[i * D + t] : 0.0;
+    // the epilogue's per-target inputs, loaded now (their latency hides behind the pair loop)
+    typename Epi::In ein{};
+    if (lane == 0 && i < n_tgt) ein = epi.load(i);
     double acc = 0.0;
     for (int64_t jt = 0; jt < n_src; jt += kWTile) {
         const int cnt = (int)((n_src - jt) < kWTile ? (n_src - jt) : kWTile);
@@ -162,7 +165,8 @@ __global__ void __launch_bounds__(WT) direct_warp_k(int64_t n_src, const double*
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     double dd = 0.0;
-    if (lane == 0 && i < n_tgt) dd = epi(i, acc);
+    double wn;
+    if (lane == 0 && i < n_tgt) dd = epi.apply(i, acc, ein, wn);
     warp_max_atomic(dmax, dd);
 }
 
