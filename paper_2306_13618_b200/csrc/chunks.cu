@@ -60,11 +60,18 @@ __global__ void chunk_desc_k(const int32_t* __restrict__ run_key, const int32_t*
 constexpr int kWinWarps = 4;
 constexpr int kMaxRow = 44;  // widest row stride (d = 3, KZ = 40)
 
+// widest row of a (D, KZ) block: the staging buffer is sized by it (not by kMaxRow), so
+// the common blocks leave room for more resident warps
+__host__ __device__ constexpr int win_row_max(int d, int kz) {
+    return d == 3 ? (chunk_zstride3(kz) > chunk_xstride3(kz) ? chunk_zstride3(kz) : chunk_xstride3(kz))
+                  : (d == 2 ? (chunk_ystride2(kz) > kChunkT ? chunk_ystride2(kz) : kChunkT) : kChunkT);
+}
 template <int D, int KZ>
 __global__ void __launch_bounds__(kWinWarps * 32)
 chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u, const int32_t* __restrict__ key,
                     int64_t n, int64_t nchunks, KBHorner hc, double* __restrict__ out) {
-    __shared__ double stage[kWinWarps][kChunk * kMaxRow];
+    static_assert(win_row_max(D, KZ) <= kMaxRow, "window row wider than the staging bound");
+    __shared__ double stage[kWinWarps][kChunk * win_row_max(D, KZ)];
     constexpr int kW = D == 3 ? chunk_win3_doubles(KZ) : (D == 2 ? chunk_win2_doubles(KZ) : chunk_win_doubles(D));
     constexpr bool YSEG = D == 2 && KZ == 24;  // d = 2 y-segment rows (chunks.cuh)
     const int lane = threadIdx.x & 31;
@@ -93,14 +100,20 @@ chunk_window_rows_k(const int4* __restrict__ desc, const double* __restrict__ u,
     // each a degree-14 polynomial in f - 1/2 (window_fit.h)
     for (int col = 0; col < stride; ++col) st[p * stride + col] = 0.0;
     if (live) {
+        // mirror pairs a, TAPS - 1 - a: phi is even, so the mirror tap is tap a's polynomial
+        // at -t — the even and odd halves in t^2 give both (15 FMA per pair instead of 28)
         constexpr int TAPS = (D == 3 && KZ == 12) ? 12 : kChunkT;
-        const double t = f - 0.5;
+        const double t = f - 0.5, t2 = t * t;
+        auto col = [&](int a) { return (D == 2 && !(YSEG && ax == 1)) ? swz2(p, a) : a + off; };
 #pragma unroll
-        for (int a = 0; a < TAPS; ++a) {
-            double v = hc.c[a][kHornerDeg];
+        for (int a = 0; a < TAPS / 2; ++a) {
+            double e = hc.c[a][kHornerDeg], o = hc.c[a][kHornerDeg - 1];
 #pragma unroll
-            for (int j = kHornerDeg - 1; j >= 0; --j) v = fma(v, t, hc.c[a][j]);
-            st[p * stride + ((D == 2 && !(YSEG && ax == 1)) ? swz2(p, a) : a + off)] = v;
+            for (int j = kHornerDeg - 2; j >= 0; j -= 2) e = fma(e, t2, hc.c[a][j]);
+#pragma unroll
+            for (int j = kHornerDeg - 3; j >= 1; j -= 2) o = fma(o, t2, hc.c[a][j]);
+            st[p * stride + col(a)] = fma(t, o, e);
+            st[p * stride + col(TAPS - 1 - a)] = fma(-t, o, e);
         }
     }
     __syncwarp();

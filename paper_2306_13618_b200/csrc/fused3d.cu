@@ -678,45 +678,49 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
         mbar_init_fence();
     }
     __syncthreads();
-    // this thread's taps of a block: tap a = tid & 15 of the 6 rows r = (tid >> 4) + 16 i of
-    // [axis 3 x slot 32]; the tap's 15 polynomial coefficients stay in registers
-    const int fa = tid & 15, frow = tid >> 4;
-    double hcr[kHornerDeg + 1];
+    // this thread's taps of a block: the mirror pair a = tid & 7 and 15 - a (phi is even, so
+    // phi at tap 15 - a is tap a's polynomial at -t: the even and odd halves in t^2 give
+    // both, 15 FMA per pair instead of 28) of point p = tid >> 3, all three axes; the pair's
+    // 15 coefficients stay in registers
+    const int fa = tid & 7, frow = tid >> 3;
+    double he[kHornerDeg / 2 + 1], ho[kHornerDeg / 2];
 #pragma unroll
-    for (int q = 0; q <= kHornerDeg; ++q) hcr[q] = hcoef.c[fa][q];
+    for (int q = 0; q <= kHornerDeg / 2; ++q) he[q] = hcoef.c[fa][2 * q];
+#pragma unroll
+    for (int q = 0; q < kHornerDeg / 2; ++q) ho[q] = hcoef.c[fa][2 * q + 1];
     // the coordinates of the next block to fill are loaded one fill ahead (their L2 latency
     // then overlaps a chunk of DMMAs instead of stalling the fill)
-    double uf[6];
+    double uf[3];
     int cntf = 0;
     auto load_rows = [&](int64_t j) {
         const int4 dj = j < nck ? desc[cbeg + j] : make_int4(0, 0, 0, 0);
         cntf = dj.y;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            const int r = frow + 16 * i;
-            const int ax = r >> 5, p = r & 31;
-            uf[i] = p < dj.y ? u[(int64_t)ax * n + dj.x + p] : 0.0;
-        }
+        for (int ax = 0; ax < 3; ++ax) uf[ax] = frow < dj.y ? u[(int64_t)ax * n + dj.x + frow] : 0.0;
     };
     auto fill = [&](int64_t j) {
         const int slot = (int)(j % kRingF);
-        double t[6];
+        double t[3];
         int cnt = cntf;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) t[i] = uf[i] - floor(uf[i]) - 0.5;
+        for (int ax = 0; ax < 3; ++ax) t[ax] = uf[ax] - floor(uf[ax]) - 0.5;
         load_rows(j + 1);
         if (j >= kRingF) mbar_wait(&sm.empty[slot], (uint32_t)(((j - kRingF) / kRingF) & 1));
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            const int r = frow + 16 * i;
-            const int ax = r >> 5, p = r & 31;
-            double v = 0.0;
-            if (p < cnt) {
-                v = hcr[kHornerDeg];
+        for (int ax = 0; ax < 3; ++ax) {
+            double v1 = 0.0, v2 = 0.0;
+            if (frow < cnt) {
+                const double t2 = t[ax] * t[ax];
+                double e = he[kHornerDeg / 2], o = ho[kHornerDeg / 2 - 1];
 #pragma unroll
-                for (int q = kHornerDeg - 1; q >= 0; --q) v = fma(v, t[i], hcr[q]);
+                for (int q = kHornerDeg / 2 - 1; q >= 0; --q) e = fma(e, t2, he[q]);
+#pragma unroll
+                for (int q = kHornerDeg / 2 - 2; q >= 0; --q) o = fma(o, t2, ho[q]);
+                v1 = fma(t[ax], o, e);
+                v2 = fma(-t[ax], o, e);
             }
-            sm.win[slot][ax][p][fa] = v;
+            sm.win[slot][ax][frow][fa] = v1;
+            sm.win[slot][ax][frow][kChunkT - 1 - fa] = v2;
         }
         mbar_arrive(&sm.full[slot]);
     };
