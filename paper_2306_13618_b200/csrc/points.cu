@@ -127,15 +127,13 @@ __global__ void max_final_k(const double* part, int nb, double* out) {
 // scaled grid coordinates (SoA) + cell key + identity index
 template <int D>
 __global__ void scale_key_k(const double* __restrict__ pts, int64_t n, double c0, double c1, double c2,
-                            double scale, int ng, double* __restrict__ u, int32_t* __restrict__ key,
-                            int32_t* __restrict__ idx) {
+                            double scale, int ng, int32_t* __restrict__ key, int32_t* __restrict__ idx) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double c[3] = {c0, c1, c2};
     int32_t k = 0;
     for (int t = 0; t < D; ++t) {
-        double v = (pts[i * D + t] - c[t]) * scale;
-        u[t * n + i] = v;
+        const double v = (pts[i * D + t] - c[t]) * scale;
         int cell = (int)floor(v) + ng / 2;
         k = k * ng + cell;
     }
@@ -144,12 +142,16 @@ __global__ void scale_key_k(const double* __restrict__ pts, int64_t n, double c0
 }
 
 template <int D>
-__global__ void gather_u_k(const double* __restrict__ u_in, const int32_t* __restrict__ perm, int64_t n,
-                           double* __restrict__ u_out) {
+// sorted SoA torus coordinates, recomputed from the caller's row-major points (the same
+// expression as scale_key_k, so the cell of u is the sorted key): one point's D contiguous
+// doubles per random read instead of D scattered ones
+__global__ void gather_u_k(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t n, double c0,
+                           double c1, double c2, double scale, double* __restrict__ u_out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int64_t j = perm[i];
-    for (int t = 0; t < D; ++t) u_out[t * n + i] = u_in[t * n + j];
+    const double c[3] = {c0, c1, c2};
+    const int64_t j = perm[i];
+    for (int t = 0; t < D; ++t) u_out[t * n + i] = (pts[j * D + t] - c[t]) * scale;
 }
 
 __global__ void permute_k(double* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ perm,
@@ -214,14 +216,13 @@ void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams&
     ps.perm.alloc(n, s);
     if (n == 0) return;
     if (n > INT32_MAX) fail(UOTK_EUNSUPPORTED, "more than 2^31-1 points per call");
-    DevBuf<double> u0((size_t)d * n, s);
     DevBuf<int32_t> key0(n, s), idx0(n, s);
     const int tb = 256;
     const double scale = fp.ng / fp.h;
     const double* c = fp.center;
-    if (d == 1) scale_key_k<1><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], 0, 0, scale, fp.ng, u0.p, key0.p, idx0.p);
-    else if (d == 2) scale_key_k<2><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], c[1], 0, scale, fp.ng, u0.p, key0.p, idx0.p);
-    else scale_key_k<3><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], c[1], c[2], scale, fp.ng, u0.p, key0.p, idx0.p);
+    if (d == 1) scale_key_k<1><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], 0, 0, scale, fp.ng, key0.p, idx0.p);
+    else if (d == 2) scale_key_k<2><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], c[1], 0, scale, fp.ng, key0.p, idx0.p);
+    else scale_key_k<3><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], c[1], c[2], scale, fp.ng, key0.p, idx0.p);
     UOTK_LAUNCHED();
     int end_bit = 1;
     double cells = std::pow((double)fp.ng, d);
@@ -234,9 +235,9 @@ void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams&
                                               end_bit, s));
     add_launches(1 + (end_bit + 7) / 8);  // CUB onesweep: histogram + one pass per 8 key bits
     trace_mark("pointset: sort");
-    if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
-    else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
-    else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(u0.p, ps.perm.p, n, ps.u.p);
+    if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(pts, ps.perm.p, n, c[0], 0, 0, scale, ps.u.p);
+    else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(pts, ps.perm.p, n, c[0], c[1], 0, scale, ps.u.p);
+    else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(pts, ps.perm.p, n, c[0], c[1], c[2], scale, ps.u.p);
     UOTK_LAUNCHED();
     chunked_prepare(ps, fp, s, use);  // chunk list + precomputed windows (tuned cell-group kernels)
 }
