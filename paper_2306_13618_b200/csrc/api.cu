@@ -733,11 +733,8 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     Y.bind(y, (size_t)m * d, s);
     B.bind(b, (size_t)m, s);
     const int64_t nz = n + m;
-    // z = x u y (row-major), w = (a, -b): MMD^2 = sum_i w_i (K w)_i  (3.5)
-    DevBuf<double> z((size_t)nz * d, s), w(nz, s), prod(nz, s), sum(1, s);
-    if (n) UOTK_CUDA(cudaMemcpyAsync(z.p, X.d, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (m) UOTK_CUDA(cudaMemcpyAsync(z.p + (size_t)n * d, Y.d, (size_t)m * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    signed_concat(A.d, n, B.d, m, w.p, s);
+    // z = x u y, w = (a, -b): MMD^2 = sum_i w_i (K w)_i  (3.5)
+    DevBuf<double> prod(nz, s), sum(1, s);
     const int method = pick_method(o, (double)nz * (double)nz, comm, direct_crossover_sum(d, kind));
     if (nz == 0 && comm_nranks(comm) == 1) {  // with several ranks an empty shard still takes part
         fill_info(info, method, nullptr, comm);
@@ -746,6 +743,10 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     }
     if (method == UOTK_DIRECT) {
         fill_info(info, method, nullptr, comm);
+        DevBuf<double> z((size_t)nz * d, s), w(nz, s);
+        if (n) UOTK_CUDA(cudaMemcpyAsync(z.p, X.d, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (m) UOTK_CUDA(cudaMemcpyAsync(z.p + (size_t)n * d, Y.d, (size_t)m * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        signed_concat(A.d, n, B.d, m, w.p, s);
         DevBuf<int> flag(1, s);
         flag.zero();
         check_finite(z.p, nz * d, flag.p, 8, s);
@@ -755,16 +756,18 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
     } else {
         // spread w on the grid, FFT, and sum_k D_k |G_k|^2 (= sum_i w_i t_i of the gather
         // form exactly; no inverse FFT or interpolation needed).  With a communicator the
-        // spectrum is all-reduced first, so every rank forms the same global value.
+        // spectrum is all-reduced first, so every rank forms the same global value.  The
+        // point set is x u y read in place (no concatenated copy); its weights are
+        // gathered from a and -b in sorted order.
         NfftSetup ns;
-        setup_nfft(ns, d, kind, param, z.p, nz, nullptr, 0, o, comm, s);
+        setup_nfft(ns, d, kind, param, X.d, n, Y.d, m, o, comm, s);
         PointSet PZ;
-        make_pointset(PZ, z.p, nz, ns.fp, s, kUseSpreadOnly);
+        make_pointset(PZ, X.d, n, Y.d, m, ns.fp, s, kUseSpreadOnly);
         fill_info(info, method, &ns.fp, comm, &PZ);
         constexpr int kParts = 296;
         DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s), part(kParts, s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
-        permute_values(ws.p, w.p, PZ.perm.p, nz, s);
+        permute_signed(ws.p, A.d, n, B.d, PZ.perm.p, nz, s);
         grid.zero();
         spread(PZ, ws.p, grid.p, ns.fp, s);
         if (ns.sp.pd->separable && !(ns.fp.flags & UOTK_FLAG_FFT)) {

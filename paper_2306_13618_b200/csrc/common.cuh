@@ -221,8 +221,13 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
 // use: what the point set will be used for (the chunk layout is skipped where no kernel
 // would use it: gather-only d = 3 sets below kGatherMinFill3)
 enum PointUse { kUseBoth = 0, kUseGatherOnly = 1, kUseSpreadOnly = 2 };
-void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
-                   PointUse use = kUseBoth);
+// the set is p1 (n1 points) followed by p2 (n2 points; may be null when n2 = 0)
+void make_pointset(PointSet& ps, const double* p1, int64_t n1, const double* p2, int64_t n2, const FastParams& fp,
+                   cudaStream_t s, PointUse use = kUseBoth);
+inline void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
+                          PointUse use = kUseBoth) {
+    make_pointset(ps, pts, n, nullptr, 0, fp, s, use);
+}
 void permute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
 void unpermute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
 

@@ -124,20 +124,35 @@ __global__ void max_final_k(const double* part, int nb, double* out) {
     if (threadIdx.x == 0) out[0] = sm[0];
 }
 
+// the caller's point i of the set p1 (n1 points) u p2, row-major
+template <int D>
+__device__ __forceinline__ const double* point_ptr(const double* p1, int64_t n1, const double* p2, int64_t i) {
+    return i < n1 ? p1 + i * D : p2 + (i - n1) * D;
+}
+
+// the cell key of a point: floor of its grid coordinate (x_t - c_t) * scale per axis,
+// x-major.  gather_u_k writes u with the same expression, so the cell of u is
+// the key.
+template <int D>
+__device__ __forceinline__ int32_t cell_key(const double* q, const double (&c)[3], double scale, int ng) {
+    int32_t k = 0;
+    for (int t = 0; t < D; ++t) {
+        const double v = (q[t] - c[t]) * scale;
+        const int cell = (int)floor(v) + ng / 2;
+        k = k * ng + cell;
+    }
+    return k;
+}
+
 // scaled grid coordinates (SoA) + cell key + identity index
 template <int D>
-__global__ void scale_key_k(const double* __restrict__ pts, int64_t n, double c0, double c1, double c2,
-                            double scale, int ng, int32_t* __restrict__ key, int32_t* __restrict__ idx) {
+__global__ void scale_key_k(const double* __restrict__ p1, int64_t n1, const double* __restrict__ p2, int64_t n,
+                            double c0, double c1, double c2, double scale, int ng, int32_t* __restrict__ key,
+                            int32_t* __restrict__ idx) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double c[3] = {c0, c1, c2};
-    int32_t k = 0;
-    for (int t = 0; t < D; ++t) {
-        const double v = (pts[i * D + t] - c[t]) * scale;
-        int cell = (int)floor(v) + ng / 2;
-        k = k * ng + cell;
-    }
-    key[i] = k;
+    key[i] = cell_key<D>(point_ptr<D>(p1, n1, p2, i), c, scale, ng);
     idx[i] = (int32_t)i;
 }
 
@@ -145,13 +160,14 @@ template <int D>
 // sorted SoA torus coordinates, recomputed from the caller's row-major points (the same
 // expression as scale_key_k, so the cell of u is the sorted key): one point's D contiguous
 // doubles per random read instead of D scattered ones
-__global__ void gather_u_k(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t n, double c0,
-                           double c1, double c2, double scale, double* __restrict__ u_out) {
+__global__ void gather_u_k(const double* __restrict__ p1, int64_t n1, const double* __restrict__ p2,
+                           const int32_t* __restrict__ perm, int64_t n, double c0, double c1, double c2, double scale,
+                           double* __restrict__ u_out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double c[3] = {c0, c1, c2};
-    const int64_t j = perm[i];
-    for (int t = 0; t < D; ++t) u_out[t * n + i] = (pts[j * D + t] - c[t]) * scale;
+    const double* q = point_ptr<D>(p1, n1, p2, perm[i]);
+    for (int t = 0; t < D; ++t) u_out[t * n + i] = (q[t] - c[t]) * scale;
 }
 
 __global__ void permute_k(double* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ perm,
@@ -205,10 +221,11 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
     return g;
 }
 
-void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
-                   PointUse use) {
+void make_pointset(PointSet& ps, const double* p1, int64_t n1, const double* p2, int64_t n2, const FastParams& fp,
+                   cudaStream_t s, PointUse use) {
     NvtxRange nvtx_("pointset");
     const int d = fp.d;
+    const int64_t n = n1 + n2;
     ps.d = d;
     ps.n = n;
     ps.u.alloc((size_t)d * n, s);
@@ -216,29 +233,31 @@ void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams&
     ps.perm.alloc(n, s);
     if (n == 0) return;
     if (n > INT32_MAX) fail(UOTK_EUNSUPPORTED, "more than 2^31-1 points per call");
-    DevBuf<int32_t> key0(n, s), idx0(n, s);
     const int tb = 256;
     const double scale = fp.ng / fp.h;
     const double* c = fp.center;
-    if (d == 1) scale_key_k<1><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], 0, 0, scale, fp.ng, key0.p, idx0.p);
-    else if (d == 2) scale_key_k<2><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], c[1], 0, scale, fp.ng, key0.p, idx0.p);
-    else scale_key_k<3><<<blocks_for(n, tb), tb, 0, s>>>(pts, n, c[0], c[1], c[2], scale, fp.ng, key0.p, idx0.p);
-    UOTK_LAUNCHED();
-    int end_bit = 1;
-    double cells = std::pow((double)fp.ng, d);
-    while ((double)(1ull << end_bit) < cells) ++end_bit;
-    size_t tmp_bytes = 0;
-    UOTK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key0.p, ps.key.p, idx0.p, ps.perm.p, (int)n, 0,
-                                              end_bit, s));
-    DevBuf<uint8_t> tmp(tmp_bytes, s);
-    UOTK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key0.p, ps.key.p, idx0.p, ps.perm.p, (int)n, 0,
-                                              end_bit, s));
-    add_launches(1 + (end_bit + 7) / 8);  // CUB onesweep: histogram + one pass per 8 key bits
-    trace_mark("pointset: sort");
-    if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(pts, ps.perm.p, n, c[0], 0, 0, scale, ps.u.p);
-    else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(pts, ps.perm.p, n, c[0], c[1], 0, scale, ps.u.p);
-    else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(pts, ps.perm.p, n, c[0], c[1], c[2], scale, ps.u.p);
-    UOTK_LAUNCHED();
+    const double cells = std::pow((double)fp.ng, d);
+    {
+        DevBuf<int32_t> key0(n, s), idx0(n, s);
+        if (d == 1) scale_key_k<1><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, n, c[0], 0, 0, scale, fp.ng, key0.p, idx0.p);
+        else if (d == 2) scale_key_k<2><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, n, c[0], c[1], 0, scale, fp.ng, key0.p, idx0.p);
+        else scale_key_k<3><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, n, c[0], c[1], c[2], scale, fp.ng, key0.p, idx0.p);
+        UOTK_LAUNCHED();
+        int end_bit = 1;
+        while ((double)(1ull << end_bit) < cells) ++end_bit;
+        size_t tmp_bytes = 0;
+        UOTK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key0.p, ps.key.p, idx0.p, ps.perm.p, (int)n, 0,
+                                                  end_bit, s));
+        DevBuf<uint8_t> tmp(tmp_bytes, s);
+        UOTK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key0.p, ps.key.p, idx0.p, ps.perm.p, (int)n, 0,
+                                                  end_bit, s));
+        add_launches(1 + (end_bit + 7) / 8);  // CUB onesweep: histogram + one pass per 8 key bits
+        trace_mark("pointset: sort");
+        if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], 0, 0, scale, ps.u.p);
+        else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], c[1], 0, scale, ps.u.p);
+        else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], c[1], c[2], scale, ps.u.p);
+        UOTK_LAUNCHED();
+    }
     chunked_prepare(ps, fp, s, use);  // chunk list + precomputed windows (tuned cell-group kernels)
 }
 

@@ -97,6 +97,16 @@ __global__ void scaled_mass_k(const double* __restrict__ mass, const double* __r
     if (i < n) w[i] = pot ? mass[i] * exp(lam * pot[i]) : mass[i];
 }
 
+// ws[i] = w[perm[i]] with w = (a, -b): MMD^2's signed weights in sorted order, read from
+// the caller's two arrays
+__global__ void permute_signed_k(double* __restrict__ ws, const double* __restrict__ a, int64_t n,
+                                 const double* __restrict__ b, const int32_t* __restrict__ perm, int64_t nz) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nz) return;
+    const int64_t j = perm[i];
+    ws[i] = j < n ? a[j] : -b[j - n];
+}
+
 __global__ void signed_concat_k(const double* __restrict__ a, int64_t n, const double* __restrict__ b, int64_t m,
                                 double* __restrict__ w) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -191,6 +201,13 @@ void join_bits(const int32_t* bits, int* flag, cudaStream_t s) {
 void scaled_mass(const double* mass, const double* pot, int64_t n, double lam, double* w, cudaStream_t s) {
     if (n == 0) return;
     scaled_mass_k<<<blocks_for(n, 256), 256, 0, s>>>(mass, pot, n, lam, w);
+    UOTK_LAUNCHED();
+}
+
+void permute_signed(double* ws, const double* a, int64_t n, const double* b, const int32_t* perm, int64_t nz,
+                    cudaStream_t s) {
+    if (nz == 0) return;
+    permute_signed_k<<<blocks_for(nz, 256), 256, 0, s>>>(ws, a, n, b, perm, nz);
     UOTK_LAUNCHED();
 }
 

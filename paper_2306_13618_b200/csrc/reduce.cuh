@@ -21,6 +21,8 @@ void scaled_mass(const double* mass, const double* pot, int64_t n, double lam, d
 void moment_cols(const double* x, const double* a, int64_t n, int d, const double* c, double* cols, cudaStream_t s);
 // prod[i] = a[i] * b[i]
 void multiply(const double* a, const double* b, int64_t n, double* prod, cudaStream_t s);
+void permute_signed(double* ws, const double* a, int64_t n, const double* b, const int32_t* perm, int64_t nz,
+                    cudaStream_t s);
 void signed_concat(const double* a, int64_t n, const double* b, int64_t m, double* w, cudaStream_t s);
 
 }  // namespace uotk
