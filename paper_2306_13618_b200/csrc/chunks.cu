@@ -5,6 +5,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -131,12 +133,14 @@ __global__ void segment_key_k(const int32_t* __restrict__ key, int64_t n, int ng
     }
 }
 
-// cost of a chunk for the static partition: 8 per chunk + g when it opens a cell group
-// (footprint load and flush), in units of 1/8 chunk
-__global__ void chunk_cost_k(const int4* __restrict__ desc, int64_t nchunks, int group_cost,
+// cost of a chunk for the static partition: fix per chunk + step per 4-point k-step of its
+// points (the kernels skip the steps past a chunk's count) + group when it opens a cell
+// group (footprint load and flush)
+__global__ void chunk_cost_k(const int4* __restrict__ desc, int64_t nchunks, int fix, int step, int group,
                              int32_t* __restrict__ cost) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < nchunks) cost[c] = 8 + ((c == 0 || desc[c].z != desc[c - 1].z) ? group_cost : 0);
+    if (c < nchunks)
+        cost[c] = fix + step * ((desc[c].y + 3) >> 2) + ((c == 0 || desc[c].z != desc[c - 1].z) ? group : 0);
 }
 
 // bounds[b] = first chunk whose inclusive cost prefix exceeds b * total / nb
@@ -386,9 +390,12 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
         UOTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const bool m6 = d == 3 && fp.m == 6;
-    const int nb = (int)std::min<int64_t>((int64_t)sms * (m6 ? kCtas3M6 : chunk_units_per_sm(d)), nchunks);
+    const int nb = (int)std::min<int64_t>(
+        (int64_t)sms * (m6 ? kCtas3M6 : (fly ? kCtasFly3 : chunk_units_per_sm(d))), nchunks);
     DevBuf<int32_t> cost(nchunks, s), prefix(nchunks, s);
-    chunk_cost_k<<<blocks_for(nchunks, 256), 256, 0, s>>>(ps.chunk_desc.p, nchunks, d == 3 ? 2 : 1, cost.p);
+    int cfix = 8, cstep = 0, cgroup = d == 3 ? 2 : 1;
+    if (const char* e = getenv("UOTK_COST")) sscanf(e, "%d,%d,%d", &cfix, &cstep, &cgroup);  // A/B only
+    chunk_cost_k<<<blocks_for(nchunks, 256), 256, 0, s>>>(ps.chunk_desc.p, nchunks, cfix, cstep, cgroup, cost.p);
     UOTK_LAUNCHED();
     size_t t4 = 0;
     UOTK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t4, cost.p, prefix.p, (int)nchunks, s));

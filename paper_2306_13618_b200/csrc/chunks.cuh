@@ -21,6 +21,8 @@ constexpr int kStride3 = 20;            // d = 3 padded row stride (doubles)
 // work units of the kernels: d = 3 one CTA (8 warps) per unit, kCtas3 CTAs per SM;
 // d <= 2 one warp per unit, kWarpsD warps per CTA, kCtasD CTAs per SM
 constexpr int kCtas3 = 2;
+// d = 3 spread-only sets with windows evaluated in the spread (fused3d.cu spread3d_fly_k)
+constexpr int kCtasFly3 = 2;
 constexpr int kWarps2 = 3, kCtas2 = 3;
 constexpr int kWarps1 = 8, kCtas1 = 2;
 // d = 2 warp-specialised Sinkhorn half-step: units of 2 gather warps + 1 spread warp,

@@ -648,14 +648,24 @@ spread3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
 // thread 6 of the 1536 taps (degree-14 polynomial per tap, window_fit.h; coefficients in
 // shared memory), released by an mbarrier all 256 threads arrive on; the eight warps
 // release a slot after their DMMAs (mbarrier, 8 arrivals) and the threads refill it.
+// The source weight is folded into the z row (B = w_p Z_p) when the row is evaluated, so
+// the DMMA loop forms only the A operand X_p[a] Y_p[b].  kCtasFly3 CTAs per SM (at most
+// 85 registers per thread).
 constexpr int kRingF = 4, kLeadF = 2;
+#ifndef UOTK_DIAG_FLY
+#define UOTK_DIAG_FLY 0  // timing diagnostics only: 1 skips the flushes, 2 the tap polynomials, 4 the DMMAs
+#endif
 struct __align__(128) SmemF {
     double win[kRingF][3][kChunk][kStride];
+    // even / odd Horner coefficients of tap pair (a, 15 - a), in t^2; a row stride of 10
+    // doubles puts the eight pairs' 16-byte reads in distinct banks
+    double he[8][10];
+    double ho[8][10];
     unsigned long long full[kRingF];
     unsigned long long empty[kRingF];
 };
 
-__global__ void __launch_bounds__(kThreads, kBlocksPerSM)
+__global__ void __launch_bounds__(kThreads, kCtasFly3)
 spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
                const int32_t* __restrict__ bounds, int ng, double* __restrict__ grid_out,
                const double* __restrict__ w_in, KBHorner hcoef) {
@@ -677,50 +687,76 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
         }
         mbar_init_fence();
     }
+    if (tid < 64) {
+        const int fa = tid >> 3, q = tid & 7;
+        sm.he[fa][q] = hcoef.c[fa][2 * q];
+        sm.ho[fa][q] = q < kHornerDeg / 2 ? hcoef.c[fa][2 * q + 1] : 0.0;
+    }
     __syncthreads();
     // this thread's taps of a block: the mirror pair a = tid & 7 and 15 - a (phi is even, so
     // phi at tap 15 - a is tap a's polynomial at -t: the even and odd halves in t^2 give
-    // both, 15 FMA per pair instead of 28) of point p = tid >> 3, all three axes; the pair's
-    // 15 coefficients stay in registers
-    const int fa = tid & 7, frow = tid >> 3;
-    double he[kHornerDeg / 2 + 1], ho[kHornerDeg / 2];
-#pragma unroll
-    for (int q = 0; q <= kHornerDeg / 2; ++q) he[q] = hcoef.c[fa][2 * q];
-#pragma unroll
-    for (int q = 0; q < kHornerDeg / 2; ++q) ho[q] = hcoef.c[fa][2 * q + 1];
-    // the coordinates of the next block to fill are loaded one fill ahead (their L2 latency
-    // then overlaps a chunk of DMMAs instead of stalling the fill)
-    double uf[3];
+    // both, 15 FMA per pair instead of 28) of point p = tid >> 3, all three axes
+    // lanes 0-15 of a warp take rows r, r + 2 and lanes 16-31 rows r + 1, r + 3 of its four:
+    // each half-warp's 8-byte stores then hit 16 distinct bank pairs (row stride 20)
+    const int fa = tid & 7, frow = 4 * warp + 2 * ((lane >> 3) & 1) + (lane >> 4);
+    // the coordinates and the weight of the next block to fill are loaded one fill ahead
+    // (their L2 latency then overlaps a chunk of DMMAs instead of stalling the fill)
+    double uf[3], wf = 0.0;
     int cntf = 0;
     auto load_rows = [&](int64_t j) {
         const int4 dj = j < nck ? desc[cbeg + j] : make_int4(0, 0, 0, 0);
         cntf = dj.y;
+        const bool live = frow < dj.y;
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) uf[ax] = frow < dj.y ? u[(int64_t)ax * n + dj.x + frow] : 0.0;
+        for (int ax = 0; ax < 3; ++ax) uf[ax] = live ? u[(int64_t)ax * n + dj.x + frow] : 0.0;
+        wf = live ? w_in[dj.x + frow] : 0.0;
     };
     auto fill = [&](int64_t j) {
         const int slot = (int)(j % kRingF);
         double t[3];
-        int cnt = cntf;
+        const int cnt = cntf;
+        const double w = wf;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) t[ax] = uf[ax] - floor(uf[ax]) - 0.5;
         load_rows(j + 1);
         if (j >= kRingF) mbar_wait(&sm.empty[slot], (uint32_t)(((j - kRingF) / kRingF) & 1));
+        if ((UOTK_DIAG_FLY & 2) == 0 && frow < cnt) {
+            double t2[3], e[3], o[3];
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-            double v1 = 0.0, v2 = 0.0;
-            if (frow < cnt) {
-                const double t2 = t[ax] * t[ax];
-                double e = he[kHornerDeg / 2], o = ho[kHornerDeg / 2 - 1];
-#pragma unroll
-                for (int q = kHornerDeg / 2 - 1; q >= 0; --q) e = fma(e, t2, he[q]);
-#pragma unroll
-                for (int q = kHornerDeg / 2 - 2; q >= 0; --q) o = fma(o, t2, ho[q]);
-                v1 = fma(t[ax], o, e);
-                v2 = fma(-t[ax], o, e);
+            for (int ax = 0; ax < 3; ++ax) {
+                t2[ax] = t[ax] * t[ax];
+                e[ax] = sm.he[fa][kHornerDeg / 2];
+                o[ax] = sm.ho[fa][kHornerDeg / 2 - 1];
             }
-            sm.win[slot][ax][frow][fa] = v1;
-            sm.win[slot][ax][frow][kChunkT - 1 - fa] = v2;
+#pragma unroll
+            for (int q = kHornerDeg / 2 - 1; q >= 0; --q) {
+                const double ce = sm.he[fa][q];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) e[ax] = fma(e[ax], t2[ax], ce);
+            }
+#pragma unroll
+            for (int q = kHornerDeg / 2 - 2; q >= 0; --q) {
+                const double co = sm.ho[fa][q];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) o[ax] = fma(o[ax], t2[ax], co);
+            }
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                double v1 = fma(t[ax], o[ax], e[ax]);
+                double v2 = fma(-t[ax], o[ax], e[ax]);
+                if (ax == 2) {  // B = w_p Z_p
+                    v1 *= w;
+                    v2 *= w;
+                }
+                sm.win[slot][ax][frow][fa] = v1;
+                sm.win[slot][ax][frow][kChunkT - 1 - fa] = v2;
+            }
+        } else {
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                sm.win[slot][ax][frow][fa] = 0.0;
+                sm.win[slot][ax][frow][kChunkT - 1 - fa] = 0.0;
+            }
         }
         mbar_arrive(&sm.full[slot]);
     };
@@ -735,6 +771,15 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
         return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
     };
     auto flush = [&]() {
+        if (UOTK_DIAG_FLY & 1) {  // keep the accumulators alive without the atomics
+            double acc = 0.0;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nz = 0; nz < 2; ++nz) acc += S[mt][nz][0] + S[mt][nz][1];
+            if (acc == -1.2345e300) grid_out[0] = acc;
+            return;
+        }
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
@@ -746,12 +791,10 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
         }
     };
     int4 d0 = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
-    double w_cur = lane < d0.y ? w_in[d0.x + lane] : 0.0;
     for (int64_t k = 0; k < nck; ++k) {
         const int slot = (int)(k % kRingF);
         const int4 dsc = d0;
         if (k + 1 < nck) d0 = desc[cbeg + k + 1];
-        const double w_nxt = (k + 1 < nck && lane < d0.y) ? w_in[d0.x + lane] : 0.0;
         if (k + kLeadF < nck) fill(k + kLeadF);  // windows of a later chunk while this one's are ready
         if (dsc.z != cur_key) {
             if (cur_key >= 0) flush();
@@ -766,12 +809,13 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
         const double(*wx)[kStride] = sm.win[slot][0];
         const double(*wy)[kStride] = sm.win[slot][1];
         const double(*wz)[kStride] = sm.win[slot][2];
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-            if (4 * ks >= dsc.y) break;  // k-steps past the chunk's points add zero windows
+        // k-steps past the chunk's points add zero windows and are skipped.  A full chunk runs
+        // its eight steps without a branch, so the compiler can load the operands of later
+        // steps while the DMMAs of earlier ones run; a partial chunk stops after its last
+        // occupied step.
+        auto kstep = [&](int ks) {
             const int p = 4 * ks + tq;
-            const double wp = __shfl_sync(0xffffffffu, w_cur, p);
-            const double bz0 = wp * wz[p][gq], bz1 = wp * wz[p][8 + gq];
+            const double bz0 = wz[p][gq], bz1 = wz[p][8 + gq];
             const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
             const double xv[2] = {xa.x, xa.y};
             const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
@@ -781,10 +825,20 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
                 dmma(S[mt][0][0], S[mt][0][1], am, bz0);
                 dmma(S[mt][1][0], S[mt][1][1], am, bz1);
             }
+        };
+        if (UOTK_DIAG_FLY & 4) {
+        } else if (dsc.y == kChunk) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) kstep(ks);
+        } else {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                if (4 * ks >= dsc.y) break;
+                kstep(ks);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);  // this warp is done with the slot
-        w_cur = w_nxt;
     }
     if (cur_key >= 0) flush();
 }
