@@ -495,8 +495,9 @@ sinkhorn3d_ws_k(const int4* __restrict__ desc, const double* __restrict__ win, c
                 const double wv = wsc[p];
                 const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
                 const double2 xb = *reinterpret_cast<const double2*>(&wx[p][a0 + 2]);
-                const double xv[4] = {wv * xa.x, wv * xa.y, wv * xb.x, wv * xb.y};
-                const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+                // w_p folded into the two y values (2 DMUL per step instead of 4 on x)
+                const double ylo = wv * wy[p][gq], yhi = wv * wy[p][8 + gq];
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
                     const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
