@@ -7,6 +7,10 @@
 //   mode 4: spread warp, w_p on x (12 DMUL per step)   mode 5: w_p on y (10 DMUL per step)
 //   mode 6: gather warp: B fragments in registers, 4 k-steps of 8 DMMAs per m-tile, then the
 //           (a, b) contraction (16 DFMA per m-tile)
+//   mode 7: mode 6 without the contraction (accumulators carried)
+//   mode 9: mode 7 with the operands swapped (the footprint fragment as A, the window as B)
+//   mode 8: mode 6 with the contraction of m-tile mt after the DMMAs of m-tile mt + 1
+//           (two accumulator sets)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/dmma_operand_probe scripts/dmma_operand_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -53,7 +57,7 @@ __global__ void probe(double* out, int iters) {
     for (int mt = 0; mt < 4; ++mt) for (int n = 0; n < 2; ++n) s += S[mt][n][0] + S[mt][n][1];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
-// modes 4-6: 64 DMMAs per iteration (4 x 16)
+// modes 4-5: 64 DMMAs per iteration (4 k-steps x 16); modes 6-9: 128 (4 m-tiles x 4 k-steps x 8)
 template <int MODE>
 __global__ void probe_ws(double* out, int iters) {
     __shared__ double ww[2][3][32][20];
@@ -73,7 +77,62 @@ __global__ void probe_ws(double* out, int iters) {
     for (int it = 0; it < iters; ++it) {
         const double(*w)[32][20] = ww[it & 1];  // operands change every iteration (no hoisting)
         const double* wsc = wsc2[it & 1];
-        if (MODE == 6) {
+        if (MODE == 9) {
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double az = w[2][p][4 * ks + tq];
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) dmma(S[nt][0][0], S[nt][0][1], Fb[nt][ks], az);
+                }
+            }
+        } else if (MODE == 7) {
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double az = w[2][p][4 * ks + tq];
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) dmma(S[nt][0][0], S[nt][0][1], az, Fb[nt][ks]);
+                }
+            }
+        } else if (MODE == 8) {
+            double acc[2][8][2];
+            auto contract = [&](int mt, double (&a)[8][2]) {
+                const int p = 8 * mt + gq;
+                const double2 ylo = *reinterpret_cast<const double2*>(&w[1][p][2 * tq]);
+                const double2 yhi = *reinterpret_cast<const double2*>(&w[1][p][8 + 2 * tq]);
+                const double2 xa = *reinterpret_cast<const double2*>(&w[0][p][a0]);
+                const double2 xb = *reinterpret_cast<const double2*>(&w[0][p][a0 + 2]);
+                const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+#pragma unroll
+                for (int al = 0; al < 4; ++al) {
+                    double q = a[2 * al][0] * ylo.x;
+                    q = fma(a[2 * al][1], ylo.y, q);
+                    q = fma(a[2 * al + 1][0], yhi.x, q);
+                    q = fma(a[2 * al + 1][1], yhi.y, q);
+                    part = fma(q, xv[al], part);
+                }
+            };
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int p = 8 * mt + gq;
+                double (&a)[8][2] = acc[mt & 1];
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) a[nt][0] = a[nt][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const double az = w[2][p][4 * ks + tq];
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) dmma(a[nt][0], a[nt][1], az, Fb[nt][ks]);
+                }
+                if (mt > 0) contract(mt - 1, acc[(mt - 1) & 1]);
+            }
+            contract(3, acc[1]);
+        } else if (MODE == 6) {
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int p = 8 * mt + gq;
@@ -139,7 +198,8 @@ void run_ws(int W, int ctas, double* out) {
     probe_ws<MODE><<<sms * ctas, 32 * W>>>(out, iters);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    const double flop = (double)sms * ctas * W * iters * 64 * 512.0;
+    const int dmma_per_iter = MODE >= 6 ? 128 : 64;  // gather pattern: 4 m-tiles x 4 k-steps x 8
+    const double flop = (double)sms * ctas * W * iters * dmma_per_iter * 512.0;
     printf("{\"mode\": %d, \"warps_per_cta\": %d, \"ctas_per_sm\": %d, \"tflops\": %.2f}\n", MODE, W, ctas, flop / ms * 1e-9);
 }
 template <int MODE>
@@ -160,5 +220,7 @@ int main() {
     for (int c : {1, 2}) { run<0>(8, c, out); run<1>(8, c, out); run<2>(8, c, out); run<3>(8, c, out); }
     for (int c : {1, 2}) { run_ws<4>(4, c, out); run_ws<5>(4, c, out); run_ws<6>(4, c, out); }
     for (int c : {1, 2}) { run_ws<4>(8, c, out); run_ws<5>(8, c, out); run_ws<6>(8, c, out); }
+    for (int c : {1, 2}) { run_ws<7>(4, c, out); run_ws<8>(4, c, out); run_ws<7>(8, c, out); run_ws<8>(8, c, out); }
+    for (int c : {1, 2}) { run_ws<9>(4, c, out); run_ws<9>(8, c, out); }
     return 0;
 }
