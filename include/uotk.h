@@ -143,7 +143,9 @@ typedef struct {
      * generic thread-per-point kernels; otherwise the z extent of a group's window
      * footprint: 16 = one-cell groups (m = 8; in d = 3 the warp-specialised half-step
      * sinkhorn3d_ws_k), 12 = one-cell groups with m = 6, 24 / 40 = z-segment groups of
-     * sparse d = 3 clouds.  Set 1 = src (kernel sum), x (UOT) or z = x u y (MMD^2);
+     * sparse d = 3 clouds, 1624 = hybrid groups of a d = 3 spread-only set (cells with
+     * >= 24 points alone, the sparser cells in 9-cell z-segments; windows evaluated in the
+     * spread).  Set 1 = src (kernel sum), x (UOT) or z = x u y (MMD^2);
      * set 2 = tgt (kernel sum) or y (UOT), 0 for MMD^2. */
     int32_t groups1;
     int32_t groups2;

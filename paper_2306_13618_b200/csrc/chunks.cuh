@@ -42,6 +42,13 @@ constexpr int kSegZ = 9;
 // spread-only sets sparser still (kernel-sum sources, MMD^2): segments of 25 cells,
 // footprint 16 x 16 x 40 — the group flushes (fp64 atomics), not the DMMAs, bind there
 constexpr int kSegZ40 = 25;
+// hybrid groups (d = 3 spread-only sets whose windows the spread evaluates, spread3d_fly_k):
+// cells with at least kHybridMin points stay one-cell groups (16 x 16 x 16 footprints), the
+// sparser cells of a kSegZ z-segment share a 16 x 16 x 24 footprint; the group key of such
+// a segment is its first cell's key with kSegFlag set (keys < 2^30)
+constexpr int kHybridMin = 24;
+constexpr int32_t kSegFlag = 1 << 30;
+constexpr int kGroupsHybrid = 1624;  // uotk_info.groups code of the hybrid layout
 // KZ = 12: the one-cell layout of m = 6 (fused3d_m6.cu): all three axes [slot 32][12 taps],
 // row stride 12 (no padding; 9 KB per chunk)
 __host__ __device__ constexpr int chunk_zstride3(int kz) {

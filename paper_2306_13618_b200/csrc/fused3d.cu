@@ -26,6 +26,8 @@
 // scripts/dmma_probe.cu) from 1/8 of the instructions of a DFMA formulation.
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include "chunks.cuh"
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -656,8 +658,13 @@ constexpr int kRingF = 4, kLeadF = 2;
 #ifndef UOTK_DIAG_FLY
 #define UOTK_DIAG_FLY 0  // timing diagnostics only: 1 skips the flushes, 2 the tap polynomials, 4 the DMMAs
 #endif
+// HYB: the set has hybrid groups (z rows 24 columns wide at stride 28, three z n-tiles of
+// accumulators); one-cell sets keep 16-tap z rows at stride 20 and two n-tiles
+template <bool HYB>
 struct __align__(128) SmemF {
-    double win[kRingF][3][kChunk][kStride];
+    static constexpr int kZS = HYB ? chunk_zstride3(24) : kStride;
+    double win[kRingF][2][kChunk][kStride];  // x and y rows
+    double winz[kRingF][kChunk][kZS];         // z rows (w_p folded in)
     // even / odd Horner coefficients of tap pair (a, 15 - a), in t^2; a row stride of 10
     // doubles puts the eight pairs' 16-byte reads in distinct banks
     double he[8][10];
@@ -666,12 +673,14 @@ struct __align__(128) SmemF {
     unsigned long long empty[kRingF];
 };
 
+template <bool HYB>
 __global__ void __launch_bounds__(kThreads, kCtasFly3)
-spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int64_t n,
-               const int32_t* __restrict__ bounds, int ng, double* __restrict__ grid_out,
+spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, const int32_t* __restrict__ key,
+               int64_t n, const int32_t* __restrict__ bounds, int ng, double* __restrict__ grid_out,
                const double* __restrict__ w_in, KBHorner hcoef) {
     extern __shared__ __align__(128) unsigned char f_raw[];
-    SmemF& sm = *reinterpret_cast<SmemF*>(f_raw);
+    SmemF<HYB>& sm = *reinterpret_cast<SmemF<HYB>*>(f_raw);
+    constexpr int NZT = HYB ? 3 : 2;  // z n-tiles of the accumulators
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
@@ -703,20 +712,26 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
     // the coordinates and the weight of the next block to fill are loaded one fill ahead
     // (their L2 latency then overlaps a chunk of DMMAs instead of stalling the fill)
     double uf[3], wf = 0.0;
-    int cntf = 0;
+    int cntf = 0, offf = 0;
+    bool segf = false;
     auto load_rows = [&](int64_t j) {
         const int4 dj = j < nck ? desc[cbeg + j] : make_int4(0, 0, 0, 0);
         cntf = dj.y;
+        segf = HYB && (dj.z & kSegFlag) != 0;
         const bool live = frow < dj.y;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) uf[ax] = live ? u[(int64_t)ax * n + dj.x + frow] : 0.0;
         wf = live ? w_in[dj.x + frow] : 0.0;
+        // a segment group's key is its first cell's: the point's z offset in the segment
+        offf = (live && segf) ? key[dj.x + frow] - (dj.z & ~kSegFlag) : 0;
     };
     auto fill = [&](int64_t j) {
         const int slot = (int)(j % kRingF);
         double t[3];
         const int cnt = cntf;
         const double w = wf;
+        const int off = offf;
+        const bool seg = segf;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) t[ax] = uf[ax] - floor(uf[ax]) - 0.5;
         load_rows(j + 1);
@@ -745,29 +760,35 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
             for (int ax = 0; ax < 3; ++ax) {
                 double v1 = fma(t[ax], o[ax], e[ax]);
                 double v2 = fma(-t[ax], o[ax], e[ax]);
-                if (ax == 2) {  // B = w_p Z_p
-                    v1 *= w;
-                    v2 *= w;
+                if (ax == 2) {  // B = w_p Z_p, the 16 taps at the point's offset in the row
+                    sm.winz[slot][frow][off + fa] = v1 * w;
+                    sm.winz[slot][frow][off + kChunkT - 1 - fa] = v2 * w;
+                } else {
+                    sm.win[slot][ax][frow][fa] = v1;
+                    sm.win[slot][ax][frow][kChunkT - 1 - fa] = v2;
                 }
-                sm.win[slot][ax][frow][fa] = v1;
-                sm.win[slot][ax][frow][kChunkT - 1 - fa] = v2;
             }
         } else {
 #pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
+            for (int ax = 0; ax < 2; ++ax) {
                 sm.win[slot][ax][frow][fa] = 0.0;
                 sm.win[slot][ax][frow][kChunkT - 1 - fa] = 0.0;
             }
+            sm.winz[slot][frow][off + fa] = 0.0;
+            sm.winz[slot][frow][off + kChunkT - 1 - fa] = 0.0;
         }
+        // a segment row's 8 columns outside the taps ([0, off) and [off + 16, 24)): one per thread
+        if (HYB && seg) sm.winz[slot][frow][fa < off ? fa : fa + kChunkT] = 0.0;
         mbar_arrive(&sm.full[slot]);
     };
     load_rows(0);
     for (int64_t j = 0; j < kLeadF && j < nck; ++j) fill(j);
 
-    double S[4][2][2];
+    double S[4][NZT][2];  // [m-tile][z n-tile][2]: n-tile 2 only for segment groups (24 z columns)
     int32_t cur_key = -1;
     int64_t gorg = 0;
     auto origin = [&](int32_t kk) -> int64_t {
+        if (HYB) kk &= ~kSegFlag;
         const int k2 = kk % ng, k1 = (kk / ng) % ng, k0 = kk / ng2;
         return ((int64_t)(k0 - kM + 1) * ng + (k1 - kM + 1)) * ng + (k2 - kM + 1);
     };
@@ -778,17 +799,19 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                 for (int nz = 0; nz < 2; ++nz) acc += S[mt][nz][0] + S[mt][nz][1];
+            acc += S[0][NZT - 1][0];
             if (acc == -1.2345e300) grid_out[0] = acc;
             return;
         }
+        const int nzt = (HYB && (cur_key & kSegFlag)) ? 3 : 2;
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int64_t row = gorg + (int64_t)(a0 + (mt >> 1)) * ng2 + (int64_t)(8 * (mt & 1) + gq) * ng;
 #pragma unroll
-            for (int nz = 0; nz < 2; ++nz)
+            for (int nz = 0; nz < NZT; ++nz)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
-                    if (S[mt][nz][i] != 0.0) atomicAdd(grid_out + row + 8 * nz + 2 * tq + i, S[mt][nz][i]);
+                    if (nz < nzt && S[mt][nz][i] != 0.0) atomicAdd(grid_out + row + 8 * nz + 2 * tq + i, S[mt][nz][i]);
         }
     };
     int4 d0 = nck > 0 ? desc[cbeg] : make_int4(0, 0, -1, 0);
@@ -804,39 +827,49 @@ spread3d_fly_k(const int4* __restrict__ desc, const double* __restrict__ u, int6
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                for (int nz = 0; nz < 2; ++nz) S[mt][nz][0] = S[mt][nz][1] = 0.0;
+                for (int nz = 0; nz < NZT; ++nz) S[mt][nz][0] = S[mt][nz][1] = 0.0;
         }
         mbar_wait(&sm.full[slot], (uint32_t)((k / kRingF) & 1));
         const double(*wx)[kStride] = sm.win[slot][0];
         const double(*wy)[kStride] = sm.win[slot][1];
-        const double(*wz)[kStride] = sm.win[slot][2];
+        const double(*wz)[SmemF<HYB>::kZS] = sm.winz[slot];
         // k-steps past the chunk's points add zero windows and are skipped.  A full chunk runs
         // its eight steps without a branch, so the compiler can load the operands of later
         // steps while the DMMAs of earlier ones run; a partial chunk stops after its last
         // occupied step.
-        auto kstep = [&](int ks) {
+        auto kstep = [&](int ks, auto nzt) {
+            constexpr int NZ = decltype(nzt)::value;
             const int p = 4 * ks + tq;
-            const double bz0 = wz[p][gq], bz1 = wz[p][8 + gq];
+            double bz[NZ];
+#pragma unroll
+            for (int nz = 0; nz < NZ; ++nz) bz[nz] = wz[p][8 * nz + gq];
             const double2 xa = *reinterpret_cast<const double2*>(&wx[p][a0]);
             const double xv[2] = {xa.x, xa.y};
             const double ylo = wy[p][gq], yhi = wy[p][8 + gq];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const double am = xv[mt >> 1] * ((mt & 1) ? yhi : ylo);
-                dmma(S[mt][0][0], S[mt][0][1], am, bz0);
-                dmma(S[mt][1][0], S[mt][1][1], am, bz1);
+#pragma unroll
+                for (int nz = 0; nz < NZ; ++nz) dmma(S[mt][nz][0], S[mt][nz][1], am, bz[nz]);
+            }
+        };
+        auto ksteps = [&](auto nzt) {
+            if (dsc.y == kChunk) {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) kstep(ks, nzt);
+            } else {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    if (4 * ks >= dsc.y) break;
+                    kstep(ks, nzt);
+                }
             }
         };
         if (UOTK_DIAG_FLY & 4) {
-        } else if (dsc.y == kChunk) {
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) kstep(ks);
+        } else if (HYB && (dsc.z & kSegFlag)) {
+            ksteps(std::integral_constant<int, NZT>{});
         } else {
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                if (4 * ks >= dsc.y) break;
-                kstep(ks);
-            }
+            ksteps(std::integral_constant<int, 2>{});
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);  // this warp is done with the slot
@@ -1052,12 +1085,16 @@ void fused3d_spread(const PointSet& ps, const double* w, double* grid, const Fas
     }
     if (ps.n == 0 || ps.nchunks == 0) return;
     ProfScope prof(kProfSpread, s);
-    if (ps.win_fly) {  // spread-only set without precomputed window blocks (KZ = 16)
-        set_smem_attr((const void*)spread3d_fly_k, (int)sizeof(SmemF));
-        spread3d_fly_k<<<ps.chunk_blocks, kThreads, sizeof(SmemF), s>>>(ps.chunk_desc.p, ps.u.p, ps.n,
-                                                                        ps.chunk_bounds.p, fp.ng, grid, w,
-                                                                        ps.win_coef);
-        UOTK_LAUNCHED();
+    if (ps.win_fly) {  // spread-only set without precomputed window blocks (one-cell or hybrid groups)
+        auto go = [&](auto hyb) {
+            constexpr bool H = decltype(hyb)::value;
+            set_smem_attr((const void*)spread3d_fly_k<H>, (int)sizeof(SmemF<H>));
+            spread3d_fly_k<H><<<ps.chunk_blocks, kThreads, sizeof(SmemF<H>), s>>>(
+                ps.chunk_desc.p, ps.u.p, ps.key.p, ps.n, ps.chunk_bounds.p, fp.ng, grid, w, ps.win_coef);
+            UOTK_LAUNCHED();
+        };
+        if (ps.chunk_kz == kGroupsHybrid) go(std::true_type{});
+        else go(std::false_type{});
         return;
     }
     if (ps.chunk_kz == 40) {

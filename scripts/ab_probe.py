@@ -39,4 +39,25 @@ if "c3" in which:
     out["c3_fused_ms"] = round(p["fused"][0] / p["fused"][1], 4)
     out["c3_primal"] = res.primal
     uk.profile_enable(False)
+if "c5" in which:
+    for kind, param in ((W.GAUSS, None), (W.IMQ, None)):
+        pr = W.c5_sum(3, 1_000_000, kind=kind)
+        args = [torch.from_numpy(v).cuda() for v in (pr.src, pr.alpha, pr.tgt)]
+        for _ in range(3):
+            uk.kernel_sum(*args, kind, pr.param, opts={"method": "nfft"})
+        torch.cuda.synchronize()
+        uk.profile_enable(True)
+        uk.profile_reset()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(5):
+            r, info = uk.kernel_sum(*args, kind, pr.param, opts={"method": "nfft"}, return_info=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        p = uk.profile_read()
+        out[f"c5_{kind}_spread_ms"] = round(p["spread"][0] / p["spread"][1], 4)
+        out[f"c5_{kind}_call_ms"] = round(ev0.elapsed_time(ev1) / 5, 4)
+        out[f"c5_{kind}_groups"] = info["groups"]
+        out[f"c5_{kind}_sum0"] = float(r[0])
+        uk.profile_enable(False)
 print(os.environ.get("UOTK_COST", "default"), out, flush=True)

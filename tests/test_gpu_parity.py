@@ -812,6 +812,33 @@ def test_auto_method_crossover(uk):
     assert rel_err(got_b.cpu().numpy(), ref_b.cpu().numpy(), False) <= 1e-9
 
 
+def test_spread_only_hybrid_groups(uk):
+    """Spread-only d = 3 sets whose one-cell chunks are partly filled take hybrid groups
+    (uotk_info.groups 1624: cells with >= 24 points alone, the sparser cells of a 9-cell
+    z-segment on one 16 x 16 x 24 footprint, windows evaluated in the spread with the z taps
+    at the point's offset): MMD^2 and a kernel sum on C2's mixtures shrunk to C2-at-1M cell
+    densities (workloads.c2_dense_mmd) against the oracle, and against the generic kernels."""
+    pr = W.c2_dense_mmd(n=10000)
+    param = 0.0025
+    v, info = uk.mmd2(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), "gauss", param, opts={"method": "nfft"},
+                      return_info=True)
+    assert info["groups"][0] == 1624, info
+    mref = oracle.mmd2_direct(pr.x, pr.a, pr.y, pr.b, W.GAUSS, param)
+    denom = max(abs(mref), 1e-3 * _mmd_tol(pr.x, pr.a, pr.y, pr.b, W.GAUSS, param))
+    assert abs(v - mref) / denom <= 1e-8, (v, mref)
+    gen = uk.mmd2(cuda(pr.x), cuda(pr.a), cuda(pr.y), cuda(pr.b), "gauss", param,
+                  opts={"method": "nfft", "flags": uk.FLAG_GENERIC})
+    assert abs(v - gen) <= 1e-12 * abs(gen), (v, gen)
+    got, kinfo = uk.kernel_sum(cuda(pr.x), cuda(pr.a), cuda(pr.y[:2000]), "gauss", param, opts={"method": "nfft"},
+                               return_info=True)
+    assert kinfo["groups"][0] == 1624, kinfo
+    ref = oracle.kernel_sum_direct(pr.x, pr.a, pr.y[:2000], W.GAUSS, param)
+    assert rel_err(got.cpu().numpy(), ref, False) <= 1e-9
+    kgen = uk.kernel_sum(cuda(pr.x), cuda(pr.a), cuda(pr.y[:2000]), "gauss", param,
+                         opts={"method": "nfft", "flags": uk.FLAG_GENERIC})
+    assert rel_err(got.cpu().numpy(), kgen.cpu().numpy(), False) <= 1e-13
+
+
 @pytest.mark.parametrize("kind", [W.GAUSS, W.IMQ])
 def test_spread_only_windows_on_the_fly(uk, kind):
     """Spread-only d = 3 one-cell sets (kernel-sum sources, MMD^2's z) evaluate their window

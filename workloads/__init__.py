@@ -121,6 +121,23 @@ def c2_mmd(n=100_000, m=None, seed=0):
                       meta={"means_x": mx, "means_y": my, "sigma": 0.03})
 
 
+def c2_dense_mmd(n=10_000, m=None, seed=0, shrink=0.2):
+    """C2's mixtures (means +-0.05 e1, sigma 0.03, nu shifted by 0.02 e2, weights
+    U(0.5,1.5)) shrunk by ``shrink`` about the origin, so that a reduced n fills the grid
+    cells (the Gaussian's h is floored by its width) about as unevenly as C2 at 1M: dense
+    cells next to sparse ones, the mix the hybrid spread groups serve (tests only)."""
+    m = n if m is None else m
+    rng = np.random.default_rng(seed)
+    mx = shrink * np.array([[0.05, 0.0, 0.0], [-0.05, 0.0, 0.0]])
+    my = mx + shrink * np.array([0.0, 0.02, 0.0])
+    x = gaussian_mixture(rng, n, mx, 0.03 * shrink)
+    y = gaussian_mixture(rng, m, my, 0.03 * shrink)
+    a = rng.uniform(0.5, 1.5, n)
+    b = rng.uniform(0.5, 1.5, m)
+    return MMDProblem("C2-dense", x, a, y, b, kernels=((GAUSS, 0.05 ** 2), (IMQ, 0.05)),
+                      meta={"shrink": shrink})
+
+
 def c3_uot(n=1_000_000, m=None, seed=0, iters=200):
     """C3: UOT d=3, n=m=1M from 8-component Gaussian mixtures clipped to radius 0.2
     (reading R15: means uniform in the ball of radius 0.12, sigma = 0.025),
