@@ -133,19 +133,37 @@ __global__ void segment_key_k(const int32_t* __restrict__ key, int64_t n, int ng
     }
 }
 
-// hybrid group keys (chunks.cuh): one warp per run of equal cell keys (one cell); cells
-// with at least minpts points keep their key, the others take their z-segment's key with
-// kSegFlag
-__global__ void hybrid_key_k(const int32_t* __restrict__ run_key, const int32_t* __restrict__ run_len,
-                             const int32_t* __restrict__ run_start, int nruns, int ng, int segz, int minpts,
-                             int32_t* __restrict__ gk) {
-    const int r = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (r >= nruns) return;
-    const int32_t k = run_key[r];
-    const int len = run_len[r], st = run_start[r];
-    const int32_t g = len >= minpts ? k : ((k - (k % ng) % segz) | kSegFlag);
-    for (int i = lane; i < len; i += 32) gk[st + i] = g;
+// hybrid group keys (chunks.cuh) straight from the sorted cell keys: each point finds its
+// cell's run [lo, hi) by binary search; cells with at least minpts points keep their key,
+// the others take their z-segment's key with kSegFlag.  The first point of each cell also
+// adds the cell's one-cell chunk count to *onecell (the layout the hybrid one replaces).
+__global__ void hybrid_key_k(const int32_t* __restrict__ key, int n, int ng, int segz, int minpts,
+                             int32_t* __restrict__ gk, int32_t* __restrict__ onecell) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int add = 0;
+    if (i < n) {
+        const int32_t k = key[i];
+        int lo = 0, hi = i;  // first index with key == k
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (key[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        const int first = lo;
+        lo = i + 1;
+        hi = n;  // first index with key > k
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (key[mid] <= k) lo = mid + 1;
+            else hi = mid;
+        }
+        const int len = lo - first;
+        gk[i] = len >= minpts ? k : ((k - (k % ng) % segz) | kSegFlag);
+        if (i == first) add = (len + kChunk - 1) / kChunk;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) add += __shfl_xor_sync(0xffffffffu, add, off);
+    if ((threadIdx.x & 31) == 0 && add) atomicAdd(onecell, add);
 }
 
 // cost of a chunk for the static partition: fix per chunk + step per 4-point k-step of its
@@ -195,7 +213,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     const int d = fp.d;
     const int n = (int)ps.n;
     trace_mark("chunks: start");
-    DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(2, s);
+    DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(3, s);
     trace_mark("chunks: 6 scratch allocations");
     size_t tmp_bytes = 0, t2 = 0;
     UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
@@ -205,6 +223,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     DevBuf<uint8_t> tmp(tmp_bytes, s);
     trace_mark("chunks: temp allocation");
     int32_t nruns = 0;
+    int32_t onecell_chunks = 0;  // cnt[2]: written by hybrid_key_k only
     // runs of equal group keys -> chunks of <= 32 points; returns the number of chunks.
     // One host synchronisation per encode: the scans run over all n run slots (the slots
     // past the last run zeroed on the device), and the run and chunk counts come back
@@ -222,20 +241,21 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
         add_launches(4);
         chunk_total_k<<<1, 1, 0, s>>>(chunk_off.p, nchunk.p, n, cnt.p);
         UOTK_LAUNCHED();
-        int32_t h[2];
-        UOTK_CUDA(cudaMemcpyAsync(h, cnt.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        int32_t h[3];
+        UOTK_CUDA(cudaMemcpyAsync(h, cnt.p, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         UOTK_CUDA(cudaStreamSynchronize(s));
         trace_mark("chunks: run-length encode + scans");
         nruns = h[0];
+        onecell_chunks = h[2];
         return (int64_t)h[1];
     };
-    int64_t nchunks = encode(ps.key.p);
-    trace_mark("chunks: encode");
     const bool forced = fp.flags & UOTK_FLAG_CHUNKED;
     // spread-only d = 3 sets whose windows the spread evaluates (spread3d_fly_k): when the
     // one-cell chunks are only partly filled (but not sparse enough for the all-segment
     // layouts below), hybrid groups — dense cells alone, sparse cells in z-segments — cut
-    // the chunk count (MMD^2 at 1M: 89k -> 73k chunks, 39k -> 20k footprint flushes)
+    // the chunk count (MMD^2 at 1M: 89k -> 73k chunks, 39k -> 20k footprint flushes).  The
+    // hybrid keys and the one-cell chunk count come from one pass over the sorted keys, so
+    // a set that takes the hybrid layout needs one run-length encode, not two.
     static const bool fly_env = [] {
         const char* e = getenv("UOTK_SPREAD_FLY");
         return !(e && e[0] == '0');
@@ -246,22 +266,23 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     }();
     bool hybrid = false;
     DevBuf<int32_t> gk;
+    int64_t nchunks = 0;
     if (fly_env && hybrid_env && d == 3 && fp.m == kChunkM && use == kUseSpreadOnly &&
-        std::pow((double)fp.ng, 3) < (double)kSegFlag && (double)n >= 0.5 * kChunk * (double)nchunks &&
-        (double)n < 0.95 * kChunk * (double)nchunks) {
+        std::pow((double)fp.ng, 3) < (double)kSegFlag) {
         gk.alloc(n, s);
-        hybrid_key_k<<<blocks_for((int64_t)nruns * 32, 256), 256, 0, s>>>(run_key.p, run_len.p, run_start.p, nruns,
-                                                                       fp.ng, kSegZ, kHybridMin, gk.p);
+        UOTK_CUDA(cudaMemsetAsync(cnt.p + 2, 0, sizeof(int32_t), s));
+        hybrid_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, n, fp.ng, kSegZ, kHybridMin, gk.p, cnt.p + 2);
         UOTK_LAUNCHED();
         const int64_t nh = encode(gk.p);
-        if ((double)nh < 0.95 * (double)nchunks) {
+        const double n1 = (double)onecell_chunks;
+        if ((double)n >= 0.5 * kChunk * n1 && (double)n < 0.95 * kChunk * n1 && (double)nh < 0.95 * n1) {
             hybrid = true;
             nchunks = nh;
-        } else {
-            nchunks = encode(ps.key.p);  // back to one-cell groups
         }
         trace_mark("chunks: hybrid groups");
     }
+    if (!hybrid) nchunks = encode(ps.key.p);
+    trace_mark("chunks: encode");
     // d = 3 sparse clouds: group z-segments of kSegZ cells when that needs sufficiently
     // fewer chunks (each costs 1.5x a one-cell chunk: 24 instead of 16 z-columns)
     int kz = fp.m == 6 ? 12 : 16;
