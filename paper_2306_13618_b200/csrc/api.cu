@@ -770,7 +770,7 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
         permute_signed(ws.p, A.d, n, B.d, PZ.perm.p, nz, s);
         grid.zero();
         spread(PZ, ws.p, grid.p, ns.fp, s);
-        if (ns.sp.pd->separable && !(ns.fp.flags & UOTK_FLAG_FFT)) {
+        if (ns.sp.sep_chain) {
             // Gaussian: <g, g'> with g' the separable chain's output (no FFT, no cuFFT plan);
             // with a communicator g' is global and <g_rank, g'> is summed over ranks
             const double* gp = fft_chain(ns.sp, grid.p, spec.p, s, comm);

@@ -198,6 +198,9 @@ struct SpectralPlan {
     size_t spec_elems = 0;   // ng^(d-1) * (ng/2+1)
     cudaStream_t use_stream = nullptr;  // the call's stream (build_spectral_plan)
     DevBuf<double> work;                // the separable chain's compact intermediate (w^d)
+    // the spectral step runs as the separable chain (Gaussian, and cheaper than the cuFFT
+    // chain for this box and grid; build_spectral_plan), else as cuFFT D2Z / D_k / Z2D
+    bool sep_chain = false;
     ~SpectralPlan() {
         if (pd) pd->note_use(use_stream);
     }

@@ -383,7 +383,7 @@ double* fft_chain(SpectralPlan& sp, double* grid, double2* spec, cudaStream_t s,
                   bool* zeroed) {
     const FastParams& fp = sp.fp;
     if (zeroed) *zeroed = false;
-    if (sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT)) {
+    if (sp.sep_chain) {
         const size_t wd = separable_work_elems(fp, comm);
         if (sp.work.n < wd) sp.work.alloc(wd, s);
         if (fp.d == 1 && zero_next == grid) zero_next = nullptr;  // d = 1: one pass, still reading it

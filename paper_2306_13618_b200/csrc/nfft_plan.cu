@@ -452,9 +452,22 @@ void build_spectral_plan(SpectralPlan& sp, cudaStream_t s) {
         g_plans.emplace_front(key, pd);
         if (g_plans.size() > kPlanCacheSize) g_plans.pop_back();
     }
+    // The separable chain costs d GEMM passes of w^(d+1) MACs on the footprint box (w =
+    // box_w), the cuFFT chain ~ n_g^d grid traffic: the separable one wins on the compact
+    // boxes of C3 / C4-auto (21 / 16 us vs 74 / 29 us), cuFFT on C4's literal 4096^2 grid
+    // (0.36 ms vs 1.18 ms per chain, w = 1982; scripts/chain_probe.py).  Estimates from those
+    // measurements (DMMA GEMMs at ~25 TFLOP/s + ~5 us per pass; cuFFT ~25 us + 20 ps per
+    // grid point); the cuFFT chain only when it is clearly cheaper.
+    sp.sep_chain = sp.pd->separable && !(fp.flags & UOTK_FLAG_FFT);
+    if (sp.sep_chain) {
+        const double w = fp.box_w, g = std::pow((double)ng, d);
+        const double t_sep = 2.0 * d * std::pow(w, d + 1) / 25e12 + 5e-6 * d;
+        const double t_fft = 25e-6 + 2e-11 * g;
+        if (t_fft < 0.7 * t_sep) sp.sep_chain = false;
+    }
     // the full-grid cuFFT plans only where the full chain runs (fft_chain also creates them
     // on first use: the separable Gaussian chain and the pruned MMD^2 transform never do)
-    if (!sp.pd->separable || (fp.flags & UOTK_FLAG_FFT)) get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
+    if (!sp.sep_chain) get_fft_plans(d, ng, &sp.r2c, &sp.c2r);
     sp.use_stream = s;
     sp.grid_elems = 1;
     for (int t = 0; t < d; ++t) sp.grid_elems *= ng;
