@@ -654,7 +654,7 @@ spread3d_k(const int4* __restrict__ desc, const double* __restrict__ win, const 
 // The source weight is folded into the z row (B = w_p Z_p) when the row is evaluated, so
 // the DMMA loop forms only the A operand X_p[a] Y_p[b].  kCtasFly3 CTAs per SM (at most
 // 85 registers per thread).
-constexpr int kRingF = 4, kLeadF = 2;
+constexpr int kRingF = 4, kLeadF = 1;
 #ifndef UOTK_DIAG_FLY
 #define UOTK_DIAG_FLY 0  // timing diagnostics only: 1 skips the flushes, 2 the tap polynomials, 4 the DMMAs
 #endif
