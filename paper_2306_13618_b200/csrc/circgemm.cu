@@ -278,6 +278,9 @@ void gemm(int M, int N, int K, const double* A, int64_t lda, int64_t sA, const d
     const int64_t tiles64 = (int64_t)((M + 63) / 64) * ((N + 63) / 64) * batch;
     if (K <= 64 && M <= 64) launch_gemm<32, 32, 64, 1>(g, batch, s);       // C3 (w = 44)
     else if (tiles64 < 2 * 148) launch_gemm<32, 32, 32, 2>(g, batch, s);  // few tiles (C4 auto, w = 164)
+    // mid-size boxes (MMD^2 / C5 at 140^3, w = 86): 32 x 32 tiles, BK = 32, two stages
+    // (61 -> 40 us per chain against the 64 x 64 tiles below; a full-K 32 x 32 x 64 tile 43 us)
+    else if (K <= 128 && M <= 128) launch_gemm<32, 32, 32, 2>(g, batch, s);
     else {
         // large boxes (C4 at 4096^2, w = 1982): 16-byte 3-stage operand ring when every row
         // start is 16-byte aligned, else the 8-byte 2-stage kernel (128 x 128 tiles with 8
