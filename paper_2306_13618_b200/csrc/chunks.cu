@@ -133,33 +133,49 @@ __global__ void segment_key_k(const int32_t* __restrict__ key, int64_t n, int ng
     }
 }
 
-// hybrid group keys (chunks.cuh) straight from the sorted cell keys: each point finds its
-// cell's run [lo, hi) by binary search; cells with at least minpts points keep their key,
-// the others take their z-segment's key with kSegFlag.  The first point of each cell also
-// adds the cell's one-cell chunk count to *onecell (the layout the hybrid one replaces).
+// hybrid group keys (chunks.cuh) straight from the sorted cell keys.  A point's cell is
+// dense (>= minpts points) iff the run holds the minpts-window [f, f + minpts) around its
+// start f: if key[i - minpts + 1] == key[i] the run already spans minpts points up to i,
+// else f lies in the last minpts slots (binary search) and key[f + minpts - 1] decides.
+// Dense cells keep their key, the others take their z-segment's key with kSegFlag.  Each
+// run's first point also adds the run's one-cell chunk count (galloping to the run's end)
+// to *onecell (the layout the hybrid one replaces).
 __global__ void hybrid_key_k(const int32_t* __restrict__ key, int n, int ng, int segz, int minpts,
                              int32_t* __restrict__ gk, int32_t* __restrict__ onecell) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int add = 0;
     if (i < n) {
         const int32_t k = key[i];
-        int lo = 0, hi = i;  // first index with key == k
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (key[mid] < k) lo = mid + 1;
-            else hi = mid;
+        bool dense;
+        int first;
+        if (i - minpts + 1 >= 0 && key[i - minpts + 1] == k) {
+            dense = true;
+            first = -1;  // not the run's first point
+        } else {
+            int lo = i - minpts + 1 < 0 ? 0 : i - minpts + 1, hi = i;  // first index with key == k
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (key[mid] < k) lo = mid + 1;
+                else hi = mid;
+            }
+            first = lo;
+            dense = first + minpts - 1 < n && key[first + minpts - 1] == k;
         }
-        const int first = lo;
-        lo = i + 1;
-        hi = n;  // first index with key > k
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (key[mid] <= k) lo = mid + 1;
-            else hi = mid;
+        gk[i] = dense ? k : ((k - (k % ng) % segz) | kSegFlag);
+        if (first == i) {  // the run's end by galloping, then a binary search in the last step
+            int step = 1, lo = i;  // key[lo] == k
+            while (lo + step < n && key[lo + step] == k) {
+                lo += step;
+                step <<= 1;
+            }
+            int hi = lo + step > n ? n : lo + step;
+            while (lo < hi) {  // first index with key > k
+                const int mid = (lo + hi) >> 1;
+                if (key[mid] <= k) lo = mid + 1;
+                else hi = mid;
+            }
+            add = (lo - i + kChunk - 1) / kChunk;
         }
-        const int len = lo - first;
-        gk[i] = len >= minpts ? k : ((k - (k % ng) % segz) | kSegFlag);
-        if (i == first) add = (len + kChunk - 1) / kChunk;
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) add += __shfl_xor_sync(0xffffffffu, add, off);
