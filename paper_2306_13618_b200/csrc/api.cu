@@ -302,14 +302,17 @@ static void kernel_sum_impl(int d, int64_t n_src, const double* src, const doubl
         NfftSetup ns;
         setup_nfft(ns, d, kind, param, S.d, n_src, T.d, n_tgt, o, comm, s);
         PointSet PS, PT;
-        make_pointset(PS, S.d, n_src, ns.fp, s, kUseSpreadOnly);
+        DevBuf<double> w(n_src, s);
+        SortedWeights sws;  // alpha in sorted order, written by the coordinate gather
+        sws.w1 = A.d;
+        sws.out = w.p;
+        make_pointset(PS, S.d, n_src, ns.fp, s, kUseSpreadOnly, sws);
         trace_mark("pointset src");
         make_pointset(PT, T.d, n_tgt, ns.fp, s, kUseGatherOnly);
         trace_mark("pointset tgt");
         fill_info(info, method, &ns.fp, comm, &PS, &PT);
-        DevBuf<double> w(n_src, s), grid(grid_elems(ns.fp), s);
+        DevBuf<double> grid(grid_elems(ns.fp), s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
-        permute_values(w.p, A.d, PS.perm.p, n_src, s);
         grid.zero();
         spread(PS, w.p, grid.p, ns.fp, s);
         const double* gp = fft_chain(ns.sp, grid.p, spec.p, s, comm);
@@ -762,12 +765,17 @@ static void mmd2_impl(int d, int64_t n, const double* x, const double* a, int64_
         NfftSetup ns;
         setup_nfft(ns, d, kind, param, X.d, n, Y.d, m, o, comm, s);
         PointSet PZ;
-        make_pointset(PZ, X.d, n, Y.d, m, ns.fp, s, kUseSpreadOnly);
+        DevBuf<double> ws(nz, s);
+        SortedWeights swz;  // w = (a, -b) in sorted order, written by the coordinate gather
+        swz.w1 = A.d;
+        swz.w2 = B.d;
+        swz.sign2 = -1.0;
+        swz.out = ws.p;
+        make_pointset(PZ, X.d, n, Y.d, m, ns.fp, s, kUseSpreadOnly, swz);
         fill_info(info, method, &ns.fp, comm, &PZ);
         constexpr int kParts = 296;
-        DevBuf<double> ws(nz, s), grid(grid_elems(ns.fp), s), part(kParts, s);
+        DevBuf<double> grid(grid_elems(ns.fp), s), part(kParts, s);
         DevBuf<double2> spec(ns.sp.spec_elems, s);
-        permute_signed(ws.p, A.d, n, B.d, PZ.perm.p, nz, s);
         grid.zero();
         spread(PZ, ws.p, grid.p, ns.fp, s);
         if (ns.sp.sep_chain) {

@@ -224,12 +224,20 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
 // use: what the point set will be used for (the chunk layout is skipped where no kernel
 // would use it: gather-only d = 3 sets below kGatherMinFill3)
 enum PointUse { kUseBoth = 0, kUseGatherOnly = 1, kUseSpreadOnly = 2 };
+// optional: the set's weights permuted into sorted order while the coordinates are
+// (out[i] = w1[j] for the first n1 points, sign2 * w2[j - n1] for the others; j = perm[i])
+struct SortedWeights {
+    const double* w1 = nullptr;
+    const double* w2 = nullptr;
+    double sign2 = 1.0;
+    double* out = nullptr;
+};
 // the set is p1 (n1 points) followed by p2 (n2 points; may be null when n2 = 0)
 void make_pointset(PointSet& ps, const double* p1, int64_t n1, const double* p2, int64_t n2, const FastParams& fp,
-                   cudaStream_t s, PointUse use = kUseBoth);
+                   cudaStream_t s, PointUse use = kUseBoth, SortedWeights sw = SortedWeights{});
 inline void make_pointset(PointSet& ps, const double* pts, int64_t n, const FastParams& fp, cudaStream_t s,
-                          PointUse use = kUseBoth) {
-    make_pointset(ps, pts, n, nullptr, 0, fp, s, use);
+                          PointUse use = kUseBoth, SortedWeights sw = SortedWeights{}) {
+    make_pointset(ps, pts, n, nullptr, 0, fp, s, use, sw);
 }
 void permute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
 void unpermute_values(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);

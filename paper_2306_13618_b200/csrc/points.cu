@@ -162,12 +162,15 @@ template <int D>
 // doubles per random read instead of D scattered ones
 __global__ void gather_u_k(const double* __restrict__ p1, int64_t n1, const double* __restrict__ p2,
                            const int32_t* __restrict__ perm, int64_t n, double c0, double c1, double c2, double scale,
-                           double* __restrict__ u_out) {
+                           double* __restrict__ u_out, SortedWeights sw) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double c[3] = {c0, c1, c2};
-    const double* q = point_ptr<D>(p1, n1, p2, perm[i]);
+    const int64_t j = perm[i];
+    const double* q = point_ptr<D>(p1, n1, p2, j);
     for (int t = 0; t < D; ++t) u_out[t * n + i] = (q[t] - c[t]) * scale;
+    // the set's weights in sorted order in the same pass (w1 for p1's points, sign2 * w2)
+    if (sw.out) sw.out[i] = j < n1 ? sw.w1[j] : sw.sign2 * sw.w2[j - n1];
 }
 
 __global__ void permute_k(double* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ perm,
@@ -222,7 +225,7 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
 }
 
 void make_pointset(PointSet& ps, const double* p1, int64_t n1, const double* p2, int64_t n2, const FastParams& fp,
-                   cudaStream_t s, PointUse use) {
+                   cudaStream_t s, PointUse use, SortedWeights sw) {
     NvtxRange nvtx_("pointset");
     const int d = fp.d;
     const int64_t n = n1 + n2;
@@ -253,9 +256,9 @@ void make_pointset(PointSet& ps, const double* p1, int64_t n1, const double* p2,
                                                   end_bit, s));
         add_launches(1 + (end_bit + 7) / 8);  // CUB onesweep: histogram + one pass per 8 key bits
         trace_mark("pointset: sort");
-        if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], 0, 0, scale, ps.u.p);
-        else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], c[1], 0, scale, ps.u.p);
-        else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], c[1], c[2], scale, ps.u.p);
+        if (d == 1) gather_u_k<1><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], 0, 0, scale, ps.u.p, sw);
+        else if (d == 2) gather_u_k<2><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], c[1], 0, scale, ps.u.p, sw);
+        else gather_u_k<3><<<blocks_for(n, tb), tb, 0, s>>>(p1, n1, p2, ps.perm.p, n, c[0], c[1], c[2], scale, ps.u.p, sw);
         UOTK_LAUNCHED();
     }
     chunked_prepare(ps, fp, s, use);  // chunk list + precomputed windows (tuned cell-group kernels)
