@@ -8,7 +8,10 @@
 // walks a contiguous, cost-balanced range of chunks, streaming each chunk's window block
 // into shared memory with a TMA bulk copy (cp.async.bulk + mbarrier, double buffered in
 // chunked3d_k, a ring of 4 in the warp-specialised sinkhorn3d_ws_k).  Sparse clouds use
-// z-segment groups (KZ = 24: 9 cells along z share one 16 x 16 x 24 footprint).
+// z-segment groups (KZ = 24: 9 cells along z share one 16 x 16 x 24 footprint).  Sets
+// that are only ever spread (kernel-sum sources, MMD^2's z) evaluate their window blocks
+// inside the spread (spread3d_fly_k) and, when their one-cell chunks are partly filled,
+// take hybrid groups (dense cells alone, the sparser cells of a z-segment together).
 //
 // Per chunk, with X_p, Y_p, Z_p the windows of point p along the three axes and F the
 // group's footprint (outer / inner sums of (4.6)):
