@@ -289,15 +289,24 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
         UOTK_CUDA(cudaMemsetAsync(cnt.p + 2, 0, sizeof(int32_t), s));
         hybrid_key_k<<<blocks_for(n, 256), 256, 0, s>>>(ps.key.p, n, fp.ng, kSegZ, kHybridMin, gk.p, cnt.p + 2);
         UOTK_LAUNCHED();
-        const int64_t nh = encode(gk.p);
-        const double n1 = (double)onecell_chunks;
-        if ((double)n >= 0.5 * kChunk * n1 && (double)n < 0.95 * kChunk * n1 && (double)nh < 0.95 * n1) {
-            hybrid = true;
-            nchunks = nh;
+        // the one-cell chunk count decides which layouts to encode: partly filled sets try the
+        // hybrid one; sparser ones go straight to the z-segment layouts below (their choice
+        // needs only this count), dense ones to the one-cell layout
+        int32_t n1h = 0;
+        UOTK_CUDA(cudaMemcpyAsync(&n1h, cnt.p + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        UOTK_CUDA(cudaStreamSynchronize(s));
+        const double n1 = (double)n1h;
+        if ((double)n >= 0.5 * kChunk * n1 && (double)n < 0.95 * kChunk * n1) {
+            const int64_t nh = encode(gk.p);
+            if ((double)nh < 0.95 * n1) {
+                hybrid = true;
+                nchunks = nh;
+            }
         }
+        if (!hybrid && (double)n < 0.5 * kChunk * n1) nchunks = n1h;  // the z-segment branch encodes
         trace_mark("chunks: hybrid groups");
     }
-    if (!hybrid) nchunks = encode(ps.key.p);
+    if (!hybrid && nchunks == 0) nchunks = encode(ps.key.p);
     trace_mark("chunks: encode");
     // d = 3 sparse clouds: group z-segments of kSegZ cells when that needs sufficiently
     // fewer chunks (each costs 1.5x a one-cell chunk: 24 instead of 16 z-columns)
