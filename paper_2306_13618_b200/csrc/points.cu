@@ -19,9 +19,25 @@ constexpr int kGeomBlocks = 592;  // 4 x 148 SMs
 constexpr int kGeomThreads = 256;
 
 // per-block partial min / max per axis, plus a non-finite flag (as max)
+// the last block to finish (a ticket on *done) reduces every block's partials into the
+// final value and resets the ticket: no separate final launch.  min / max are exact in any
+// order, so the result equals the two-launch reduction's.
+__device__ __forceinline__ bool last_block(unsigned* done) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
 template <int D>
 __global__ void bbox_k(const double* __restrict__ p1, int64_t n1, const double* __restrict__ p2, int64_t n2,
-                       double* __restrict__ pmin, double* __restrict__ pmax) {
+                       double* __restrict__ pmin, double* __restrict__ pmax, double* out_min, double* out_max,
+                       unsigned* done) {
     double lo[D], hi[D];
     double bad = 0;
     for (int t = 0; t < D; ++t) { lo[t] = DBL_MAX; hi[t] = -DBL_MAX; }
@@ -55,42 +71,42 @@ __global__ void bbox_k(const double* __restrict__ p1, int64_t n1, const double* 
         }
         pmax[blockIdx.x * (D + 1) + D] = smax[D][0];
     }
-}
-
-// final single-block reduction of the partials into out_min[D], out_max[D+1]
-template <int D>
-__global__ void bbox_final_k(const double* pmin, const double* pmax, int nb, double* out_min, double* out_max) {
-    __shared__ double smin[D][kGeomThreads], smax[D + 1][kGeomThreads];
-    for (int t = 0; t < D; ++t) { smin[t][threadIdx.x] = DBL_MAX; smax[t][threadIdx.x] = -DBL_MAX; }
-    smax[D][threadIdx.x] = 0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        for (int t = 0; t < D; ++t) {
-            smin[t][threadIdx.x] = fmin(smin[t][threadIdx.x], pmin[b * D + t]);
-            smax[t][threadIdx.x] = fmax(smax[t][threadIdx.x], pmax[b * (D + 1) + t]);
-        }
-        smax[D][threadIdx.x] = fmax(smax[D][threadIdx.x], pmax[b * (D + 1) + D]);
-    }
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
+    if (last_block(done)) {
+        __syncthreads();
+        // the final reduction over the blocks' partials, by this block
+        for (int t = 0; t < D; ++t) { smin[t][threadIdx.x] = DBL_MAX; smax[t][threadIdx.x] = -DBL_MAX; }
+        smax[D][threadIdx.x] = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
             for (int t = 0; t < D; ++t) {
-                smin[t][threadIdx.x] = fmin(smin[t][threadIdx.x], smin[t][threadIdx.x + w]);
-                smax[t][threadIdx.x] = fmax(smax[t][threadIdx.x], smax[t][threadIdx.x + w]);
+                smin[t][threadIdx.x] = fmin(smin[t][threadIdx.x], __ldcg(pmin + b * D + t));
+                smax[t][threadIdx.x] = fmax(smax[t][threadIdx.x], __ldcg(pmax + b * (D + 1) + t));
             }
-            smax[D][threadIdx.x] = fmax(smax[D][threadIdx.x], smax[D][threadIdx.x + w]);
+            smax[D][threadIdx.x] = fmax(smax[D][threadIdx.x], __ldcg(pmax + b * (D + 1) + D));
         }
         __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        for (int t = 0; t < D; ++t) { out_min[t] = smin[t][0]; out_max[t] = smax[t][0]; }
-        out_max[D] = smax[D][0];
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) {
+                for (int t = 0; t < D; ++t) {
+                    smin[t][threadIdx.x] = fmin(smin[t][threadIdx.x], smin[t][threadIdx.x + w]);
+                    smax[t][threadIdx.x] = fmax(smax[t][threadIdx.x], smax[t][threadIdx.x + w]);
+                }
+                smax[D][threadIdx.x] = fmax(smax[D][threadIdx.x], smax[D][threadIdx.x + w]);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            for (int t = 0; t < D; ++t) { out_min[t] = smin[t][0]; out_max[t] = smax[t][0]; }
+            out_max[D] = smax[D][0];
+            *done = 0u;
+        }
     }
 }
 
 // per-block partial max of ||p - c||^2 with c = (min + max)/2 read from device memory
 template <int D>
 __global__ void radius_k(const double* __restrict__ p1, int64_t n1, const double* __restrict__ p2, int64_t n2,
-                         const double* __restrict__ gmin, const double* __restrict__ gmax, double* __restrict__ part) {
+                         const double* __restrict__ gmin, const double* __restrict__ gmax, double* __restrict__ part,
+                         double* out, unsigned* done) {
     double c[D];
     for (int t = 0; t < D; ++t) c[t] = 0.5 * (gmin[t] + gmax[t]);
     double r2 = 0;
@@ -109,19 +125,20 @@ __global__ void radius_k(const double* __restrict__ p1, int64_t n1, const double
         __syncthreads();
     }
     if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
-}
-
-__global__ void max_final_k(const double* part, int nb, double* out) {
-    __shared__ double sm[kGeomThreads];
-    double v = 0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) v = fmax(v, part[b]);
-    sm[threadIdx.x] = v;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + w]);
+    if (last_block(done)) {  // the final reduction, by this block
+        double v = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v = fmax(v, __ldcg(part + b));
+        sm[threadIdx.x] = v;
         __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + w]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            out[0] = sm[0];
+            *done = 0u;
+        }
     }
-    if (threadIdx.x == 0) out[0] = sm[0];
 }
 
 // the caller's point i of the set p1 (n1 points) u p2, row-major
@@ -195,21 +212,19 @@ Geometry compute_geometry(int d, const double* p1, int64_t n1, const double* p2,
     g.d = d;
     const int nb = kGeomBlocks;
     DevBuf<double> pmin(nb * d, s), pmax(nb * (d + 1), s), fin(2 * d + 1 + 1, s), part(nb, s);
+    DevBuf<unsigned> done(2, s);
+    done.zero();
     double* gmin = fin.p;
     double* gmax = fin.p + d;  // d + 1 entries (last = non-finite flag)
-    if (d == 1) { bbox_k<1><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, pmin.p, pmax.p); UOTK_LAUNCHED();
-                  bbox_final_k<1><<<1, kGeomThreads, 0, s>>>(pmin.p, pmax.p, nb, gmin, gmax); UOTK_LAUNCHED(); }
-    else if (d == 2) { bbox_k<2><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, pmin.p, pmax.p); UOTK_LAUNCHED();
-                       bbox_final_k<2><<<1, kGeomThreads, 0, s>>>(pmin.p, pmax.p, nb, gmin, gmax); UOTK_LAUNCHED(); }
-    else { bbox_k<3><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, pmin.p, pmax.p); UOTK_LAUNCHED();
-           bbox_final_k<3><<<1, kGeomThreads, 0, s>>>(pmin.p, pmax.p, nb, gmin, gmax); UOTK_LAUNCHED(); }
+    if (d == 1) bbox_k<1><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, pmin.p, pmax.p, gmin, gmax, done.p);
+    else if (d == 2) bbox_k<2><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, pmin.p, pmax.p, gmin, gmax, done.p);
+    else bbox_k<3><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, pmin.p, pmax.p, gmin, gmax, done.p);
+    UOTK_LAUNCHED();
     if (comm) comm_allreduce_minmax(gmin, d, gmax, d + 1, comm, s);
     double* rfin = fin.p + 2 * d + 1;
-    if (d == 1) radius_k<1><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, gmin, gmax, part.p);
-    else if (d == 2) radius_k<2><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, gmin, gmax, part.p);
-    else radius_k<3><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, gmin, gmax, part.p);
-    UOTK_LAUNCHED();
-    max_final_k<<<1, kGeomThreads, 0, s>>>(part.p, nb, rfin);
+    if (d == 1) radius_k<1><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, gmin, gmax, part.p, rfin, done.p + 1);
+    else if (d == 2) radius_k<2><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, gmin, gmax, part.p, rfin, done.p + 1);
+    else radius_k<3><<<nb, kGeomThreads, 0, s>>>(p1, n1, p2, n2, gmin, gmax, part.p, rfin, done.p + 1);
     UOTK_LAUNCHED();
     if (comm) comm_allreduce_minmax(nullptr, 0, rfin, 1, comm, s);
     double h[2 * kMaxD + 2];
