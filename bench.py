@@ -35,6 +35,7 @@ import json
 import os
 import statistics
 import subprocess
+import threading
 import sys
 import time
 
@@ -146,24 +147,46 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # nvidia-smi is started and has produced its first sample BEFORE the caller's timed
+        # region begins (its start-up — NVML initialisation, a process spawn — otherwise
+        # lands in the first timed step); samples are taken every 200 ms throughout, and
+        # summary() keeps those from start() on
+        self.lines, self.t_start = [], None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+
+        def reader():
+            for ln in self.proc.stdout:
+                if ln.strip():
+                    self.lines.append((time.perf_counter(), ln))
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        t0 = time.perf_counter()
+        while not self.lines and time.perf_counter() - t0 < 3.0 and self.proc.poll() is None:
+            time.sleep(0.01)
         return self
 
+    def start(self):
+        self.t_start = time.perf_counter()
+
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
+            time.sleep(0.25)  # one more sample after the timed region's last kernels
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.thread.join(timeout=5)
+        t = self.t_start or 0.0
+        timed = [ln for ts, ln in self.lines if ts >= t]
+        self.lines = timed or [ln for _, ln in self.lines[-1:]]
 
     def summary(self):
         sm, smax, reasons = [], None, set()
@@ -450,16 +473,21 @@ def main_ours(args):
     def step():
         return uk.uot_sinkhorn(xd, ad, yd, bd, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm)
 
-    for _ in range(args.warmup):
-        beta, gamma, res = step()
-    torch.cuda.synchronize()
-
-    # ---- timed region: K steps, L2 flushed between steps (outside the events)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    uk.reset_launch_counter()
-    barrier()
-    torch.cuda.synchronize()
+    # the clock sampler runs from before the warm-up (its start-up is not in the timed
+    # region, and the GPU does not idle between the warm-up and the timed steps); its
+    # summary keeps the samples taken from clk.start() on
     with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.warmup):
+            beta, gamma, res = step()
+        torch.cuda.synchronize()
+
+        # ---- timed region: K steps, L2 flushed between steps (outside the events)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        uk.reset_launch_counter()
+        barrier()
+        torch.cuda.synchronize()
+        clk.start()
         for k in range(args.steps):
             flush.fill_(float(k))
             ev[k][0].record(stream)
