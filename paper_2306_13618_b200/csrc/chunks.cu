@@ -230,6 +230,7 @@ void chunked_prepare(PointSet& ps, const FastParams& fp, cudaStream_t s, PointUs
     const int n = (int)ps.n;
     trace_mark("chunks: start");
     DevBuf<int32_t> run_key(n, s), run_len(n, s), run_start(n, s), nchunk(n, s), chunk_off(n, s), cnt(3, s);
+    cnt.zero();  // cnt[2] (the hybrid pass's one-cell count) is read back by every encode
     trace_mark("chunks: 6 scratch allocations");
     size_t tmp_bytes = 0, t2 = 0;
     UOTK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, ps.key.p, run_key.p, run_len.p, cnt.p, n, s));
