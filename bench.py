@@ -594,11 +594,11 @@ def _timed_calls(fn, steps, barrier):
     return (time.perf_counter() - t0) / steps, v
 
 
-def _mmd_roofline(uk, fn, n_z):
+def _mmd_roofline(uk, fn, n_z, traffic_key=None):
     """MMD^2 (Fourier-domain form: spread + pruned forward FFT + sum_k D_k |G_k|^2): the
     spread kernel against the FP64 roofline, and its share of the whole call."""
     prof = profiled(uk, fn)
-    return pass_roofline(prof, 3, 8, n_z, 0, traffic_key=None)
+    return pass_roofline(prof, 3, 8, n_z, 0, traffic_key=traffic_key)
 
 
 def mmd_leg(uk, world, rank, comm, dev, barrier, cpu=None):
@@ -616,7 +616,7 @@ def mmd_leg(uk, world, rank, comm, dev, barrier, cpu=None):
     for _ in range(3):
         call()
     dt, v = _timed_calls(call, 10, barrier)
-    roof = _mmd_roofline(uk, call, len(x) + len(y))
+    roof = _mmd_roofline(uk, call, len(x) + len(y), traffic_key="mmd_spread")
     if roof:
         roof["call_ms"] = dt * 1e3
     # cold: every cache released first, so the call also rebuilds the
