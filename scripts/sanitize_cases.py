@@ -76,6 +76,21 @@ def main():
     v = uk.mmd2(t(m.x), t(m.a), t(m.y), t(m.b), "gauss", 0.0025, opts={"method": "nfft", "flags": uk.FLAG_CHUNKED})
     ref = oracle.mmd2_direct(m.x, m.a, m.y, m.b, W.GAUSS, 0.0025)
     print(f"mmd2: {v:.6e} vs {ref:.6e}", flush=True)
+    # late round 2: spread3d_fly_k (windows evaluated in the spread) on one-cell and on
+    # hybrid groups (dense cells alone, sparse cells in 9-cell z-segments)
+    h = W.c2_dense_mmd(n=10000)
+    v, info = uk.mmd2(t(h.x), t(h.a), t(h.y), t(h.b), "gauss", 0.0025, opts={"method": "nfft"}, return_info=True)
+    assert info["groups"][0] == 1624, info
+    ref = oracle.mmd2_direct(h.x, h.a, h.y, h.b, W.GAUSS, 0.0025)
+    assert abs(v - ref) <= 1e-8 * max(abs(ref), 1e-12), (v, ref)
+    print(f"spread3d_fly_k<hybrid> (mmd2): {v:.6e} vs {ref:.6e}", flush=True)
+    f = W.c3_dense_uot(n=20000, m=1001)
+    got, info = uk.kernel_sum(t(f.x), t(f.a), t(f.y), "gauss", 0.02, opts={"method": "nfft"}, return_info=True)
+    assert info["groups"][0] == 16, info
+    ref = oracle.kernel_sum_direct(f.x, f.a, f.y, W.GAUSS, 0.02)
+    err = float(np.max(np.abs(got.cpu().numpy() - ref) / np.abs(ref)))
+    assert err < 1e-9, err
+    print(f"spread3d_fly_k<one-cell> (kernel sum): ok (err {err:.1e})", flush=True)
     uot("direct", W.c1_uot(n=300, m=200), {"method": "direct"})
     uot("deterministic (pull spread)", W.c3_dense_uot(n=900, m=700), {"deterministic": 1})
     print("SANITIZE_CASES_DONE", flush=True)

@@ -119,6 +119,34 @@ def test_stress_spread_gather_rings(uk, d, n, kind, flags):
     assert worst <= 1e-12, worst
 
 
+def test_stress_spread_on_the_fly_and_hybrid(uk):
+    """The late round-2 spread kernels, 40 repetitions each: spread3d_fly_k on hybrid
+    groups (MMD^2 on C2's mixtures at C2-at-1M cell densities, uotk_info.groups 1624) and
+    on one-cell groups (kernel-sum sources at C3 density, groups 16).  Each run must equal
+    the first to the atomic-flush spread, and the first must equal the oracle."""
+    h = W.c2_dense_mmd(n=10000)
+    args = (cuda(h.x), cuda(h.a), cuda(h.y), cuda(h.b), "gauss", 0.0025)
+    v0, info = uk.mmd2(*args, opts={"method": "nfft"}, return_info=True)
+    assert info["groups"][0] == 1624, info
+    ref = oracle.mmd2_direct(h.x, h.a, h.y, h.b, W.GAUSS, 0.0025)
+    # the energy form's cancellation scale: sum of |w_i| |w_j| K over the pairs (bounded by (sum|w|)^2)
+    scale = float((np.sum(np.abs(h.a)) + np.sum(np.abs(h.b))) ** 2)
+    assert abs(v0 - ref) <= 1e-12 * scale, (v0, ref)
+    worst = max(abs(uk.mmd2(*args, opts={"method": "nfft"}) - v0) for _ in range(40))
+    assert worst <= 1e-13 * scale, worst
+    f = W.c3_dense_uot(n=20000, m=1001)
+    src, al, tgt = cuda(f.x), cuda(f.a), cuda(f.y)
+    s0, info = uk.kernel_sum(src, al, tgt, "gauss", 0.02, opts={"method": "nfft"}, return_info=True)
+    assert info["groups"][0] == 16, info
+    ref = oracle.kernel_sum_direct(f.x, f.a, f.y[:200], W.GAUSS, 0.02)
+    assert np.max(np.abs(s0.cpu().numpy()[:200] - ref) / np.abs(ref)) <= 1e-9
+    worst = 0.0
+    for _ in range(40):
+        s = uk.kernel_sum(src, al, tgt, "gauss", 0.02, opts={"method": "nfft"})
+        worst = max(worst, float(torch.max(torch.abs(s - s0) / torch.abs(s0))))
+    assert worst <= 1e-12, worst
+
+
 def test_guard_bands_on_every_kernel_family():
     """UOTK_GUARD=1 (the memcheck substitute): every library buffer carries 64 KB guard
     bands that are checked when it is freed; scripts/sanitize_cases.py launches every
