@@ -98,10 +98,13 @@ def _dim(points, name):
 
 
 def _like(ref, n):
-    """Allocate an output of n doubles like `ref` (CUDA tensor, CPU tensor or numpy)."""
+    """Allocate an output of n doubles like `ref` (CUDA tensor, CPU tensor or numpy); a
+    pinned CPU tensor gets a pinned output, so the library's device->host copy of it runs
+    at full DMA speed instead of through the driver's pageable bounce buffer."""
     torch = _torch()
     if ref.is_torch:
-        return torch.empty(n, dtype=torch.float64, device=ref.obj.device)
+        pin = ref.obj.device.type == "cpu" and ref.obj.is_pinned()
+        return torch.empty(n, dtype=torch.float64, device=ref.obj.device, pin_memory=pin)
     return np.empty(n, dtype=np.float64)
 
 
