@@ -559,8 +559,12 @@ def e2e_leg(uk, pr, x, a, y, b, comm, barrier, world, dev):
     hx, ha, hy, hb = (torch.from_numpy(v).pin_memory() for v in (x, a, y, b))
     opts = {"method": "nfft"}
     stream = torch.cuda.current_stream()
-    uk.uot_sinkhorn(hx, ha, hy, hb, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm, stream=stream)
     steps = 2
+    # warm-up in the timed loop's own pattern (each call's outputs alive while the next one
+    # allocates), so the pinned host allocator already holds the output blocks it recycles
+    for _ in range(steps):
+        beta, gamma, res = uk.uot_sinkhorn(hx, ha, hy, hb, pr.eps, pr.lam, iters=pr.iters, opts=opts, comm=comm,
+                                           stream=stream)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
