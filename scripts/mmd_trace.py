@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 import paper_2306_13618_b200 as uk  # noqa: E402
 import workloads as W  # noqa: E402
 
-pr = W.c2_mmd(n=1_000_000)
+pr = W.c2_mmd(n=int(os.environ.get("MMD_N", "1000000")))
 x, a, y, b = (torch.from_numpy(v).cuda() for v in (pr.x, pr.a, pr.y, pr.b))
 for _ in range(3):
     uk.mmd2(x, a, y, b, "gauss", 0.0025, opts={"method": "nfft"})
