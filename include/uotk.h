@@ -10,8 +10,10 @@
  * by NFFT-based fast summation (Sec. 4; factorisation (4.5)-(4.6),
  * P:590-592) or by a direct O(n m) sum (Eq. 4.3), and uses it inside the
  * entropic unbalanced-OT Sinkhorn iteration (Algorithm 2) and the
- * MMD^2 sums (Eq. 3.5).  Every step runs in hand-written sm_100a kernels;
- * cuFFT provides the equispaced FFT of (4.6).
+ * MMD^2 sums (Eq. 3.5).  Every step runs in hand-written sm_100a kernels
+ * except two library calls: cuFFT provides the equispaced FFT of (4.6) where the
+ * cuFFT chain is chosen, and CUB provides the radix sort of the points by cell and
+ * the run-length encode / scans of the chunk layout (setup, once per call).
  *
  * Conventions shared by all entry points
  * --------------------------------------
