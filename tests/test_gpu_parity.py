@@ -885,3 +885,24 @@ def test_kernel_sum_d2_y_segments(uk, kind):
                               opts={"method": "nfft", "flags": uk.FLAG_CHUNKED}, return_info=True)
     assert info["groups"][0] == 24, info
     assert rel_err(got.cpu().numpy(), ref, True) <= 1e-9
+
+
+def test_pinned_host_inputs_give_pinned_outputs(uk):
+    """Host (pinned CPU tensor) inputs: the library stages the copies itself and the binding
+    returns pinned CPU outputs (so the device->host copy runs at DMA speed); the values equal
+    the oracle and the device-resident call's."""
+    pr = W.random_sum(3, 3001, 1999, kind=W.GAUSS, param=0.0025, seed=21)
+    host = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for v in (pr.src, pr.alpha, pr.tgt)]
+    got = uk.kernel_sum(*host, "gauss", 0.0025, opts={"method": "nfft"})
+    assert got.device.type == "cpu" and got.is_pinned()
+    ref = oracle.kernel_sum_direct(pr.src, pr.alpha, pr.tgt, W.GAUSS, 0.0025)
+    assert rel_err(got.numpy(), ref, False) <= 1e-9
+    dev = uk.kernel_sum(*(h.cuda() for h in host), "gauss", 0.0025, opts={"method": "nfft"})
+    assert rel_err(got.numpy(), dev.cpu().numpy(), False) <= 1e-13
+    u = W.c1_uot(n=700, m=500)
+    hu = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for v in (u.x, u.a, u.y, u.b)]
+    beta, gamma, res = uk.uot_sinkhorn(*hu, u.eps, u.lam, iters=5, opts={"method": "nfft"})
+    assert beta.is_pinned() and gamma.is_pinned()
+    bd, gd, _ = uk.uot_sinkhorn(*(h.cuda() for h in hu), u.eps, u.lam, iters=5, opts={"method": "nfft"})
+    assert np.max(np.abs(beta.numpy() - bd.cpu().numpy())) <= 1e-12 * np.max(np.abs(bd.cpu().numpy()))
+    assert np.max(np.abs(gamma.numpy() - gd.cpu().numpy())) <= 1e-12 * np.max(np.abs(gd.cpu().numpy()))
